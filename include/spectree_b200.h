@@ -1,0 +1,163 @@
+/*
+ * spectree_b200 -- C ABI of the B200-native classification-tree evaluator.
+ *
+ * This is the drop-in boundary for the reference's evaluate API
+ * (/root/reference/proj/core).  Every entry point is plain C: pointers, sizes
+ * and POD structs, no C++ or torch types.  The reference-side binding a
+ * maintainer adds is in INTEGRATION.md; the C++ wrapper that mirrors the
+ * reference signatures exactly is include/spectree_b200.hpp.
+ *
+ * Semantics are the reference's, bit for bit:
+ *   successor(i, x) = child(i) + (uint32)(x[attr(i)] > thr(i))    tree.hpp:51-54
+ *   walk from node 0 until class_id != ST_NO_CLASS                 eval_serial.cpp:21-29
+ *   one uint32 label per record, positional                        dataset.hpp:35-36
+ * (ordered IEEE '>' without flush-to-zero: ties and NaN go left.)
+ *
+ * Return codes mirror the reference error taxonomy / CLI exit codes
+ * (errors.hpp:12-46, main.cpp:703-712):
+ *   0 ok, 2 argument (ArgumentError), 3 io/parse, 4 CUDA failure,
+ *   5 no CUDA device.  There is NO CPU fallback: without a usable device
+ *   every evaluating call returns 5.
+ * st_last_error() returns the thread-local message of the last failure.
+ *
+ * Thread safety: trees/forests are immutable after creation and may be shared
+ * by concurrent callers (device replicas are created lazily under a lock),
+ * like the reference's pure evaluators.
+ */
+#ifndef SPECTREE_B200_H
+#define SPECTREE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ST_NO_CLASS 0xFFFFFFFFu /* spectree::kNoClass, tree.hpp:15-16 */
+
+/* Layout-identical to spectree::EncodedNode (tree.hpp:43-55), 16 bytes:
+ * {u32 attribute @0, f32 threshold @4, u32 child @8, u32 class_id @12}. */
+typedef struct st_node {
+  uint32_t attribute;
+  float threshold;
+  uint32_t child;
+  uint32_t class_id;
+} st_node;
+
+enum st_status {
+  ST_OK = 0,
+  ST_ERR_ARGUMENT = 2,
+  ST_ERR_IO = 3,
+  ST_ERR_CUDA = 4,
+  ST_ERR_NO_DEVICE = 5
+};
+
+/* Feature matrix layout.  AoS = the reference Dataset (row-major, record(i) =
+ * values + i*ld, dataset.hpp:20-22).  SoA = attribute-major, x[a*ld + r]. */
+enum st_layout { ST_LAYOUT_AOS = 0, ST_LAYOUT_SOA = 1 };
+
+/* Algorithm 1 = data decomposition (eval_data_parallel.cpp:35-88),
+ * Algorithm 2 = speculative decomposition (eval_speculative.cpp:207-273). */
+enum st_algo { ST_ALGO_AUTO = 0, ST_ALGO_DATA = 1, ST_ALGO_SPECULATIVE = 2 };
+
+/* Where the data kernel reads the node array from. */
+enum st_tree_loc {
+  ST_TREE_AUTO = 0,
+  ST_TREE_SHARED = 1,   /* staged once per CTA into shared memory */
+  ST_TREE_CONSTANT = 2, /* __grid_constant__ kernel parameter (constant bank), N <= 4064 */
+  ST_TREE_GLOBAL = 3    /* read-only global path (L1/L2), any size */
+};
+
+/* GPU geometry.  Zero-initialise for defaults (st_geom_default). */
+typedef struct st_geom {
+  uint32_t algo;               /* st_algo */
+  uint32_t tree_loc;           /* st_tree_loc (data kernel) */
+  uint32_t samples_per_thread; /* data kernel: independent walks per lane (0 = auto) */
+  uint32_t group_lanes;        /* speculative: lanes per record group, power of two <= 32 (0 = auto) */
+  uint32_t window_levels;      /* speculative: max window height in tree levels (0 = auto) */
+  uint32_t reductions;         /* speculative: 0 = fixed per-window doubling count;
+                                  k >= 1 = check the root after every k doublings
+                                  (reference ReductionMode::barrier_separated, k = reductions_per_iteration) */
+  uint32_t blocks_per_sm;      /* 0 = occupancy-derived persistent grid */
+  uint32_t reserved[5];
+} st_geom;
+
+/* Optional per-record speculative counters (SpeculativeStats,
+ * eval_speculative.hpp:73-77).  Arrays of m uint32, in the same memory space
+ * as the labels of the call they are passed to. */
+typedef struct st_stats {
+  uint32_t* iterations;     /* reduction-loop trips (summed over windows) */
+  uint32_t* doubling_steps; /* pointer-jumping steps applied */
+} st_stats;
+
+typedef struct st_tree_info {
+  uint32_t nodes, leaves, internal, depth, max_attribute;
+  uint32_t compact;        /* 1 if the 8-byte device node format applies */
+  uint32_t spec_windows;   /* speculative windows for the default geometry */
+  uint32_t spec_group_lanes;
+} st_tree_info;
+
+typedef struct st_tree st_tree;
+typedef struct st_forest st_forest;
+
+const char* st_last_error(void);
+const char* st_version(void);
+int st_device_count(int* count);
+void st_geom_default(st_geom* g);
+
+/* Tree-load boundary: replaces constructing spectree::EncodedTree for the GPU
+ * (tree.hpp:61-92, EncodedTree ctor tree.cpp:35-61).  Rejects, with
+ * ST_ERR_ARGUMENT, n == 0 and any internal node whose child link is not
+ * strictly forward or whose right child is out of range (the subset of
+ * validate(), tree.cpp:138-189, that a walk needs to terminate in bounds). */
+int st_tree_create(const st_node* nodes, uint32_t n, st_tree** out);
+void st_tree_destroy(st_tree* tree);
+int st_tree_get_info(const st_tree* tree, st_tree_info* out);
+
+/* Random forest: t trees, per-sample majority vote over their labels, smallest
+ * class id on ties.  Every leaf class must be < n_classes (<= 64). */
+int st_forest_create(const st_node* const* trees, const uint32_t* sizes, uint32_t t,
+                     uint32_t n_classes, st_forest** out);
+void st_forest_destroy(st_forest* forest);
+
+/* Host-buffer evaluation ("outer" window of bench.cpp:267-296): copies the
+ * records in, runs the kernel on the current CUDA device, copies labels out;
+ * chunked and double-buffered over two streams.  x is m records of arity a
+ * (AoS: ld >= a floats between records; SoA: ld >= m floats between
+ * attributes; ld = 0 means packed).  labels: m uint32.  Throws the
+ * reference's ArgumentError (code 2) before any work when
+ * max_attribute >= a (check_attribute_range, eval_serial.cpp:10-17).
+ * m == 0 returns immediately with no launch. */
+int st_eval(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+            int layout, const st_geom* geom, uint32_t* labels, st_stats* stats);
+
+/* Device-resident evaluation ("inner" window): x and labels are device
+ * pointers on the current device, enqueued on `stream` (a cudaStream_t, NULL =
+ * legacy default stream).  Asynchronous: no host synchronisation. */
+int st_eval_device(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                   int layout, const st_geom* geom, uint32_t* labels, st_stats* stats,
+                   void* stream);
+
+/* Sample-sharded evaluation over several devices of one box: device k owns
+ * records [floor(k*m/n), floor((k+1)*m/n)) (the Proc. 3 range rule,
+ * eval_data_parallel.cpp:47-51); the tree is replicated, labels are gathered
+ * into disjoint slices of `labels`.  No collective in the hot loop. */
+int st_eval_sharded(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                    int layout, const st_geom* geom, const int* devices, int ndev,
+                    uint32_t* labels);
+
+int st_forest_eval(const st_forest* forest, const float* x, uint64_t m, uint32_t a,
+                   uint64_t ld, int layout, uint32_t* labels);
+int st_forest_eval_device(const st_forest* forest, const float* x, uint64_t m, uint32_t a,
+                          uint64_t ld, int layout, uint32_t* labels, void* stream);
+
+/* Number of kernel launches the last successful evaluating call on this
+ * thread enqueued (for bench.py's gpu_launches claim). */
+uint32_t st_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPECTREE_B200_H */

@@ -1,0 +1,1077 @@
+// C-ABI implementation of include/spectree_b200.h.
+//
+// Host-side responsibilities (native C++, no Python on the path):
+//   * tree preprocessing: validation (subset of tree.cpp:138-189), the compact
+//     8-byte node format for the data kernel, the speculative window tables
+//     (the paper's proposed level windows);
+//   * lazy per-device replicas of every tree/forest (tree replicated to each
+//     GPU);
+//   * dispatch to the sm_100a kernels in st_kernels.cuh with an
+//     occupancy-derived persistent grid;
+//   * the host-buffer path (chunked H2D / kernel / D2H over two streams) and
+//     the sample-sharded multi-GPU driver.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "../../include/spectree_b200.h"
+#include "st_kernels.cuh"
+
+using namespace stk;
+
+static_assert(sizeof(st_node) == 16, "st_node must match spectree::EncodedNode");
+static_assert(offsetof(st_node, attribute) == 0 && offsetof(st_node, threshold) == 4 &&
+                  offsetof(st_node, child) == 8 && offsetof(st_node, class_id) == 12,
+              "st_node field offsets must match spectree::EncodedNode");
+
+namespace {
+
+thread_local std::string g_error;
+thread_local uint32_t g_launches = 0;
+
+struct StError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, std::string msg) { throw StError{code, std::move(msg)}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
+      fail(ST_ERR_NO_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(ST_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_error.clear();
+    return ST_OK;
+  } catch (const StError& e) {
+    g_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return ST_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return ST_ERR_CUDA;
+  }
+}
+
+uint32_t ceil_log2(uint32_t v) {
+  uint32_t s = 0, reach = 1;
+  while (reach < v) {
+    reach *= 2;
+    ++s;
+  }
+  return s;
+}
+
+int current_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) fail(ST_ERR_NO_DEVICE, "no CUDA device available (no CPU fallback)");
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  return d;
+}
+
+struct DevProps {
+  int sms = 0;
+  size_t smem_optin = 0;
+};
+DevProps dev_props(int dev) {
+  static std::mutex mu;
+  static std::map<int, DevProps> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  DevProps p;
+  int v = 0;
+  CK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+  p.sms = v;
+  CK(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  p.smem_optin = (size_t)v;
+  cache[dev] = p;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// Speculative windows
+// ---------------------------------------------------------------------------
+struct WinTable {
+  std::vector<SEntry> entries;  // padded by 32 entries
+  uint32_t root_code = 0;
+  uint32_t windows = 0;
+  uint32_t max_steps = 0;
+};
+
+}  // namespace
+
+struct st_tree {
+  std::vector<st_node> nodes;
+  st_tree_info info{};
+  uint32_t abits = 1;
+  bool compact_ok = true;
+  bool leaf_table = false;            // some class >= 2^31: leaves carry ordinals
+  std::vector<uint32_t> leaf_classes;  // ordinal -> class
+  std::vector<uint32_t> leaf_code;     // node -> code payload (class or ordinal)
+  std::vector<CNode> compact;
+
+  std::mutex mu;
+  std::map<std::pair<uint32_t, uint32_t>, std::shared_ptr<WinTable>> wins;  // (G, H)
+  struct Dev {
+    CNode* compact = nullptr;
+    uint4* wide = nullptr;
+    uint32_t* leaf_tbl = nullptr;
+    std::map<std::pair<uint32_t, uint32_t>, SEntry*> wins;
+  };
+  std::map<int, Dev> dev;
+
+  ~st_tree() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    for (auto& kv : dev) {
+      if (cudaSetDevice(kv.first) != cudaSuccess) continue;
+      cudaFree(kv.second.compact);
+      cudaFree(kv.second.wide);
+      cudaFree(kv.second.leaf_tbl);
+      for (auto& w : kv.second.wins) cudaFree(w.second);
+    }
+    if (cur >= 0) cudaSetDevice(cur);
+  }
+
+  bool is_leaf(uint32_t i) const { return nodes[i].class_id != ST_NO_CLASS; }
+
+  std::shared_ptr<WinTable> windows(uint32_t G, uint32_t H) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(G, H);
+    auto it = wins.find(key);
+    if (it != wins.end()) return it->second;
+    auto w = std::make_shared<WinTable>(build_windows(G, H));
+    wins[key] = w;
+    return w;
+  }
+
+  // Partition the internal nodes into windows of <= G nodes and <= H levels,
+  // breadth-first from each window root.  Lane j of a window holds its j-th
+  // member (for a tree with I <= G internal nodes and H >= depth this is the
+  // reference's processor_node_map, tree.cpp:204-209).
+  WinTable build_windows(uint32_t G, uint32_t H) const {
+    WinTable wt;
+    const uint32_t n = (uint32_t)nodes.size();
+    if (is_leaf(0)) {
+      wt.root_code = kLeafBit | leaf_code[0];
+      wt.entries.assign(32, SEntry{0.0f, 0u, 0u, 0u});
+      return wt;
+    }
+    std::vector<int32_t> win_of_root(n, -1);
+    std::vector<std::vector<uint32_t>> members;
+    std::vector<std::vector<uint32_t>> ldepth;
+    std::deque<uint32_t> roots;
+    win_of_root[0] = 0;
+    members.emplace_back();
+    ldepth.emplace_back();
+    roots.push_back(0);
+    while (!roots.empty()) {
+      const uint32_t root = roots.front();
+      roots.pop_front();
+      const int32_t w = win_of_root[root];
+      std::vector<uint32_t> mem, dep;
+      std::deque<std::pair<uint32_t, uint32_t>> q;
+      q.emplace_back(root, 0);
+      std::vector<std::pair<uint32_t, uint32_t>> exits;
+      std::vector<uint32_t> seen;  // DAG-shaped inputs may reach a node twice
+      while (!q.empty()) {
+        auto [u, d] = q.front();
+        q.pop_front();
+        if (std::find(seen.begin(), seen.end(), u) != seen.end()) continue;
+        seen.push_back(u);
+        if (mem.size() >= G || d >= H) {
+          exits.emplace_back(u, d);
+          continue;
+        }
+        mem.push_back(u);
+        dep.push_back(d);
+        for (uint32_t c : {nodes[u].child, nodes[u].child + 1})
+          if (!is_leaf(c)) q.emplace_back(c, d + 1);
+      }
+      for (auto [u, d] : exits) {
+        (void)d;
+        if (win_of_root[u] < 0) {
+          win_of_root[u] = (int32_t)members.size();
+          members.emplace_back();
+          ldepth.emplace_back();
+          roots.push_back(u);
+        }
+      }
+      members[w] = std::move(mem);
+      ldepth[w] = std::move(dep);
+    }
+    const uint32_t nw = (uint32_t)members.size();
+    std::vector<uint32_t> base(nw);
+    uint64_t total = 0;
+    for (uint32_t w = 0; w < nw; ++w) {
+      base[w] = (uint32_t)total;
+      total += members[w].size();
+    }
+    if (total + 32 >= (1u << 30)) fail(ST_ERR_ARGUMENT, "tree too large for speculative windows");
+    wt.entries.resize(total + 32, SEntry{0.0f, 0u, 0u, 0u});
+    std::vector<int32_t> lane_of(n, -1);
+    for (uint32_t w = 0; w < nw; ++w) {
+      const auto& mem = members[w];
+      uint32_t h = 0;
+      for (uint32_t j = 0; j < mem.size(); ++j) {
+        lane_of[mem[j]] = (int32_t)j;
+        h = std::max(h, ldepth[w][j] + 1);
+      }
+      const uint32_t steps = ceil_log2(h);
+      wt.max_steps = std::max(wt.max_steps, steps);
+      auto code = [&](uint32_t c) -> uint32_t {
+        if (is_leaf(c)) return kLeafBit | leaf_code[c];
+        if (lane_of[c] >= 0) return (uint32_t)lane_of[c];
+        return kExitBit | base[win_of_root[c]];
+      };
+      for (uint32_t j = 0; j < mem.size(); ++j) {
+        const st_node& nd = nodes[mem[j]];
+        SEntry e;
+        e.thr = nd.threshold;
+        e.attr_steps = nd.attribute | (steps << 24);
+        e.left = code(nd.child);
+        e.right = code(nd.child + 1);
+        wt.entries[base[w] + j] = e;
+      }
+      for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = -1;
+    }
+    wt.root_code = kExitBit | 0u;
+    wt.windows = nw;
+    return wt;
+  }
+
+  Dev& device(int d) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = dev.find(d);
+    if (it != dev.end()) return it->second;
+    Dev dv;
+    CK(cudaMalloc(&dv.wide, nodes.size() * sizeof(st_node)));
+    CK(cudaMemcpy(dv.wide, nodes.data(), nodes.size() * sizeof(st_node), cudaMemcpyHostToDevice));
+    if (compact_ok) {
+      const size_t bytes = ((compact.size() * sizeof(CNode) + 15) & ~size_t(15)) + 16;
+      CK(cudaMalloc(&dv.compact, bytes));
+      CK(cudaMemset(dv.compact, 0, bytes));
+      CK(cudaMemcpy(dv.compact, compact.data(), compact.size() * sizeof(CNode),
+                    cudaMemcpyHostToDevice));
+    }
+    if (leaf_table) {
+      CK(cudaMalloc(&dv.leaf_tbl, leaf_classes.size() * 4));
+      CK(cudaMemcpy(dv.leaf_tbl, leaf_classes.data(), leaf_classes.size() * 4,
+                    cudaMemcpyHostToDevice));
+    }
+    return dev.emplace(d, dv).first->second;
+  }
+
+  SEntry* device_windows(int d, uint32_t G, uint32_t H, const WinTable& wt) {
+    Dev& dv = device(d);
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(G, H);
+    auto it = dv.wins.find(key);
+    if (it != dv.wins.end()) return it->second;
+    SEntry* p = nullptr;
+    CK(cudaMalloc(&p, wt.entries.size() * sizeof(SEntry)));
+    CK(cudaMemcpy(p, wt.entries.data(), wt.entries.size() * sizeof(SEntry), cudaMemcpyHostToDevice));
+    dv.wins[key] = p;
+    return p;
+  }
+};
+
+struct st_forest {
+  std::vector<CNode> compact;
+  std::vector<uint32_t> offsets;
+  uint32_t t_count = 0, n_classes = 0, abits = 1, max_attribute = 0;
+  std::mutex mu;
+  struct Dev {
+    CNode* nodes = nullptr;
+    uint32_t* offsets = nullptr;
+  };
+  std::map<int, Dev> dev;
+  ~st_forest() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    for (auto& kv : dev) {
+      if (cudaSetDevice(kv.first) != cudaSuccess) continue;
+      cudaFree(kv.second.nodes);
+      cudaFree(kv.second.offsets);
+    }
+    if (cur >= 0) cudaSetDevice(cur);
+  }
+  Dev& device(int d) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = dev.find(d);
+    if (it != dev.end()) return it->second;
+    Dev dv;
+    CK(cudaMalloc(&dv.nodes, compact.size() * sizeof(CNode) + 16));
+    CK(cudaMemcpy(dv.nodes, compact.data(), compact.size() * sizeof(CNode), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&dv.offsets, offsets.size() * 4));
+    CK(cudaMemcpy(dv.offsets, offsets.data(), offsets.size() * 4, cudaMemcpyHostToDevice));
+    return dev.emplace(d, dv).first->second;
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Tree construction
+// ---------------------------------------------------------------------------
+void validate_links(const st_node* nodes, uint32_t n, const char* what) {
+  if (n == 0) fail(ST_ERR_ARGUMENT, "encoded tree requires at least one node");
+  for (uint32_t i = 0; i < n; ++i) {
+    const st_node& nd = nodes[i];
+    if (nd.class_id != ST_NO_CLASS) continue;
+    if (nd.child + 1 >= n || nd.child + 1 < nd.child)
+      fail(ST_ERR_ARGUMENT, std::string(what) + ": node " + std::to_string(i) + ": child index " +
+                                std::to_string(nd.child) + " out of range");
+    if (nd.child <= i)
+      fail(ST_ERR_ARGUMENT, std::string(what) + ": node " + std::to_string(i) +
+                                ": non-BFS child link: child " + std::to_string(nd.child) +
+                                " does not point forward");
+  }
+}
+
+uint32_t bits_for(uint32_t v) {  // bits to hold values 0..v
+  uint32_t b = 1;
+  while (b < 32 && (v >> b) != 0) ++b;
+  return b;
+}
+
+std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
+  validate_links(nodes, n, "tree");
+  auto t = std::make_unique<st_tree>();
+  t->nodes.assign(nodes, nodes + n);
+  st_tree_info& in = t->info;
+  in.nodes = n;
+  std::vector<uint32_t> depth(n, 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    const st_node& nd = nodes[i];
+    in.max_attribute = std::max(in.max_attribute, nd.attribute);  // tree.cpp:47: all nodes
+    if (nd.class_id != ST_NO_CLASS) {
+      ++in.leaves;
+      in.depth = std::max(in.depth, depth[i]);
+      if (nd.class_id >= kLeafBit) t->leaf_table = true;
+    } else {
+      ++in.internal;
+      depth[nd.child] = std::max(depth[nd.child], depth[i] + 1);
+      depth[nd.child + 1] = std::max(depth[nd.child + 1], depth[i] + 1);
+    }
+  }
+  t->leaf_code.assign(n, 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (nodes[i].class_id == ST_NO_CLASS) continue;
+    if (t->leaf_table) {
+      t->leaf_code[i] = (uint32_t)t->leaf_classes.size();
+      t->leaf_classes.push_back(nodes[i].class_id);
+    } else {
+      t->leaf_code[i] = nodes[i].class_id;
+    }
+  }
+  t->abits = bits_for(in.max_attribute);
+  t->compact_ok = t->abits < 31 && ((uint64_t)n << t->abits) < (1ull << 31);
+  if (t->compact_ok) {
+    t->compact.resize(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      const st_node& nd = nodes[i];
+      if (nd.class_id != ST_NO_CLASS)
+        t->compact[i] = CNode{nd.threshold, kLeafBit | t->leaf_code[i]};
+      else
+        t->compact[i] = CNode{nd.threshold, (nd.child << t->abits) | nd.attribute};
+    }
+  }
+  in.compact = t->compact_ok ? 1 : 0;
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// Launch helpers
+// ---------------------------------------------------------------------------
+struct Launch {
+  const void* fn;
+  size_t smem;
+};
+
+int blocks_for(const void* fn, size_t smem, int dev, uint32_t blocks_per_sm, uint64_t n_tiles) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, size_t, int>, int> occ_cache;
+  const DevProps pr = dev_props(dev);
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(fn, smem, dev);
+    auto it = occ_cache.find(key);
+    if (it != occ_cache.end()) {
+      occ = it->second;
+    } else {
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarpsPerCta * 32, smem));
+      if (occ < 1) fail(ST_ERR_ARGUMENT, "kernel configuration does not fit on an SM");
+      occ_cache[key] = occ;
+    }
+  }
+  uint64_t blocks = (uint64_t)pr.sms * (blocks_per_sm ? std::min<uint32_t>(blocks_per_sm, occ) : occ);
+  const uint64_t need = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+  return (int)std::max<uint64_t>(1, std::min(blocks, need));
+}
+
+void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(ST_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  ++g_launches;
+}
+
+void check_common(uint64_t m, uint32_t a, uint64_t& ld, int layout, uint32_t max_attribute) {
+  if (a == 0) fail(ST_ERR_ARGUMENT, "dataset arity must be >= 1");
+  if (layout != ST_LAYOUT_AOS && layout != ST_LAYOUT_SOA) fail(ST_ERR_ARGUMENT, "unknown layout");
+  if (ld == 0) ld = layout == ST_LAYOUT_AOS ? a : m;
+  if (layout == ST_LAYOUT_AOS && ld < a) fail(ST_ERR_ARGUMENT, "AoS ld must be >= arity");
+  if (layout == ST_LAYOUT_SOA && ld < m) fail(ST_ERR_ARGUMENT, "SoA ld must be >= record count");
+  if (ld > 0xFFFFFFFFull) fail(ST_ERR_ARGUMENT, "ld too large");
+  // check_attribute_range (eval_serial.cpp:10-17), before any work
+  if (max_attribute >= a)
+    fail(ST_ERR_ARGUMENT, "tree reads attribute " + std::to_string(max_attribute) +
+                              " but records have arity " + std::to_string(a));
+}
+
+// ---- data kernel dispatch ------------------------------------------------
+template <int A, int S, int TLOC, int LOADER, int CAP>
+void launch_data_t(const DataArgs& d, const ConstTree<CAP>* ct, size_t smem, int dev,
+                   uint32_t bps, cudaStream_t s) {
+  auto fn = k_data<A, S, TLOC, LOADER, CAP>;
+  const uint64_t n_tiles = (d.m + 32 * S - 1) / (32 * S);
+  const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles);
+  static const ConstTree<1> dummy{};
+  if constexpr (CAP == 1) {
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(d, ct ? *ct : dummy);
+  } else {
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(d, *ct);
+  }
+  check_launch();
+}
+
+template <int A, int S, int LOADER>
+void launch_data_tloc(int tloc, const DataArgs& d, const st_tree* t, size_t smem, int dev,
+                      uint32_t bps, cudaStream_t s) {
+  switch (tloc) {
+    case ST_TREE_SHARED:
+      return launch_data_t<A, S, kShared, LOADER, 1>(d, nullptr, smem, dev, bps, s);
+    case ST_TREE_GLOBAL:
+      return launch_data_t<A, S, kGlobal, LOADER, 1>(d, nullptr, smem, dev, bps, s);
+    case ST_TREE_CONSTANT: {
+      if constexpr (LOADER == kVec) {
+        if (t->compact.size() <= 512) {
+          ConstTree<512> ct{};
+          std::copy(t->compact.begin(), t->compact.end(), ct.n);
+          return launch_data_t<A, S, kConst, LOADER, 512>(d, &ct, smem, dev, bps, s);
+        }
+        auto ct = std::make_unique<ConstTree<4064>>();
+        std::copy(t->compact.begin(), t->compact.end(), ct->n);
+        return launch_data_t<A, S, kConst, LOADER, 4064>(d, ct.get(), smem, dev, bps, s);
+      }
+      break;
+    }
+    default:
+      break;
+  }
+  return launch_data_t<A, S, kWide, LOADER, 1>(d, nullptr, smem, dev, bps, s);
+}
+
+template <int A, int LOADER>
+void launch_data_s(uint32_t S, int tloc, const DataArgs& d, const st_tree* t, size_t smem,
+                   int dev, uint32_t bps, cudaStream_t s) {
+  if constexpr (A == 8 || A == 16) {
+    if (S >= 4) return launch_data_tloc<A, 4, LOADER>(tloc, d, t, smem, dev, bps, s);
+    if (S == 2) return launch_data_tloc<A, 2, LOADER>(tloc, d, t, smem, dev, bps, s);
+  } else if constexpr (A == 19 || A == 32) {
+    if (S >= 2) return launch_data_tloc<A, 2, LOADER>(tloc, d, t, smem, dev, bps, s);
+  }
+  return launch_data_tloc<A, 1, LOADER>(tloc, d, t, smem, dev, bps, s);
+}
+
+uint32_t supported_S(uint32_t a, uint32_t want, bool vec) {
+  if (!vec) return 1;
+  uint32_t maxS = (a == 8 || a == 16) ? 4 : (a == 19 || a == 32) ? 2 : 1;
+  if (want == 0) want = a <= 8 ? 4 : a <= 16 ? 2 : 1;
+  uint32_t S = 1;
+  while (S * 2 <= std::min(want, maxS)) S *= 2;
+  return S;
+}
+
+bool vec_arity(uint32_t a) { return a == 8 || a == 16 || a == 19 || a == 32 || a == 64; }
+
+uint32_t pitch_rt(uint32_t a, bool vec) {
+  if (vec) {
+    if ((a & (a - 1)) == 0 || a % 32 == 0) return a;
+    return (a & 1) ? a : a + 1;
+  }
+  return a | 1u;
+}
+
+void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+                      const st_geom& g, uint32_t* labels, cudaStream_t s, int dev) {
+  st_tree::Dev& dv = t->device(dev);
+  const DevProps pr = dev_props(dev);
+  DataArgs d{};
+  d.x = x;
+  d.m = m;
+  d.a = a;
+  d.ld = (uint32_t)ld;
+  d.nodes = dv.compact;
+  d.wide = dv.wide;
+  d.n_nodes = (uint32_t)t->nodes.size();
+  d.abits = t->abits;
+  d.leaf_class = dv.leaf_tbl;
+  d.labels = labels;
+
+  const bool vec = layout == ST_LAYOUT_AOS && ld == a && vec_arity(a) &&
+                   (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+  int loader = layout == ST_LAYOUT_SOA ? kSoa : vec ? kVec : kScalar;
+  const uint32_t S = supported_S(a, g.samples_per_thread, loader == kVec);
+  const uint32_t p = pitch_rt(a, loader == kVec);
+  size_t tile_bytes = (size_t)kWarpsPerCta * 32 * S * p * 4;
+  const size_t tree_bytes = ((t->nodes.size() * sizeof(CNode) + 15) & ~size_t(15));
+  int tloc = g.tree_loc;
+  if (!t->compact_ok) tloc = ST_TREE_GLOBAL + 1;  // wide
+  else if (tloc == ST_TREE_AUTO)
+    tloc = tree_bytes + tile_bytes <= std::min<size_t>(pr.smem_optin, 200 * 1024) ? ST_TREE_SHARED
+                                                                                 : ST_TREE_GLOBAL;
+  if (tloc == ST_TREE_CONSTANT && (loader != kVec || t->compact.size() > 4064)) tloc = ST_TREE_GLOBAL;
+  if (tloc == ST_TREE_SHARED && tree_bytes + tile_bytes > pr.smem_optin) tloc = ST_TREE_GLOBAL;
+  if (tloc != ST_TREE_SHARED && tile_bytes > pr.smem_optin) {
+    loader = kDirect;
+    tile_bytes = 0;
+  }
+  const size_t smem = (tloc == ST_TREE_SHARED ? tree_bytes : 0) + (loader == kDirect ? 0 : tile_bytes);
+  const uint32_t bps = g.blocks_per_sm;
+  if (loader == kVec) {
+    switch (a) {
+      case 8: return launch_data_s<8, kVec>(S, tloc, d, t, smem, dev, bps, s);
+      case 16: return launch_data_s<16, kVec>(S, tloc, d, t, smem, dev, bps, s);
+      case 19: return launch_data_s<19, kVec>(S, tloc, d, t, smem, dev, bps, s);
+      case 32: return launch_data_s<32, kVec>(S, tloc, d, t, smem, dev, bps, s);
+      case 64: return launch_data_s<64, kVec>(S, tloc, d, t, smem, dev, bps, s);
+    }
+  }
+  if (tloc == ST_TREE_CONSTANT) tloc = ST_TREE_GLOBAL;
+  switch (loader) {
+    case kSoa: return launch_data_tloc<0, 1, kSoa>(tloc, d, t, smem, dev, bps, s);
+    case kDirect: return launch_data_tloc<0, 1, kDirect>(tloc, d, t, smem, dev, bps, s);
+    default: return launch_data_tloc<0, 1, kScalar>(tloc, d, t, smem, dev, bps, s);
+  }
+}
+
+// ---- speculative kernel dispatch -----------------------------------------
+template <int A, int LOADER>
+void launch_spec_t(bool win_shared, const SpecArgs& sa, size_t smem, int dev, uint32_t bps,
+                   cudaStream_t s) {
+  const uint64_t n_tiles = (sa.m + 31) / 32;
+  if (win_shared) {
+    auto fn = k_spec<A, LOADER, true>;
+    const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles);
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(sa);
+  } else {
+    auto fn = k_spec<A, LOADER, false>;
+    const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles);
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(sa);
+  }
+  check_launch();
+}
+
+void spec_geometry(const st_tree* t, const st_geom& g, uint32_t& G, uint32_t& H) {
+  G = g.group_lanes;
+  if (G == 0) {
+    G = 16;  // the paper's half-warp record group
+    const uint32_t I = std::max<uint32_t>(1, t->info.internal);
+    if (I < 16) {
+      G = 1;
+      while (G < I) G *= 2;
+    }
+  }
+  if (G > 32 || (G & (G - 1)) != 0)
+    fail(ST_ERR_ARGUMENT, "group_lanes must be a power of two <= 32 on the GPU, got " +
+                              std::to_string(g.group_lanes));
+  H = g.window_levels;
+  if (H == 0) {
+    if (t->info.internal <= G) {
+      // whole tree in one window: the paper's Proc. 5 geometry (mapped lanes)
+      H = std::max<uint32_t>(1, t->info.depth);
+    } else {
+      // complete-level windows: largest H with 2^H - 1 <= G
+      H = 1;
+      while ((2u << H) - 1 <= G) ++H;
+    }
+  }
+}
+
+void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+                      const st_geom& g, uint32_t* labels, st_stats* stats, cudaStream_t s, int dev) {
+  uint32_t G, H;
+  spec_geometry(t, g, G, H);
+  if (t->info.max_attribute >= (1u << 24))
+    fail(ST_ERR_ARGUMENT, "speculative kernel requires attribute indices < 2^24");
+  auto wt = t->windows(G, H);
+  SEntry* wdev = t->device_windows(dev, G, H, *wt);
+  st_tree::Dev& dv = t->device(dev);
+  const DevProps pr = dev_props(dev);
+  SpecArgs sa{};
+  sa.x = x;
+  sa.m = m;
+  sa.a = a;
+  sa.ld = (uint32_t)ld;
+  sa.win = wdev;
+  sa.n_entries = (uint32_t)wt->entries.size();
+  sa.root_code = wt->root_code;
+  sa.G = G;
+  sa.k = g.reductions;
+  sa.leaf_class = dv.leaf_tbl;
+  sa.labels = labels;
+  if (stats) {
+    sa.iters = stats->iterations;
+    sa.steps = stats->doubling_steps;
+    if (!sa.iters || !sa.steps) fail(ST_ERR_ARGUMENT, "st_stats requires both arrays");
+  }
+  const bool vec = layout == ST_LAYOUT_AOS && ld == a && vec_arity(a) &&
+                   (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+  int loader = layout == ST_LAYOUT_SOA ? kSoa : vec ? kVec : kScalar;
+  const uint32_t p = pitch_rt(a, loader == kVec);
+  size_t tile_bytes = (size_t)kWarpsPerCta * 32 * p * 4;
+  const size_t win_bytes = wt->entries.size() * sizeof(SEntry);
+  bool win_shared = win_bytes + tile_bytes <= std::min<size_t>(pr.smem_optin, 160 * 1024);
+  if (!win_shared && tile_bytes > pr.smem_optin) {
+    loader = kDirect;
+    tile_bytes = 0;
+  }
+  const size_t smem = (win_shared ? win_bytes : 0) + (loader == kDirect ? 0 : tile_bytes);
+  const uint32_t bps = g.blocks_per_sm;
+  if (loader == kVec) {
+    switch (a) {
+      case 8: return launch_spec_t<8, kVec>(win_shared, sa, smem, dev, bps, s);
+      case 16: return launch_spec_t<16, kVec>(win_shared, sa, smem, dev, bps, s);
+      case 19: return launch_spec_t<19, kVec>(win_shared, sa, smem, dev, bps, s);
+      case 32: return launch_spec_t<32, kVec>(win_shared, sa, smem, dev, bps, s);
+      case 64: return launch_spec_t<64, kVec>(win_shared, sa, smem, dev, bps, s);
+    }
+  }
+  switch (loader) {
+    case kSoa: return launch_spec_t<0, kSoa>(win_shared, sa, smem, dev, bps, s);
+    case kDirect: return launch_spec_t<0, kDirect>(win_shared, sa, smem, dev, bps, s);
+    default: return launch_spec_t<0, kScalar>(win_shared, sa, smem, dev, bps, s);
+  }
+}
+
+uint32_t resolve_algo(const st_tree* t, const st_geom& g, bool want_stats) {
+  if (g.algo == ST_ALGO_DATA || g.algo == ST_ALGO_SPECULATIVE) return g.algo;
+  if (g.algo != ST_ALGO_AUTO) fail(ST_ERR_ARGUMENT, "unknown algorithm " + std::to_string(g.algo));
+  (void)t;
+  return want_stats ? ST_ALGO_SPECULATIVE : ST_ALGO_DATA;
+}
+
+void eval_device_impl(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+                      const st_geom* geom, uint32_t* labels, st_stats* stats, cudaStream_t s) {
+  if (!t) fail(ST_ERR_ARGUMENT, "null tree");
+  check_common(m, a, ld, layout, t->info.max_attribute);
+  st_geom g{};
+  if (geom) g = *geom;
+  const uint32_t algo = resolve_algo(t, g, stats != nullptr);
+  if (stats && algo != ST_ALGO_SPECULATIVE)
+    fail(ST_ERR_ARGUMENT, "per-record stats are produced by the speculative kernel only");
+  if (m == 0) return;  // empty dataset: empty output, no launch
+  if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
+  const int dev = current_device();
+  if (algo == ST_ALGO_DATA)
+    eval_data_device(t, x, m, a, ld, layout, g, labels, s, dev);
+  else
+    eval_spec_device(t, x, m, a, ld, layout, g, labels, stats, s, dev);
+}
+
+// ---- forest ----------------------------------------------------------------
+template <int A, int LOADER>
+void launch_forest_t(bool packed, const ForestArgs& fa, size_t smem, int dev, cudaStream_t s) {
+  const uint64_t n_tiles = (fa.m + 31) / 32;
+  if (packed) {
+    auto fn = k_forest<A, LOADER, true>;
+    const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles);
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(fa);
+  } else {
+    auto fn = k_forest<A, LOADER, false>;
+    const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles);
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(fa);
+  }
+  check_launch();
+}
+
+void forest_device_impl(st_forest* f, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                        int layout, uint32_t* labels, cudaStream_t s) {
+  if (!f) fail(ST_ERR_ARGUMENT, "null forest");
+  check_common(m, a, ld, layout, f->max_attribute);
+  if (m == 0) return;
+  if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
+  const int dev = current_device();
+  const DevProps pr = dev_props(dev);
+  st_forest::Dev& dv = f->device(dev);
+  ForestArgs fa{};
+  fa.x = x;
+  fa.m = m;
+  fa.a = a;
+  fa.ld = (uint32_t)ld;
+  fa.nodes = dv.nodes;
+  fa.offsets = dv.offsets;
+  fa.t_count = f->t_count;
+  fa.n_classes = f->n_classes;
+  fa.abits = f->abits;
+  fa.labels = labels;
+  const bool packed = f->n_classes <= 8 && f->t_count <= 255;
+  const bool vec = layout == ST_LAYOUT_AOS && ld == a && vec_arity(a) &&
+                   (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+  int loader = layout == ST_LAYOUT_SOA ? kSoa : vec ? kVec : kScalar;
+  const uint32_t p = pitch_rt(a, loader == kVec);
+  size_t tile_bytes = (size_t)kWarpsPerCta * 32 * p * 4;
+  const size_t cnt_bytes = packed ? 0 : (size_t)kWarpsPerCta * 32 * f->n_classes * 4;
+  if (tile_bytes + cnt_bytes > pr.smem_optin) {
+    loader = kDirect;
+    tile_bytes = 0;
+  }
+  const size_t smem = tile_bytes + cnt_bytes;
+  if (loader == kVec) {
+    switch (a) {
+      case 8: return launch_forest_t<8, kVec>(packed, fa, smem, dev, s);
+      case 16: return launch_forest_t<16, kVec>(packed, fa, smem, dev, s);
+      case 19: return launch_forest_t<19, kVec>(packed, fa, smem, dev, s);
+      case 32: return launch_forest_t<32, kVec>(packed, fa, smem, dev, s);
+      case 64: return launch_forest_t<64, kVec>(packed, fa, smem, dev, s);
+    }
+  }
+  switch (loader) {
+    case kSoa: return launch_forest_t<0, kSoa>(packed, fa, smem, dev, s);
+    case kDirect: return launch_forest_t<0, kDirect>(packed, fa, smem, dev, s);
+    default: return launch_forest_t<0, kScalar>(packed, fa, smem, dev, s);
+  }
+}
+
+// ---- host-buffer path --------------------------------------------------------
+bool is_pinned_or_device(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeDevice ||
+         at.type == cudaMemoryTypeManaged;
+}
+
+// Runs `kernel(x_dev, rows, ld_dev, labels_dev, stream)` over chunks of the
+// host records with H2D / kernel / D2H overlapped across two streams.
+template <class K>
+void host_pipeline(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+                   uint32_t* labels, std::vector<std::pair<uint32_t*, uint32_t*>> extra_out,
+                   K&& kernel) {
+  constexpr int kStreams = 2;
+  const uint64_t row_bytes = (uint64_t)a * 4;
+  uint64_t chunk = std::max<uint64_t>(256, (256ull << 20) / row_bytes);
+  chunk = (chunk + 255) / 256 * 256;
+  chunk = std::min<uint64_t>(chunk, m);
+  const uint64_t n_chunks = (m + chunk - 1) / chunk;
+  const int ns = (int)std::min<uint64_t>(kStreams, n_chunks);
+  cudaStream_t st[kStreams] = {};
+  float* xd[kStreams] = {};
+  uint32_t* ld_out[kStreams] = {};
+  std::vector<uint32_t*> extra_dev[kStreams];
+  struct Cleanup {
+    cudaStream_t* st;
+    float** xd;
+    uint32_t** lo;
+    std::vector<uint32_t*>* ex;
+    int n;
+    ~Cleanup() {
+      for (int i = 0; i < n; ++i) {
+        if (st[i]) cudaStreamSynchronize(st[i]);
+        cudaFree(xd[i]);
+        cudaFree(lo[i]);
+        for (auto p : ex[i]) cudaFree(p);
+        if (st[i]) cudaStreamDestroy(st[i]);
+      }
+    }
+  } cleanup{st, xd, ld_out, extra_dev, ns};
+  const bool pin_in = is_pinned_or_device(x);
+  (void)pin_in;
+  for (int i = 0; i < ns; ++i) {
+    CK(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+    CK(cudaMalloc(&xd[i], chunk * row_bytes));
+    CK(cudaMalloc(&ld_out[i], chunk * 4));
+    for (size_t e = 0; e < extra_out.size(); ++e) {
+      uint32_t* p = nullptr;
+      CK(cudaMalloc(&p, chunk * 4));
+      extra_dev[i].push_back(p);
+    }
+  }
+  for (uint64_t c = 0; c < n_chunks; ++c) {
+    const int i = (int)(c % ns);
+    const uint64_t r0 = c * chunk;
+    const uint64_t rows = std::min(chunk, m - r0);
+    if (layout == ST_LAYOUT_AOS) {
+      if (ld == a)
+        CK(cudaMemcpyAsync(xd[i], x + r0 * a, rows * row_bytes, cudaMemcpyHostToDevice, st[i]));
+      else
+        CK(cudaMemcpy2DAsync(xd[i], row_bytes, x + r0 * ld, ld * 4, row_bytes, rows,
+                             cudaMemcpyHostToDevice, st[i]));
+    } else {
+      CK(cudaMemcpy2DAsync(xd[i], rows * 4, x + r0, ld * 4, rows * 4, a, cudaMemcpyHostToDevice,
+                           st[i]));
+    }
+    kernel(xd[i], rows, layout == ST_LAYOUT_AOS ? (uint64_t)a : rows, ld_out[i], extra_dev[i], st[i]);
+    CK(cudaMemcpyAsync(labels + r0, ld_out[i], rows * 4, cudaMemcpyDeviceToHost, st[i]));
+    for (size_t e = 0; e < extra_out.size(); ++e)
+      CK(cudaMemcpyAsync(extra_out[e].first + r0, extra_dev[i][e], rows * 4, cudaMemcpyDeviceToHost,
+                         st[i]));
+  }
+  for (int i = 0; i < ns; ++i) CK(cudaStreamSynchronize(st[i]));
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* st_last_error(void) { return g_error.c_str(); }
+const char* st_version(void) { return "spectree_b200 0.1 (sm_100a)"; }
+uint32_t st_last_launch_count(void) { return g_launches; }
+
+void st_geom_default(st_geom* g) {
+  if (g) std::memset(g, 0, sizeof(*g));
+}
+
+int st_device_count(int* count) {
+  return guarded([&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
+int st_tree_create(const st_node* nodes, uint32_t n, st_tree** out) {
+  return guarded([&] {
+    if (!out) fail(ST_ERR_ARGUMENT, "null output handle");
+    if (!nodes && n) fail(ST_ERR_ARGUMENT, "null node array");
+    *out = make_tree(nodes, n).release();
+  });
+}
+
+void st_tree_destroy(st_tree* tree) { delete tree; }
+
+int st_tree_get_info(const st_tree* tree, st_tree_info* out) {
+  return guarded([&] {
+    if (!tree || !out) fail(ST_ERR_ARGUMENT, "null argument");
+    *out = tree->info;
+    st_geom g{};
+    uint32_t G, H;
+    st_tree* t = const_cast<st_tree*>(tree);
+    spec_geometry(t, g, G, H);
+    out->spec_group_lanes = G;
+    out->spec_windows = t->windows(G, H)->windows;
+  });
+}
+
+int st_forest_create(const st_node* const* trees, const uint32_t* sizes, uint32_t t,
+                     uint32_t n_classes, st_forest** out) {
+  return guarded([&] {
+    if (!out || (!trees && t) || (!sizes && t)) fail(ST_ERR_ARGUMENT, "null argument");
+    if (t == 0) fail(ST_ERR_ARGUMENT, "forest requires at least one tree");
+    if (n_classes == 0 || n_classes > 64) fail(ST_ERR_ARGUMENT, "forest n_classes must be in [1, 64]");
+    auto f = std::make_unique<st_forest>();
+    f->t_count = t;
+    f->n_classes = n_classes;
+    uint32_t maxattr = 0;
+    uint64_t total = 0;
+    for (uint32_t k = 0; k < t; ++k) {
+      validate_links(trees[k], sizes[k], ("forest tree " + std::to_string(k)).c_str());
+      for (uint32_t i = 0; i < sizes[k]; ++i) {
+        maxattr = std::max(maxattr, trees[k][i].attribute);
+        const uint32_t c = trees[k][i].class_id;
+        if (c != ST_NO_CLASS && c >= n_classes)
+          fail(ST_ERR_ARGUMENT, "forest tree " + std::to_string(k) + " has class " + std::to_string(c) +
+                                    " >= n_classes " + std::to_string(n_classes));
+      }
+      total += sizes[k];
+    }
+    f->max_attribute = maxattr;
+    f->abits = bits_for(maxattr);
+    uint32_t maxn = 0;
+    for (uint32_t k = 0; k < t; ++k) maxn = std::max(maxn, sizes[k]);
+    if (((uint64_t)maxn << f->abits) >= (1ull << 31) || total >= (1ull << 32))
+      fail(ST_ERR_ARGUMENT, "forest too large for the compact device format");
+    f->compact.reserve(total);
+    f->offsets.push_back(0);
+    for (uint32_t k = 0; k < t; ++k) {
+      for (uint32_t i = 0; i < sizes[k]; ++i) {
+        const st_node& nd = trees[k][i];
+        if (nd.class_id != ST_NO_CLASS)
+          f->compact.push_back(CNode{nd.threshold, kLeafBit | nd.class_id});
+        else
+          f->compact.push_back(CNode{nd.threshold, (nd.child << f->abits) | nd.attribute});
+      }
+      f->offsets.push_back((uint32_t)f->compact.size());
+    }
+    *out = f.release();
+  });
+}
+
+void st_forest_destroy(st_forest* forest) { delete forest; }
+
+int st_eval_device(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                   int layout, const st_geom* geom, uint32_t* labels, st_stats* stats,
+                   void* stream) {
+  return guarded([&] {
+    g_launches = 0;
+    eval_device_impl(const_cast<st_tree*>(tree), x, m, a, ld, layout, geom, labels, stats,
+                     static_cast<cudaStream_t>(stream));
+  });
+}
+
+int st_eval(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+            const st_geom* geom, uint32_t* labels, st_stats* stats) {
+  return guarded([&] {
+    g_launches = 0;
+    st_tree* t = const_cast<st_tree*>(tree);
+    if (!t) fail(ST_ERR_ARGUMENT, "null tree");
+    uint64_t ld2 = ld;
+    check_common(m, a, ld2, layout, t->info.max_attribute);
+    st_geom g{};
+    if (geom) g = *geom;
+    resolve_algo(t, g, stats != nullptr);
+    if (m == 0) return;
+    if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
+    current_device();
+    std::vector<std::pair<uint32_t*, uint32_t*>> extra;
+    if (stats) {
+      if (!stats->iterations || !stats->doubling_steps)
+        fail(ST_ERR_ARGUMENT, "st_stats requires both arrays");
+      extra.push_back({stats->iterations, nullptr});
+      extra.push_back({stats->doubling_steps, nullptr});
+    }
+    uint32_t launches = 0;
+    host_pipeline(x, m, a, ld2, layout, labels, extra,
+                  [&](const float* xd, uint64_t rows, uint64_t ldd, uint32_t* lab,
+                      std::vector<uint32_t*>& ex, cudaStream_t s) {
+                    st_stats sd{};
+                    if (stats) {
+                      sd.iterations = ex[0];
+                      sd.doubling_steps = ex[1];
+                    }
+                    eval_device_impl(t, xd, rows, a, ldd, layout, &g, lab, stats ? &sd : nullptr, s);
+                    launches += g_launches;
+                    g_launches = 0;
+                  });
+    g_launches = launches;
+  });
+}
+
+int st_forest_eval_device(const st_forest* forest, const float* x, uint64_t m, uint32_t a,
+                          uint64_t ld, int layout, uint32_t* labels, void* stream) {
+  return guarded([&] {
+    g_launches = 0;
+    forest_device_impl(const_cast<st_forest*>(forest), x, m, a, ld, layout, labels,
+                       static_cast<cudaStream_t>(stream));
+  });
+}
+
+int st_forest_eval(const st_forest* forest, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                   int layout, uint32_t* labels) {
+  return guarded([&] {
+    g_launches = 0;
+    st_forest* f = const_cast<st_forest*>(forest);
+    if (!f) fail(ST_ERR_ARGUMENT, "null forest");
+    uint64_t ld2 = ld;
+    check_common(m, a, ld2, layout, f->max_attribute);
+    if (m == 0) return;
+    if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
+    current_device();
+    uint32_t launches = 0;
+    host_pipeline(x, m, a, ld2, layout, labels, {},
+                  [&](const float* xd, uint64_t rows, uint64_t ldd, uint32_t* lab,
+                      std::vector<uint32_t*>&, cudaStream_t s) {
+                    forest_device_impl(f, xd, rows, a, ldd, layout, lab, s);
+                    launches += g_launches;
+                    g_launches = 0;
+                  });
+    g_launches = launches;
+  });
+}
+
+int st_eval_sharded(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                    int layout, const st_geom* geom, const int* devices, int ndev,
+                    uint32_t* labels) {
+  return guarded([&] {
+    g_launches = 0;
+    st_tree* t = const_cast<st_tree*>(tree);
+    if (!t) fail(ST_ERR_ARGUMENT, "null tree");
+    if (ndev <= 0 || !devices) fail(ST_ERR_ARGUMENT, "ndev must be >= 1 with a device list");
+    uint64_t ld2 = ld;
+    check_common(m, a, ld2, layout, t->info.max_attribute);
+    if (m == 0) return;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      fail(ST_ERR_NO_DEVICE, "no CUDA device available (no CPU fallback)");
+    for (int k = 0; k < ndev; ++k)
+      if (devices[k] < 0 || devices[k] >= count)
+        fail(ST_ERR_ARGUMENT, "device id " + std::to_string(devices[k]) + " out of range");
+    std::vector<int> rc(ndev, 0);
+    std::vector<std::string> msg(ndev);
+    std::vector<uint32_t> launches(ndev, 0);
+    std::vector<std::thread> th;
+    for (int k = 0; k < ndev; ++k) {
+      th.emplace_back([&, k] {
+        // Proc. 3 ranges: shard k owns [floor(k m / n), floor((k+1) m / n))
+        const uint64_t lo = (uint64_t)((unsigned __int128)m * k / ndev);
+        const uint64_t hi = (uint64_t)((unsigned __int128)m * (k + 1) / ndev);
+        if (hi <= lo) return;
+        if (cudaSetDevice(devices[k]) != cudaSuccess) {
+          rc[k] = ST_ERR_CUDA;
+          msg[k] = "cudaSetDevice failed";
+          return;
+        }
+        const float* xs = layout == ST_LAYOUT_AOS ? x + lo * ld2 : x + lo;
+        rc[k] = st_eval(t, xs, hi - lo, a, ld2, layout, geom, labels + lo, nullptr);
+        if (rc[k]) msg[k] = st_last_error();
+        launches[k] = st_last_launch_count();
+      });
+    }
+    for (auto& h : th) h.join();
+    uint32_t total = 0;
+    for (int k = 0; k < ndev; ++k) {
+      if (rc[k]) fail(rc[k], "shard " + std::to_string(k) + ": " + msg[k]);
+      total += launches[k];
+    }
+    g_launches = total;
+  });
+}
+
+}  // extern "C"
