@@ -1,0 +1,434 @@
+#!/usr/bin/env python
+"""Benchmark: samples classified/sec per B200 (and N x B200, weak scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload C2] [--algo auto|data|speculative]
+
+One "step" = one pass of the hot path (tree evaluation) over one batch of
+synthetic records: the BASELINE.json configs[1] workload by default, C2 =
+unbalanced depth-24 tree (reference generator tree(24,256,32,8,201)) over
+16,000,000 records x 32 float32 attributes (data(16e6,32,202) on rank 0;
+rank r > 0 uses seed 202 + 1000 r), one batch per GPU (weak scaling).
+
+value  -- device-timed (CUDA events on the launching stream, barrier + sync on
+          both sides, max over ranks) with the records resident in HBM; the
+          2.05 GB/GPU input exceeds the 126 MB L2, so no flush is needed.
+e2e    -- the same metric through the public host API (st_eval: pinned host
+          records -> H2D -> kernel -> D2H labels), copies inside the timed region.
+roofline -- algorithmic bytes (4*A per record) per launch / the
+          kernel's average event-timed duration, against MEASURED_PEAKS.json.
+cpu_baseline -- the reference's eval_serial (oracle/_ref, compiled from the
+          unmodified sources) on 1 host core over a bounded sample.
+--impl reference -- the reference's eval_data_parallel on all host cores
+          (oracle/_ref) over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "C2": dict(desc="unbalanced depth-24 tree (skewed splits), 32 float32 attributes, "
+                    "16M samples per GPU: divergence stress for data decomposition",
+               tree=(24, 256, 32, 8, 201), m=16_000_000, a=32, seed=202,
+               labels_fnv=0x9e7e87e9cc15c4e0),
+    "C1": dict(desc="complete depth-10 tree, 16 float32 attributes, 1M samples",
+               tree=(10, 1024, 16, 8, 101), m=1_000_000, a=16, seed=102,
+               labels_fnv=0xe52f8e46c62dc8f1),
+    "C3": dict(desc="per-pixel segmentation: 1920x1080 frame, 8 features/pixel, depth-12 tree",
+               tree=(12, 2048, 8, 8, 301), m=2_073_600, a=8, seed=302,
+               labels_fnv=0xd57c3eb045278e36),
+    "C5d8": dict(desc="C5 shard: depth-8 tree, 16 attributes, 15.625M samples",
+                 tree=(8, 256, 16, 8, 508), m=15_625_000, a=16, seed=5000,
+                 labels_fnv=0xa41b18f5886a3516),
+    "C5d12": dict(desc="C5 shard: depth-12 tree, 16 attributes, 15.625M samples",
+                  tree=(12, 4096, 16, 8, 512), m=15_625_000, a=16, seed=5000,
+                  labels_fnv=0x8a36c71851f61114),
+    "C5d16": dict(desc="C5 shard: depth-16 tree, 16 attributes, 15.625M samples",
+                  tree=(16, 4096, 16, 8, 516), m=15_625_000, a=16, seed=5000,
+                  labels_fnv=0x4bbe70e47d70a501),
+    "C5d20": dict(desc="C5 shard: depth-20 tree, 16 attributes, 15.625M samples",
+                  tree=(20, 4096, 16, 8, 520), m=15_625_000, a=16, seed=5000,
+                  labels_fnv=0x894ffd1cd01ac0a5),
+}
+METRIC = "samples classified/sec per B200 and 8xB200 (+% of HBM roofline) vs CPU serial"
+UNIT = "samples/s"
+L2_BYTES = 126 * 2**20
+
+NVML_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                0x100: "display_clock_setting"}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, b.copy_ read+write)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler(threading.Thread):
+    """NVML SM clock + throttle-reason sampler run during the timed region."""
+
+    def __init__(self, cuda_index: int, period: float = 0.005):
+        super().__init__(daemon=True)
+        self.period = period
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            idx = cuda_index
+            try:
+                import torch
+
+                idx = torch.cuda._get_nvml_device_index(cuda_index)
+            except Exception:
+                pass
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - reported in JSON
+            self.err = repr(e)
+
+    def read(self):
+        t = time.perf_counter()
+        mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+        try:
+            reasons = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            reasons = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.samples.append((t, mhz, reasons))
+
+    def run(self):
+        while self.ok and not self.stop_ev.is_set():
+            try:
+                self.read()
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def summary(self, t0, t1):
+        if not self.ok:
+            return {"error": getattr(self, "err", "nvml unavailable")}
+        win = [s for s in self.samples if t0 <= s[0] <= t1]
+        if not win:  # very short timed region: the nearest sample on each side
+            before = [s for s in self.samples if s[0] < t0][-1:]
+            after = [s for s in self.samples if s[0] > t1][:1]
+            win = before + after
+        reasons = set()
+        for _, _, r in win:
+            for bit, name in NVML_REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median([s[1] for s in win]) if win else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons), "samples": len(win)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def ncu_traffic(workload, algo):
+    """dram bytes per launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", f"ncu_{workload}_{algo}.json")
+    try:
+        d = json.load(open(p))
+        return float(d["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- our arm ---
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1111_1373_b200 as st
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    W = WORKLOADS[args.workload]
+    m, a = W["m"], W["a"]
+    tree = st.generate_synthetic_tree(*W["tree"])
+    seed = W["seed"] + 1000 * rank
+    x_host = torch.empty((m, a), dtype=torch.float32, pin_memory=True)
+    st.generate_synthetic_dataset(m, a, seed, out=x_host.numpy())
+    x_dev = x_host.to(dev, non_blocking=False)
+    labels = torch.empty(m, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(algo, steps, warmup, sampler=None):
+        geom = st.GpuGeom(algo=algo)
+        for _ in range(warmup):
+            st.eval_device(tree, x_dev, labels, geom, stream=stream)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        launches = 0
+        t0 = time.perf_counter()
+        ev0.record(stream)
+        for _ in range(steps):
+            st.eval_device(tree, x_dev, labels, geom, stream=stream)
+            launches += st.last_launch_count()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        barrier()
+        torch.cuda.synchronize()
+        local_s = ev0.elapsed_time(ev1) / 1e3
+        return max_over_ranks(local_s), local_s, launches, (t0, t1)
+
+    # correctness of the measured configuration (rank 0 = canonical records)
+    labels_ok = {}
+    for algo in ("data", "speculative"):
+        st.eval_device(tree, x_dev, labels, st.GpuGeom(algo=algo), stream=stream)
+        torch.cuda.synchronize()
+        if rank == 0:
+            h = st.fnv1a64(labels.cpu().numpy())
+            labels_ok[algo] = h == W["labels_fnv"]
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    headline = args.algo if args.algo != "auto" else "data"
+    t_max, t_local, launches, (c0, c1) = timed(args.algo, args.steps, args.warmup)
+    clocks = sampler.summary(c0, c1)
+    by_algo = {}
+    peak, peak_src = peaks()
+    bytes_per_launch = 4.0 * a * m
+    for algo in ("data", "speculative"):
+        if algo == headline:
+            tm, tl, k = t_max, t_local, args.steps
+        else:
+            k = max(3, min(args.steps, args.alt_steps))
+            tm, tl, _, _ = timed(algo, k, max(3, min(args.warmup, 10)))
+        by_algo[algo] = {"value": world * m * k / tm, "ms_per_step": tm / k * 1e3,
+                         "roofline_frac": (bytes_per_launch / (tl / k) / 1e9) / peak}
+    sampler.stop_ev.set()
+
+    # e2e through the public host API: pinned host records -> labels on host
+    e2e_steps = max(1, args.e2e_steps)
+    labels_host = torch.empty(m, dtype=torch.int32, pin_memory=True)
+    geom = st.GpuGeom(algo=args.algo)
+    xnp = x_host.numpy()
+    st.eval_gpu(tree, xnp, geom, out=labels_host.numpy().view(np.uint32))  # warm
+    barrier()
+    e0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        st.eval_gpu(tree, xnp, geom, out=labels_host.numpy().view(np.uint32))
+    e_local = time.perf_counter() - e0
+    barrier()
+    e_max = max_over_ranks(e_local)
+
+    kernel_s = t_local / args.steps
+    achieved = bytes_per_launch / kernel_s / 1e9
+    line = {
+        "metric": METRIC,
+        "value": world * m * args.steps / t_max,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic: reference generators (tree + records), canonical seeds",
+        "config": {
+            "workload": f"{args.workload}: {W['desc']}",
+            "tree": "generate_synthetic_tree{} -> {} nodes, depth {}".format(
+                W["tree"], tree.size(), tree.depth()),
+            "records_per_gpu": m, "arity": a, "layout": "AoS float32",
+            "algo": args.algo if args.algo != "auto" else "auto(data)",
+            "parallelism": f"sample-sharded x{world} (weak), tree replicated, no collective",
+            "l2": f"inputs {4 * a * m / 1e9:.2f} GB/GPU > L2 126 MB: no flush needed"
+                  if 4 * a * m > 2 * L2_BYTES else "inputs L2-resident: results optimistic",
+        },
+        "labels_match_reference_hash": labels_ok if rank == 0 else None,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "frac_vs_8TBs": achieved / 8000.0,
+                     "traffic": ncu_traffic(args.workload, headline),
+                     "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "kernel_ms": kernel_s * 1e3},
+        "by_algorithm": by_algo,
+        "e2e": {"value": world * m * e2e_steps / e_max, "unit": UNIT,
+                "h2d_bytes_per_step": 4 * a * m, "d2h_bytes_per_step": 4 * m,
+                "steps": e2e_steps, "api": "st_eval (host pinned buffers, chunked H2D/kernel/D2H)"},
+        "clocks": clocks,
+        "gpu_launches": launches,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, tree.nodes(), xnp)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _ref_or_port():
+    import oracle
+
+    if oracle.ref_available():
+        return oracle.RefOracle(), "reference"
+    return oracle.COracle(), "port"
+
+
+def cpu_baseline(args, nodes, x):
+    """oracle/_ref eval_serial on ONE host core over a bounded sample."""
+    import oracle
+
+    impl, kind = _ref_or_port()
+    sample = min(len(x), args.cpu_sample)
+    xs = np.ascontiguousarray(x[:sample])
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+        pinned = True
+    except Exception:
+        pinned = False
+    done = 0
+    t0 = time.perf_counter()
+    if kind == "reference":
+        with impl.tree(nodes) as t, impl.data(xs) as d:
+            t.eval_serial(d)  # warm
+            t0 = time.perf_counter()
+            while True:
+                t.eval_serial(d)
+                done += sample
+                if time.perf_counter() - t0 >= args.cpu_seconds:
+                    break
+    else:
+        while True:
+            impl.eval_serial(nodes, xs)
+            done += sample
+            if time.perf_counter() - t0 >= args.cpu_seconds:
+                break
+    el = time.perf_counter() - t0
+    if pinned:
+        try:
+            os.sched_setaffinity(0, set(range(os.cpu_count())))
+        except Exception:
+            pass
+    return {"value": done / el, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"first {sample} records of the rank-0 workload, {done // sample} passes "
+                      f"({el:.1f} s) of spectree::eval_serial pinned to 1 core",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# --------------------------------------------------------- reference arm ---
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    W = WORKLOADS[args.workload]
+    impl, kind = _ref_or_port()
+    a = W["a"]
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    sample = min(W["m"], args.ref_sample)
+    nodes = impl.gen_tree(*W["tree"])
+    x = impl.gen_dataset(sample, a, W["seed"])  # = the first `sample` canonical records
+    chunk = -(-sample // cores)
+    if kind == "reference":
+        with impl.tree(nodes) as t, impl.data(x) as d:
+            for _ in range(args.warmup):
+                t.eval_data_parallel(d, cores, chunk, os_threads=cores)
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                t.eval_data_parallel(d, cores, chunk, os_threads=cores)
+            el = time.perf_counter() - t0
+    else:
+        for _ in range(args.warmup):
+            impl.eval_serial(nodes, x)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            impl.eval_serial(nodes, x)
+        el = time.perf_counter() - t0
+        cores = 1
+    value = sample * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: reference generators, canonical seeds",
+        "config": {"workload": f"{args.workload}: {W['desc']}", "records_per_step": sample,
+                   "arity": a, "algo": "spectree::eval_data_parallel (CPU threads)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"first {sample} records of {args.workload} per step; "
+                                   f"eval_data_parallel workers=os_threads={cores}, chunk={chunk}",
+                         "cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C2")
+    ap.add_argument("--algo", choices=["auto", "data", "speculative"], default="auto")
+    ap.add_argument("--alt-steps", type=int, default=200,
+                    help="timed steps for the non-headline algorithm in by_algorithm")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-sample", type=int, default=2_000_000)
+    ap.add_argument("--ref-sample", type=int, default=2_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)  # timing rule: >= 3 untimed warm-up steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

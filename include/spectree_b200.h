@@ -156,6 +156,21 @@ int st_forest_eval_device(const st_forest* forest, const float* x, uint64_t m, u
  * thread enqueued (for bench.py's gpu_launches claim). */
 uint32_t st_last_launch_count(void);
 
+/* ---- input side of the boundary (reference layer L1) ----------------------
+ * Canonical synthetic inputs, bit-identical to the reference generators for
+ * the same seed: generate_synthetic_tree (synthetic.cpp:82-154, breadth-first
+ * encoded as by encode_breadth_first, tree.cpp:72-113) and
+ * generate_synthetic_dataset (synthetic.cpp:156-182; gaussian != 0 selects
+ * Distribution::gaussian).  st_synthetic_tree writes at most `cap` nodes and
+ * always sets *n_out to the node count (call with out = NULL to size).
+ * Infeasible shapes return ST_ERR_ARGUMENT with the reference's message. */
+int st_synthetic_tree(uint32_t depth, uint32_t leaves, uint32_t arity, uint32_t classes,
+                      uint64_t seed, st_node* out, uint32_t cap, uint32_t* n_out);
+int st_synthetic_dataset(uint64_t count, uint32_t arity, uint64_t seed, int gaussian, float* out);
+/* dataset_checksum (dataset.cpp:76-93) and raw FNV-1a-64 (label hashes). */
+uint64_t st_dataset_checksum(const float* x, uint64_t count, uint32_t arity);
+uint64_t st_fnv1a64(const void* data, uint64_t n);
+
 #ifdef __cplusplus
 }
 #endif

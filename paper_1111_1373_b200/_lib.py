@@ -67,6 +67,7 @@ EXPORTS = (
     "st_forest_create", "st_forest_destroy",
     "st_eval", "st_eval_device", "st_eval_sharded",
     "st_forest_eval", "st_forest_eval_device", "st_last_launch_count",
+    "st_synthetic_tree", "st_synthetic_dataset", "st_dataset_checksum", "st_fnv1a64",
 )
 
 _lib = None
@@ -110,6 +111,14 @@ def load() -> C.CDLL:
     L.st_forest_eval_device.restype = i32
     L.st_forest_eval_device.argtypes = [vp, vp, u64, u32, u64, i32, vp, vp]
     L.st_last_launch_count.restype = u32
+    L.st_synthetic_tree.restype = i32
+    L.st_synthetic_tree.argtypes = [u32, u32, u32, u32, u64, vp, u32, C.POINTER(u32)]
+    L.st_synthetic_dataset.restype = i32
+    L.st_synthetic_dataset.argtypes = [u64, u32, u64, i32, vp]
+    L.st_dataset_checksum.restype = u64
+    L.st_dataset_checksum.argtypes = [vp, u64, u32]
+    L.st_fnv1a64.restype = u64
+    L.st_fnv1a64.argtypes = [vp, u64]
     _lib = L
     return L
 

@@ -13,8 +13,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "st_capi.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "st_kernels.cuh"),
+SRCS = [os.path.join(HERE, "csrc", "st_capi.cu"), os.path.join(HERE, "csrc", "st_synth.cpp")]
+DEPS = [*SRCS, os.path.join(HERE, "csrc", "st_kernels.cuh"),
         os.path.join(ROOT, "include", "spectree_b200.h")]
 OUT = os.path.join(HERE, "libspectree_b200.so")
 
@@ -42,7 +42,7 @@ def up_to_date() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or not up_to_date():
-        cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", SRC]
+        cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *SRCS]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

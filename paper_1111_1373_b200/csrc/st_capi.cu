@@ -125,6 +125,10 @@ struct WinTable {
 
 }  // namespace
 
+namespace st_internal {
+void set_error(const std::string& msg) { g_error = msg; }
+}  // namespace st_internal
+
 struct st_tree {
   std::vector<st_node> nodes;
   st_tree_info info{};

@@ -111,13 +111,17 @@ def check_attribute_range(tree: EncodedTree, dataset: Dataset) -> None:
 
 
 def eval_gpu(tree, dataset, geom: Optional[GpuGeom] = None, stats: Optional["SpeculativeStats"] = None,
-             layout: str = "aos") -> np.ndarray:
-    """Host-buffer evaluation through ``st_eval`` (H2D + kernel + D2H)."""
+             layout: str = "aos", out: Optional[np.ndarray] = None) -> np.ndarray:
+    """Host-buffer evaluation through ``st_eval`` (H2D + kernel + D2H).
+    ``out`` may be a preallocated (e.g. pinned) uint32 buffer of m labels."""
     tree = _as_tree(tree)
     dataset = _as_data(dataset)
     check_attribute_range(tree, dataset)
     m = dataset.count()
-    out = np.empty(m, dtype=np.uint32)
+    if out is None:
+        out = np.empty(m, dtype=np.uint32)
+    if out.dtype != np.uint32 or out.size != m or not out.flags.c_contiguous:
+        raise ArgumentError("out must be a contiguous uint32 array of one label per record")
     g = (geom or GpuGeom()).to_c()
     x = dataset.values()
     if layout == "soa":

@@ -1,0 +1,322 @@
+"""GPU parity tests: every kernel through the C ABI against the pinned oracle
+and the reference-generated golden fixtures.  Bar: bit-exact labels (integer
+classification output), and exact speculative step counters where the
+reference defines them."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1111_1373_b200 as st
+import support
+from paper_1111_1373_b200.tree import encode_breadth_first
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+DATA_GEOMS = [st.GpuGeom(algo="data"),
+              st.GpuGeom(algo="data", samples_per_thread=1),
+              st.GpuGeom(algo="data", tree_loc="global"),
+              st.GpuGeom(algo="data", tree_loc="constant")]
+SPEC_GEOMS = [st.GpuGeom(algo="speculative"),
+              st.GpuGeom(algo="speculative", group_lanes=4),
+              st.GpuGeom(algo="speculative", group_lanes=8),
+              st.GpuGeom(algo="speculative", group_lanes=32),
+              st.GpuGeom(algo="speculative", group_lanes=16, window_levels=8),
+              st.GpuGeom(algo="speculative", reductions=2)]
+ALL_GEOMS = DATA_GEOMS + SPEC_GEOMS
+
+
+def _dev_eval(tree, x_dev, geom, m):
+    out = torch.empty(m, dtype=torch.int32, device="cuda")
+    st.eval_device(tree, x_dev, out, geom)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint32)
+
+
+# ------------------------------------------------ canonical workloads ---
+@pytest.mark.parametrize("name", list(support.APPENDIX_A))
+def test_appendix_a_labels(cuda, co, name):
+    """Full-size canonical workloads: GPU label hash == the reference's."""
+    nodes, x = support.workload(co, name)
+    lab_fnv, first8 = support.APPENDIX_A[name][5], support.APPENDIX_A[name][6]
+    tree = st.EncodedTree(nodes)
+    xd = torch.from_numpy(x).to(cuda)
+    geoms = ALL_GEOMS if name in ("paper", "C1", "C2", "C3") else [DATA_GEOMS[0], SPEC_GEOMS[0]]
+    for g in geoms:
+        got = _dev_eval(tree, xd, g, len(x))
+        assert co.fnv1a(got) == lab_fnv, f"{name} {g}"
+        assert got[:8].tolist() == first8
+
+
+def test_c4_forest_vote_hash(cuda, co):
+    """128-tree forest vote on data(8e6, 64, 499) == reference hash (Appendix A)."""
+    trees = [co.gen_tree(12, 1024, 64, 8, 401 + t) for t in range(128)]
+    x = co.gen_dataset(8_000_000, 64, 499)
+    f = st.Forest(trees, 8)
+    out = torch.empty(len(x), dtype=torch.int32, device="cuda")
+    st.eval_forest_device(f, torch.from_numpy(x).to(cuda), out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint32)
+    assert co.fnv1a(got) == support.C4_FOREST_LABELS_FNV
+    assert got[:8].tolist() == support.C4_FOREST_FIRST8
+    # spot-check the vote on a slice with the oracle
+    sl = slice(0, 20000)
+    assert np.array_equal(got[sl], co.eval_forest(trees, x[sl], 8))
+
+
+# ------------------------------------------ acceptance-style corpora ---
+def test_exhaustive_shapes_all_kernels(cuda, co):
+    """acceptance.cpp:100-116: 626 shapes on grid records (ties + gaps)."""
+    n = 0
+    for leaves in range(1, 9):
+        for shape in support.all_shapes(leaves):
+            internal = support.assign_labels(shape)
+            x = support.grid_records(internal)
+            tree = encode_breadth_first(shape)
+            want = support.recursive_oracle(shape, x)
+            for g in (DATA_GEOMS[0], DATA_GEOMS[3], SPEC_GEOMS[0], SPEC_GEOMS[1], SPEC_GEOMS[5]):
+                assert np.array_equal(st.eval_gpu(tree, x, g), want), (leaves, g)
+            n += 1
+    assert n == 626
+
+
+def test_fuzz_corpus_1000(cuda, co):
+    """acceptance.cpp:119-143: 1000 synthetic trees, 1000 records each,
+    uniform/gaussian, all kernels vs the oracle."""
+    for seed in range(1, 1001):
+        depth, leaves, arity, classes = support.fuzz_shape(seed)
+        nodes = co.gen_tree(depth, leaves, arity, classes, seed)
+        x = co.gen_dataset(1000, arity, seed + 5000, gaussian=(seed % 2 == 0))
+        want = co.eval_serial(nodes, x)
+        g1 = DATA_GEOMS[seed % len(DATA_GEOMS)]
+        g2 = SPEC_GEOMS[seed % len(SPEC_GEOMS)]
+        assert np.array_equal(st.eval_gpu(nodes, x, g1), want), (seed, g1)
+        assert np.array_equal(st.eval_gpu(nodes, x, g2), want), (seed, g2)
+
+
+def test_reference_fixture_labels_and_step_counters(cuda):
+    """Reference eval_speculative counters (mapped, barrier-separated, k=1,2)
+    reproduced exactly by the shfl kernel when the tree fits one warp group."""
+    g = np.load(os.path.join(GOLD, "ref_fuzz.npz"))
+    checked = 0
+    for seed in range(1, 61):
+        nodes = g[f"s{seed}_nodes"].view(st.NODE_DTYPE)
+        x = g[f"s{seed}_x"]
+        tree = st.EncodedTree(nodes)
+        assert np.array_equal(st.eval_data_parallel(tree, x), g[f"s{seed}_labels"])
+        for k in (1, 2):
+            cfg = st.default_speculative(tree, len(x), reductions=k)
+            stats = st.SpeculativeStats()
+            lab = st.eval_speculative(tree, x, cfg, stats)
+            assert np.array_equal(lab, g[f"s{seed}_labels"]), seed
+            if len(tree.internal_indices()) <= 32:
+                assert np.array_equal(stats.iterations, g[f"s{seed}_it{k}"]), (seed, k)
+                assert np.array_equal(stats.doubling_steps, g[f"s{seed}_st{k}"]), (seed, k)
+                checked += 1
+    assert checked >= 20
+
+
+def test_step_law_depth_chain(cuda):
+    """test_eval_speculative.cpp:138-168 on the 11-chain."""
+    tree = encode_breadth_first(support.depth_chain_tree(11))
+    x = np.array([[0.75], [0.25]], np.float32)
+    for k, it0, st0 in ((1, 4, 4), (2, 2, 4), (3, 2, 6)):
+        stats = st.SpeculativeStats()
+        st.eval_speculative(tree, x, st.default_speculative(tree, 2, reductions=k), stats)
+        assert stats.iterations.tolist() == [it0, 0]
+        assert stats.doubling_steps.tolist() == [st0, 0]
+
+
+def test_step_law_random_single_window(cuda, co):
+    """Criterion-2 law (acceptance.cpp:173-211) on trees that fit a warp."""
+    for seed in range(1, 40):
+        nodes = co.gen_tree(12, 20 + seed % 13, 8, 5, 97 + seed)
+        x = co.gen_dataset(5000, 8, 13 + seed)
+        tree = st.EncodedTree(nodes)
+        assert len(tree.internal_indices()) <= 32
+        depths = co.traversal_depths(nodes, x)
+        want = np.array([support.ceil_log2(int(d)) for d in depths])
+        stats = st.SpeculativeStats()
+        lab = st.eval_speculative(tree, x, st.default_speculative(tree, len(x), reductions=1), stats)
+        assert np.array_equal(lab, co.eval_serial(nodes, x))
+        assert np.array_equal(stats.doubling_steps, want)
+        assert np.array_equal(stats.iterations, want)
+        stats2 = st.SpeculativeStats()
+        st.eval_speculative(tree, x, st.default_speculative(tree, len(x), reductions=2), stats2)
+        assert np.array_equal(stats2.iterations, (want + 1) // 2)
+        assert stats2.barriers == len(x) + int(stats2.doubling_steps.sum())
+
+
+# ------------------------------------------------------------ edge cases ---
+def test_edge_semantics(cuda, co):
+    """Ties, NaN, +/-inf, -0.0 and subnormals: ordered '>' without FTZ."""
+    sub = np.float32(1e-40)
+    thr_vals = [0.5, 0.0, -0.0, sub, -sub, 1e30, -1e30]
+    for thr in thr_vals:
+        t = encode_breadth_first(st.make_split(0, float(thr), st.make_leaf(1), st.make_leaf(2)))
+        vals = [thr, 0.0, -0.0, sub, -sub, 2 * sub, np.nan, np.inf, -np.inf, 0.49999997, 0.5,
+                0.50000006, np.float32(np.nextafter(np.float32(thr), np.float32(1)))]
+        x = np.array(vals, np.float32).reshape(-1, 1)
+        want = co.eval_serial(t.nodes(), x)
+        for g in ALL_GEOMS:
+            assert np.array_equal(st.eval_gpu(t, x, g), want), (thr, g)
+
+
+def test_single_leaf_and_empty(cuda):
+    leaf = st.EncodedTree(np.array([(0, np.inf, 0, 6)], dtype=st.NODE_DTYPE))
+    x = np.array([[0.1], [0.9]], np.float32)
+    for g in ALL_GEOMS:
+        assert st.eval_gpu(leaf, x, g).tolist() == [6, 6]
+    stats = st.SpeculativeStats()
+    cfg = st.SpeculativeConfig(group_lanes=1, groups=1, records_per_group=2)
+    assert st.eval_speculative(leaf, x, cfg, stats).tolist() == [6, 6]
+    assert stats.iterations.tolist() == [0, 0]
+    empty = np.zeros((0, 2), np.float32)
+    assert st.eval_gpu(leaf, empty).size == 0
+    assert st.last_launch_count() == 0
+
+
+@pytest.mark.parametrize("m", [1, 31, 33, 127, 129, 4097, 100003])
+def test_ragged_record_counts(cuda, co, m):
+    nodes = co.gen_tree(10, 300, 16, 8, 5)
+    x = co.gen_dataset(m, 16, 6)
+    want = co.eval_serial(nodes, x)
+    for g in ALL_GEOMS:
+        assert np.array_equal(st.eval_gpu(nodes, x, g), want), (m, g)
+
+
+@pytest.mark.parametrize("arity", [1, 3, 5, 8, 16, 19, 24, 32, 40, 64, 100, 300])
+def test_arities_layouts_and_strides(cuda, co, arity):
+    """Compile-time and runtime arities, AoS/SoA, strided rows, unaligned
+    base pointers."""
+    nodes = co.gen_tree(9, 120, arity, 6, 1000 + arity)
+    x = co.gen_dataset(3001, arity, 77)
+    want = co.eval_serial(nodes, x)
+    tree = st.EncodedTree(nodes)
+    for g in (DATA_GEOMS[0], DATA_GEOMS[2], SPEC_GEOMS[0], SPEC_GEOMS[2]):
+        assert np.array_equal(st.eval_gpu(tree, x, g), want)
+        assert np.array_equal(st.eval_gpu(tree, x, g, layout="soa"), want)
+        xd = torch.from_numpy(x).cuda()
+        assert np.array_equal(_dev_eval(tree, xd, g, len(x)), want)
+        # strided rows: view into a wider matrix
+        wide = torch.zeros(len(x), arity + 3, device="cuda")
+        wide[:, :arity] = xd
+        assert np.array_equal(_dev_eval(tree, wide[:, :arity], g, len(x)), want)
+        # unaligned base pointer (offset by one float)
+        buf = torch.zeros(len(x) * arity + 1, device="cuda")
+        buf[1:] = xd.reshape(-1)
+        assert np.array_equal(_dev_eval(tree, buf[1:].view(len(x), arity), g, len(x)), want)
+        # SoA device tensor
+        out = torch.empty(len(x), dtype=torch.int32, device="cuda")
+        st.eval_device(tree, xd.t().contiguous(), out, g, layout="soa")
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+
+
+def test_large_class_ids_and_wide_format(cuda, co):
+    """class ids >= 2^31 (leaf-class table) and attribute indices too wide for
+    the compact node (16-byte fallback + direct loader)."""
+    nodes = co.gen_tree(8, 50, 6, 7, 3).copy()
+    leaf = nodes["class_id"] != st.NO_CLASS
+    nodes["class_id"][leaf] = 0xFFFFFFF0 - nodes["class_id"][leaf]
+    x = co.gen_dataset(2000, 6, 4)
+    want = co.eval_serial(nodes, x)
+    for g in ALL_GEOMS:
+        assert np.array_equal(st.eval_gpu(nodes, x, g), want)
+    # a 2047-node tree reading attribute 2^20: child << 21 overflows the
+    # compact meta word, so the 16-byte node path + direct loader run
+    big = co.gen_tree(10, 1024, 16, 8, 101).copy()
+    big[0]["attribute"] = 1 << 20
+    a = (1 << 20) + 1
+    x = np.random.default_rng(0).random((6, a), dtype=np.float32)
+    assert st.tree_info(big)["compact"] == 0
+    want = co.eval_serial(big, x)
+    for g in (DATA_GEOMS[0], SPEC_GEOMS[0]):
+        assert np.array_equal(st.eval_gpu(big, x, g), want)
+
+
+def test_deep_and_large_trees(cuda, co):
+    """A 16K-node tree (global-memory node array / window table) and a deep
+    skewed chain."""
+    nodes = co.gen_tree(20, 8192, 16, 8, 77)
+    x = co.gen_dataset(50000, 16, 78)
+    want = co.eval_serial(nodes, x)
+    for g in ALL_GEOMS:
+        assert np.array_equal(st.eval_gpu(nodes, x, g), want)
+    chain = encode_breadth_first(support.depth_chain_tree(300))
+    xc = np.array([[0.75], [0.25], [0.5], [1.0]], np.float32)
+    want = co.eval_serial(chain.nodes(), xc)
+    for g in ALL_GEOMS:
+        assert np.array_equal(st.eval_gpu(chain, xc, g), want)
+
+
+def test_dag_shaped_input(cuda, co):
+    """Forward-linked but non-tree node arrays (shared subtrees) evaluate like
+    the reference walk."""
+    nodes = np.array([(0, 0.5, 1, st.NO_CLASS), (1, 0.3, 3, st.NO_CLASS), (1, 0.7, 3, st.NO_CLASS),
+                      (0, 0.2, 5, st.NO_CLASS), (0, np.inf, 4, 9), (0, np.inf, 5, 1),
+                      (0, np.inf, 6, 2)], dtype=st.NODE_DTYPE)
+    x = co.gen_dataset(1000, 2, 5)
+    want = co.eval_serial(nodes, x)
+    for g in ALL_GEOMS:
+        assert np.array_equal(st.eval_gpu(nodes, x, g), want)
+
+
+def test_forest_variants(cuda, co):
+    x = co.gen_dataset(7001, 12, 9)
+    for t_count, classes in ((1, 3), (7, 8), (300, 5), (9, 40)):
+        trees = [co.gen_tree(7, 40, 12, classes, 50 + t) for t in range(t_count)]
+        want = co.eval_forest(trees, x, classes)
+        assert np.array_equal(st.eval_forest(st.Forest(trees, classes), x), want), (t_count, classes)
+    with pytest.raises(st.ArgumentError):
+        st.Forest([co.gen_tree(7, 40, 12, 9, 1)], 4)  # class >= n_classes
+
+
+def test_sharded_driver(cuda, co):
+    """st_eval_sharded partitions records by the Proc. 3 range rule; on one
+    GPU the device list may repeat device 0."""
+    nodes = co.gen_tree(24, 256, 32, 8, 201)
+    x = co.gen_dataset(100_003, 32, 202)
+    want = co.eval_serial(nodes, x)
+    for devs in ([0], [0, 0], [0, 0, 0, 0]):
+        for g in (DATA_GEOMS[0], SPEC_GEOMS[0]):
+            assert np.array_equal(st.eval_sharded(nodes, x, devs, g), want)
+    with pytest.raises(st.ArgumentError):
+        st.eval_sharded(nodes, x, [torch.cuda.device_count()])
+
+
+def test_host_pipeline_multi_chunk(cuda, co):
+    """Host-buffer path with several H2D/kernel/D2H chunks over two streams."""
+    nodes = co.gen_tree(12, 2048, 8, 8, 301)
+    x = co.gen_dataset(9_000_000, 8, 302)  # 288 MB > one 256 MB chunk
+    want = co.eval_serial(nodes, x)
+    for g in (DATA_GEOMS[0], SPEC_GEOMS[0]):
+        assert np.array_equal(st.eval_gpu(nodes, x, g), want)
+        assert st.last_launch_count() >= 2
+
+
+def test_concurrent_callers(cuda, co):
+    """Pure-function contract: concurrent host threads
+    sharing one tree."""
+    import threading
+
+    nodes = co.gen_tree(10, 1024, 16, 8, 101)
+    tree = st.EncodedTree(nodes)
+    xs = [co.gen_dataset(20000, 16, s) for s in range(8)]
+    wants = [co.eval_serial(nodes, x) for x in xs]
+    errors = []
+
+    def work(i):
+        try:
+            for g in (DATA_GEOMS[i % 4], SPEC_GEOMS[i % 6]):
+                if not np.array_equal(st.eval_gpu(tree, xs[i], g), wants[i]):
+                    errors.append(i)
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(8)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    assert not errors
