@@ -65,7 +65,7 @@ enum st_algo { ST_ALGO_AUTO = 0, ST_ALGO_DATA = 1, ST_ALGO_SPECULATIVE = 2 };
 enum st_tree_loc {
   ST_TREE_AUTO = 0,
   ST_TREE_SHARED = 1,   /* staged once per CTA into shared memory */
-  ST_TREE_CONSTANT = 2, /* __grid_constant__ kernel parameter (constant bank), N <= 4064 */
+  ST_TREE_CONSTANT = 2, /* __grid_constant__ kernel parameter (constant bank), N <= 4000 */
   ST_TREE_GLOBAL = 3    /* read-only global path (L1/L2), any size */
 };
 
@@ -80,7 +80,8 @@ typedef struct st_geom {
                                   k >= 1 = check the root after every k doublings
                                   (reference ReductionMode::barrier_separated, k = reductions_per_iteration) */
   uint32_t blocks_per_sm;      /* 0 = occupancy-derived persistent grid */
-  uint32_t reserved[5];
+  uint32_t stages;             /* TMA record-pipeline stages per warp (0 = auto, 2-4) */
+  uint32_t reserved[4];
 } st_geom;
 
 /* Optional per-record speculative counters (SpeculativeStats,

@@ -39,7 +39,8 @@ class st_geom(C.Structure):
         ("window_levels", C.c_uint32),
         ("reductions", C.c_uint32),
         ("blocks_per_sm", C.c_uint32),
-        ("reserved", C.c_uint32 * 5),
+        ("stages", C.c_uint32),
+        ("reserved", C.c_uint32 * 4),
     ]
 
 

@@ -236,7 +236,7 @@ struct st_tree {
       base[w] = (uint32_t)total;
       total += members[w].size();
     }
-    if (total + 32 >= (1u << 30)) fail(ST_ERR_ARGUMENT, "tree too large for speculative windows");
+    if (16 * (total + 32) >= (1u << 30)) fail(ST_ERR_ARGUMENT, "tree too large for speculative windows");
     wt.entries.resize(total + 32, SEntry{0.0f, 0u, 0u, 0u});
     std::vector<int32_t> lane_of(n, -1);
     for (uint32_t w = 0; w < nw; ++w) {
@@ -251,13 +251,13 @@ struct st_tree {
       auto code = [&](uint32_t c) -> uint32_t {
         if (is_leaf(c)) return kLeafBit | leaf_code[c];
         if (lane_of[c] >= 0) return (uint32_t)lane_of[c];
-        return kExitBit | base[win_of_root[c]];
+        return kExitBit | (16u * base[win_of_root[c]]);  // byte offset of the window
       };
       for (uint32_t j = 0; j < mem.size(); ++j) {
         const st_node& nd = nodes[mem[j]];
         SEntry e;
         e.thr = nd.threshold;
-        e.attr_steps = nd.attribute | (steps << 24);
+        e.attr_steps = (4u * nd.attribute) | (steps << 24);
         e.left = code(nd.child);
         e.right = code(nd.child + 1);
         wt.entries[base[w] + j] = e;
@@ -358,10 +358,16 @@ void validate_links(const st_node* nodes, uint32_t n, const char* what) {
   }
 }
 
-uint32_t bits_for(uint32_t v) {  // bits to hold values 0..v
+uint32_t bits_for(uint64_t v) {  // bits to hold values 0..v
   uint32_t b = 1;
-  while (b < 32 && (v >> b) != 0) ++b;
+  while (b < 64 && (v >> b) != 0) ++b;
   return b;
+}
+
+// Compact meta for an internal node: (8*child) << abits | 4*attr.
+bool compact_fits(uint32_t n, uint32_t max_attribute, uint32_t* abits) {
+  *abits = bits_for(4ull * max_attribute);
+  return *abits < 31 && ((8ull * n) << *abits) < (1ull << 31);
 }
 
 std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
@@ -394,8 +400,7 @@ std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
       t->leaf_code[i] = nodes[i].class_id;
     }
   }
-  t->abits = bits_for(in.max_attribute);
-  t->compact_ok = t->abits < 31 && ((uint64_t)n << t->abits) < (1ull << 31);
+  t->compact_ok = compact_fits(n, in.max_attribute, &t->abits);
   if (t->compact_ok) {
     t->compact.resize(n);
     for (uint32_t i = 0; i < n; ++i) {
@@ -403,7 +408,7 @@ std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
       if (nd.class_id != ST_NO_CLASS)
         t->compact[i] = CNode{nd.threshold, kLeafBit | t->leaf_code[i]};
       else
-        t->compact[i] = CNode{nd.threshold, (nd.child << t->abits) | nd.attribute};
+        t->compact[i] = CNode{nd.threshold, ((8u * nd.child) << t->abits) | (4u * nd.attribute)};
     }
   }
   in.compact = t->compact_ok ? 1 : 0;
@@ -413,24 +418,29 @@ std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
 // ---------------------------------------------------------------------------
 // Launch helpers
 // ---------------------------------------------------------------------------
-struct Launch {
-  const void* fn;
-  size_t smem;
-};
-
 int blocks_for(const void* fn, size_t smem, int dev, uint32_t blocks_per_sm, uint64_t n_tiles) {
   static std::mutex mu;
+  static std::map<std::pair<const void*, int>, bool> attr_set;
   static std::map<std::tuple<const void*, size_t, int>, int> occ_cache;
   const DevProps pr = dev_props(dev);
+  if (smem > pr.smem_optin)
+    fail(ST_ERR_ARGUMENT, "kernel needs " + std::to_string(smem) + " B of shared memory (max " +
+                              std::to_string(pr.smem_optin) + ")");
   int occ = 0;
   {
     std::lock_guard<std::mutex> lk(mu);
+    // The dynamic-smem ceiling is set once per (kernel, device) to the opt-in
+    // maximum, so launches of any size after it stay valid.
+    auto akey = std::make_pair(fn, dev);
+    if (!attr_set.count(akey)) {
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr.smem_optin));
+      attr_set[akey] = true;
+    }
     auto key = std::make_tuple(fn, smem, dev);
     auto it = occ_cache.find(key);
     if (it != occ_cache.end()) {
       occ = it->second;
     } else {
-      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarpsPerCta * 32, smem));
       if (occ < 1) fail(ST_ERR_ARGUMENT, "kernel configuration does not fit on an SM");
       occ_cache[key] = occ;
@@ -440,6 +450,10 @@ int blocks_for(const void* fn, size_t smem, int dev, uint32_t blocks_per_sm, uin
   const uint64_t need = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
   return (int)std::max<uint64_t>(1, std::min(blocks, need));
 }
+
+// Clear a stale, non-sticky error left by an earlier runtime call (ours or the
+// host application's) so the post-launch check reports this launch only.
+void clear_stale_error() { (void)cudaGetLastError(); }
 
 void check_launch() {
   cudaError_t e = cudaGetLastError();
@@ -460,78 +474,176 @@ void check_common(uint64_t m, uint32_t a, uint64_t& ld, int layout, uint32_t max
                               " but records have arity " + std::to_string(a));
 }
 
+// ---- TMA tensor maps ---------------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return (EncodeTiledFn) nullptr;
+    }
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// Record staging plan for one launch.
+struct Staging {
+  int loader = kScalar;
+  uint32_t S = 1;           // records per lane per tile (tile = 32*S records)
+  uint32_t ns = 1;          // pipeline stages per warp
+  uint32_t stage_bytes = 0;
+  CUtensorMap tmap{};
+  size_t tile_smem() const {  // all warps' stages + their mbarriers
+    return loader == kDirect ? 0 : (size_t)kWarpsPerCta * ns * (stage_bytes + 8u);
+  }
+};
+
+uint32_t round1024(uint64_t b) { return (uint32_t)((b + 1023) & ~uint64_t(1023)); }
+
+// TMA applies to packed AoS, 16 B-aligned, with a tile of <= 256 rows of 32 floats.
+bool tma_ok(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout, uint32_t S) {
+  if (layout != ST_LAYOUT_AOS || ld != a) return false;
+  if ((reinterpret_cast<uintptr_t>(x) & 15u) != 0) return false;
+  if (32ull * S * a > 8192) return false;         // box rows = 32*S*a/32 <= 256
+  if (m < 32ull * S) return false;                 // no full tile: nothing for TMA to move
+  if (m * (uint64_t)a / 32 >= (1ull << 31)) return false;
+  return encode_tiled() != nullptr;
+}
+
+void make_tmap(Staging& st, const float* x, uint64_t m, uint32_t a) {
+  const cuuint64_t dims[2] = {32, (cuuint64_t)(m * (uint64_t)a / 32)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {32, 32u * st.S * a / 32u};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_tiled()(&st.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x),
+                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+}
+
+// Choose loader, S and stages.  `fixed` = shared bytes needed besides the
+// record stages (tree / windows / counters).
+Staging plan_staging(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout, uint32_t S,
+                     uint32_t want_ns, size_t fixed, const DevProps& pr) {
+  Staging st;
+  st.S = S;
+  const bool tma = tma_ok(x, m, a, ld, layout, S);
+  st.loader = tma ? kTma : (layout == ST_LAYOUT_SOA ? kSoa : kScalar);
+  st.stage_bytes = round1024(32ull * S * a * 4);
+  if (tma) {
+    // ~100 KB per CTA so two CTAs (16 warps) share an SM: 2-4 stages per warp
+    // Two stages per warp (one tile walked, one in flight) measured best on
+    // C2: more bytes in flight per SM did not raise HBM throughput.
+    const uint32_t ns = want_ns ? want_ns : 2;
+    st.ns = std::max<uint32_t>(1, std::min<uint32_t>(ns, 8));
+    while (st.ns > 1 && fixed + 1024 + st.tile_smem() > pr.smem_optin) --st.ns;
+    make_tmap(st, x, m, a);
+  } else {
+    st.ns = 1;
+  }
+  if (fixed + 1024 + st.tile_smem() > pr.smem_optin) {
+    st.loader = kDirect;  // records too wide to stage: read features from global
+    st.S = 1;
+    st.ns = 1;
+  }
+  return st;
+}
+
+// Persistent-grid width: on large TMA-streamed inputs 2 CTAs (16 warps) per SM
+// saturate HBM and beat the occupancy maximum (C2 sweep, profiles/); small
+// inputs use every resident CTA to hide latency.
+uint32_t default_bps(uint32_t want, const Staging& st, uint64_t m, const DevProps& pr) {
+  if (want) return want;
+  if (st.loader != kTma) return 0;
+  const uint64_t tiles = m / (32ull * st.S);
+  return tiles >= (uint64_t)pr.sms * 2 * kWarpsPerCta * 16 ? 2u : 0u;
+}
+
+PipeArgs pipe_args(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout) {
+  PipeArgs p{};
+  p.x = x;
+  p.m = m;
+  p.a = a;
+  p.ld = (uint32_t)ld;
+  p.layout_soa = layout == ST_LAYOUT_SOA ? 1u : 0u;
+  return p;
+}
+
 // ---- data kernel dispatch ------------------------------------------------
 template <int A, int S, int TLOC, int LOADER, int CAP>
-void launch_data_t(const DataArgs& d, const ConstTree<CAP>* ct, size_t smem, int dev,
-                   uint32_t bps, cudaStream_t s) {
+void launch_data_t(const DataArgs& d, const Staging& stg, const ConstTree<CAP>* ct, size_t smem,
+                   int dev, uint32_t bps, cudaStream_t s) {
   auto fn = k_data<A, S, TLOC, LOADER, CAP>;
-  const uint64_t n_tiles = (d.m + 32 * S - 1) / (32 * S);
+  const uint64_t n_tiles = (d.p.m + 32 * S - 1) / (32 * S);
   const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles);
   static const ConstTree<1> dummy{};
+  clear_stale_error();
   if constexpr (CAP == 1) {
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(d, ct ? *ct : dummy);
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(d, stg.tmap, ct ? *ct : dummy);
   } else {
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(d, *ct);
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(d, stg.tmap, *ct);
   }
   check_launch();
 }
 
 template <int A, int S, int LOADER>
-void launch_data_tloc(int tloc, const DataArgs& d, const st_tree* t, size_t smem, int dev,
-                      uint32_t bps, cudaStream_t s) {
+void launch_data_tloc(int tloc, const DataArgs& d, const Staging& stg, const st_tree* t,
+                      size_t smem, int dev, uint32_t bps, cudaStream_t s) {
   switch (tloc) {
     case ST_TREE_SHARED:
-      return launch_data_t<A, S, kShared, LOADER, 1>(d, nullptr, smem, dev, bps, s);
+      return launch_data_t<A, S, kShared, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
     case ST_TREE_GLOBAL:
-      return launch_data_t<A, S, kGlobal, LOADER, 1>(d, nullptr, smem, dev, bps, s);
+      return launch_data_t<A, S, kGlobal, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
     case ST_TREE_CONSTANT: {
-      if constexpr (LOADER == kVec) {
+      if constexpr (LOADER == kTma) {
         if (t->compact.size() <= 512) {
           ConstTree<512> ct{};
           std::copy(t->compact.begin(), t->compact.end(), ct.n);
-          return launch_data_t<A, S, kConst, LOADER, 512>(d, &ct, smem, dev, bps, s);
+          return launch_data_t<A, S, kConst, LOADER, 512>(d, stg, &ct, smem, dev, bps, s);
         }
-        auto ct = std::make_unique<ConstTree<4064>>();
+        auto ct = std::make_unique<ConstTree<4000>>();
         std::copy(t->compact.begin(), t->compact.end(), ct->n);
-        return launch_data_t<A, S, kConst, LOADER, 4064>(d, ct.get(), smem, dev, bps, s);
+        return launch_data_t<A, S, kConst, LOADER, 4000>(d, stg, ct.get(), smem, dev, bps, s);
       }
       break;
     }
     default:
       break;
   }
-  return launch_data_t<A, S, kWide, LOADER, 1>(d, nullptr, smem, dev, bps, s);
+  return launch_data_t<A, S, kWide, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
 }
 
-template <int A, int LOADER>
-void launch_data_s(uint32_t S, int tloc, const DataArgs& d, const st_tree* t, size_t smem,
-                   int dev, uint32_t bps, cudaStream_t s) {
-  if constexpr (A == 8 || A == 16) {
-    if (S >= 4) return launch_data_tloc<A, 4, LOADER>(tloc, d, t, smem, dev, bps, s);
-    if (S == 2) return launch_data_tloc<A, 2, LOADER>(tloc, d, t, smem, dev, bps, s);
-  } else if constexpr (A == 19 || A == 32) {
-    if (S >= 2) return launch_data_tloc<A, 2, LOADER>(tloc, d, t, smem, dev, bps, s);
-  }
-  return launch_data_tloc<A, 1, LOADER>(tloc, d, t, smem, dev, bps, s);
-}
+// Compile-time arities with a TMA fast path; everything else runs A = 0.
+bool ct_arity(uint32_t a) { return a == 8 || a == 16 || a == 32 || a == 64; }
 
-uint32_t supported_S(uint32_t a, uint32_t want, bool vec) {
-  if (!vec) return 1;
-  uint32_t maxS = (a == 8 || a == 16) ? 4 : (a == 19 || a == 32) ? 2 : 1;
+uint32_t choose_S(uint32_t a, uint32_t want) {
+  // instantiated: a=8 {1,2,4}, a=16 {1,2}, a=32 {1,2}, others {1}
+  const uint32_t maxS = a == 8 ? 4 : (a == 16 || a == 32) ? 2 : 1;
   if (want == 0) want = a <= 8 ? 4 : a <= 16 ? 2 : 1;
   uint32_t S = 1;
   while (S * 2 <= std::min(want, maxS)) S *= 2;
   return S;
 }
 
-bool vec_arity(uint32_t a) { return a == 8 || a == 16 || a == 19 || a == 32 || a == 64; }
-
-uint32_t pitch_rt(uint32_t a, bool vec) {
-  if (vec) {
-    if ((a & (a - 1)) == 0 || a % 32 == 0) return a;
-    return (a & 1) ? a : a + 1;
+template <int A>
+void launch_data_a(const Staging& stg, int tloc, const DataArgs& d, const st_tree* t, size_t smem,
+                   int dev, uint32_t bps, cudaStream_t s) {
+  if constexpr (A == 8) {
+    if (stg.S == 4) return launch_data_tloc<A, 4, kTma>(tloc, d, stg, t, smem, dev, bps, s);
   }
-  return a | 1u;
+  if constexpr (A == 8 || A == 16 || A == 32) {
+    if (stg.S == 2) return launch_data_tloc<A, 2, kTma>(tloc, d, stg, t, smem, dev, bps, s);
+  }
+  return launch_data_tloc<A, 1, kTma>(tloc, d, stg, t, smem, dev, bps, s);
 }
 
 void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
@@ -539,10 +651,7 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   st_tree::Dev& dv = t->device(dev);
   const DevProps pr = dev_props(dev);
   DataArgs d{};
-  d.x = x;
-  d.m = m;
-  d.a = a;
-  d.ld = (uint32_t)ld;
+  d.p = pipe_args(x, m, a, ld, layout);
   d.nodes = dv.compact;
   d.wide = dv.wide;
   d.n_nodes = (uint32_t)t->nodes.size();
@@ -550,58 +659,76 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.leaf_class = dv.leaf_tbl;
   d.labels = labels;
 
-  const bool vec = layout == ST_LAYOUT_AOS && ld == a && vec_arity(a) &&
-                   (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-  int loader = layout == ST_LAYOUT_SOA ? kSoa : vec ? kVec : kScalar;
-  const uint32_t S = supported_S(a, g.samples_per_thread, loader == kVec);
-  const uint32_t p = pitch_rt(a, loader == kVec);
-  size_t tile_bytes = (size_t)kWarpsPerCta * 32 * S * p * 4;
-  const size_t tree_bytes = ((t->nodes.size() * sizeof(CNode) + 15) & ~size_t(15));
+  const uint32_t tree_bytes = round1024(t->nodes.size() * sizeof(CNode));
   int tloc = g.tree_loc;
-  if (!t->compact_ok) tloc = ST_TREE_GLOBAL + 1;  // wide
-  else if (tloc == ST_TREE_AUTO)
-    tloc = tree_bytes + tile_bytes <= std::min<size_t>(pr.smem_optin, 200 * 1024) ? ST_TREE_SHARED
-                                                                                 : ST_TREE_GLOBAL;
-  if (tloc == ST_TREE_CONSTANT && (loader != kVec || t->compact.size() > 4064)) tloc = ST_TREE_GLOBAL;
-  if (tloc == ST_TREE_SHARED && tree_bytes + tile_bytes > pr.smem_optin) tloc = ST_TREE_GLOBAL;
-  if (tloc != ST_TREE_SHARED && tile_bytes > pr.smem_optin) {
-    loader = kDirect;
-    tile_bytes = 0;
+  if (!t->compact_ok) tloc = kWide;
+  else if (tloc == ST_TREE_AUTO) tloc = tree_bytes <= 96 * 1024 ? ST_TREE_SHARED : ST_TREE_GLOBAL;
+  if (tloc == ST_TREE_CONSTANT && t->compact.size() > 4000) tloc = ST_TREE_GLOBAL;
+  const uint32_t S0 = ct_arity(a) ? choose_S(a, g.samples_per_thread) : 1;
+  Staging stg = plan_staging(x, m, a, ld, layout, S0, g.stages,
+                             tloc == ST_TREE_SHARED ? tree_bytes : 0, pr);
+  if (tloc == ST_TREE_SHARED && tree_bytes + 1024 + stg.tile_smem() > pr.smem_optin) {
+    tloc = ST_TREE_GLOBAL;
+    stg = plan_staging(x, m, a, ld, layout, S0, g.stages, 0, pr);
   }
-  const size_t smem = (tloc == ST_TREE_SHARED ? tree_bytes : 0) + (loader == kDirect ? 0 : tile_bytes);
-  const uint32_t bps = g.blocks_per_sm;
-  if (loader == kVec) {
+  if (tloc == ST_TREE_CONSTANT && stg.loader != kTma) tloc = ST_TREE_GLOBAL;
+  d.ns = stg.ns;
+  d.stage_bytes = stg.stage_bytes;
+  d.tree_bytes = tloc == ST_TREE_SHARED ? tree_bytes : 0;
+  const size_t smem = 1024 + d.tree_bytes + stg.tile_smem();
+  const uint32_t bps = default_bps(g.blocks_per_sm, stg, m, pr);
+  if (stg.loader == kTma && ct_arity(a)) {
     switch (a) {
-      case 8: return launch_data_s<8, kVec>(S, tloc, d, t, smem, dev, bps, s);
-      case 16: return launch_data_s<16, kVec>(S, tloc, d, t, smem, dev, bps, s);
-      case 19: return launch_data_s<19, kVec>(S, tloc, d, t, smem, dev, bps, s);
-      case 32: return launch_data_s<32, kVec>(S, tloc, d, t, smem, dev, bps, s);
-      case 64: return launch_data_s<64, kVec>(S, tloc, d, t, smem, dev, bps, s);
+      case 8: return launch_data_a<8>(stg, tloc, d, t, smem, dev, bps, s);
+      case 16: return launch_data_a<16>(stg, tloc, d, t, smem, dev, bps, s);
+      case 32: return launch_data_a<32>(stg, tloc, d, t, smem, dev, bps, s);
+      case 64: return launch_data_a<64>(stg, tloc, d, t, smem, dev, bps, s);
     }
   }
-  if (tloc == ST_TREE_CONSTANT) tloc = ST_TREE_GLOBAL;
-  switch (loader) {
-    case kSoa: return launch_data_tloc<0, 1, kSoa>(tloc, d, t, smem, dev, bps, s);
-    case kDirect: return launch_data_tloc<0, 1, kDirect>(tloc, d, t, smem, dev, bps, s);
-    default: return launch_data_tloc<0, 1, kScalar>(tloc, d, t, smem, dev, bps, s);
+  switch (stg.loader) {
+    case kTma: return launch_data_tloc<0, 1, kTma>(tloc, d, stg, t, smem, dev, bps, s);
+    case kDirect:
+      return launch_data_tloc<0, 1, kDirect>(tloc == ST_TREE_CONSTANT ? ST_TREE_GLOBAL : tloc, d,
+                                             stg, t, smem, dev, bps, s);
+    default:
+      return launch_data_tloc<0, 1, kScalar>(tloc == ST_TREE_CONSTANT ? ST_TREE_GLOBAL : tloc, d,
+                                             stg, t, smem, dev, bps, s);
   }
 }
 
 // ---- speculative kernel dispatch -----------------------------------------
-template <int A, int LOADER>
-void launch_spec_t(bool win_shared, const SpecArgs& sa, size_t smem, int dev, uint32_t bps,
+template <int A, int LOADER, bool WS, bool EXACT, int STEPS>
+void launch_spec_k(const SpecArgs& sa, const Staging& stg, size_t smem, int dev, uint32_t bps,
                    cudaStream_t s) {
-  const uint64_t n_tiles = (sa.m + 31) / 32;
-  if (win_shared) {
-    auto fn = k_spec<A, LOADER, true>;
-    const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles);
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(sa);
-  } else {
-    auto fn = k_spec<A, LOADER, false>;
-    const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles);
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(sa);
-  }
+  auto fn = k_spec<A, LOADER, WS, EXACT, STEPS>;
+  const uint64_t n_tiles = (sa.p.m + 31) / 32;
+  const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles);
+  clear_stale_error();
+  fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(sa, stg.tmap);
   check_launch();
+}
+
+// Fast path: the doubling count is a compile-time constant for the usual
+// window heights (steps 0..3); EXACT (reference counters) and taller windows
+// use a runtime count.
+template <int A, int LOADER, bool WS>
+void launch_spec_steps(const SpecArgs& sa, const Staging& stg, size_t smem, int dev, uint32_t bps,
+                       cudaStream_t s) {
+  if (sa.iters) return launch_spec_k<A, LOADER, WS, true, -1>(sa, stg, smem, dev, bps, s);
+  switch (sa.smax) {
+    case 0: return launch_spec_k<A, LOADER, WS, false, 0>(sa, stg, smem, dev, bps, s);
+    case 1: return launch_spec_k<A, LOADER, WS, false, 1>(sa, stg, smem, dev, bps, s);
+    case 2: return launch_spec_k<A, LOADER, WS, false, 2>(sa, stg, smem, dev, bps, s);
+    case 3: return launch_spec_k<A, LOADER, WS, false, 3>(sa, stg, smem, dev, bps, s);
+    default: return launch_spec_k<A, LOADER, WS, false, -1>(sa, stg, smem, dev, bps, s);
+  }
+}
+
+template <int A, int LOADER>
+void launch_spec_t(bool win_shared, const SpecArgs& sa, const Staging& stg, size_t smem, int dev,
+                   uint32_t bps, cudaStream_t s) {
+  if (win_shared) return launch_spec_steps<A, LOADER, true>(sa, stg, smem, dev, bps, s);
+  return launch_spec_steps<A, LOADER, false>(sa, stg, smem, dev, bps, s);
 }
 
 void spec_geometry(const st_tree* t, const st_geom& g, uint32_t& G, uint32_t& H) {
@@ -634,21 +761,19 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
                       const st_geom& g, uint32_t* labels, st_stats* stats, cudaStream_t s, int dev) {
   uint32_t G, H;
   spec_geometry(t, g, G, H);
-  if (t->info.max_attribute >= (1u << 24))
-    fail(ST_ERR_ARGUMENT, "speculative kernel requires attribute indices < 2^24");
+  if (4ull * t->info.max_attribute >= (1u << 24))
+    fail(ST_ERR_ARGUMENT, "speculative kernel requires attribute indices < 2^22");
   auto wt = t->windows(G, H);
   SEntry* wdev = t->device_windows(dev, G, H, *wt);
   st_tree::Dev& dv = t->device(dev);
   const DevProps pr = dev_props(dev);
   SpecArgs sa{};
-  sa.x = x;
-  sa.m = m;
-  sa.a = a;
-  sa.ld = (uint32_t)ld;
+  sa.p = pipe_args(x, m, a, ld, layout);
   sa.win = wdev;
   sa.n_entries = (uint32_t)wt->entries.size();
   sa.root_code = wt->root_code;
   sa.G = G;
+  sa.smax = wt->max_steps;
   sa.k = g.reductions;
   sa.leaf_class = dv.leaf_tbl;
   sa.labels = labels;
@@ -656,33 +781,37 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     sa.iters = stats->iterations;
     sa.steps = stats->doubling_steps;
     if (!sa.iters || !sa.steps) fail(ST_ERR_ARGUMENT, "st_stats requires both arrays");
+    if (sa.k == 0) sa.k = 1;  // counters follow the reference loop (k per root check)
+  } else if (sa.k != 0) {
+    // k without counters: same labels; the fixed-step path is used
+    sa.k = 0;
   }
-  const bool vec = layout == ST_LAYOUT_AOS && ld == a && vec_arity(a) &&
-                   (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-  int loader = layout == ST_LAYOUT_SOA ? kSoa : vec ? kVec : kScalar;
-  const uint32_t p = pitch_rt(a, loader == kVec);
-  size_t tile_bytes = (size_t)kWarpsPerCta * 32 * p * 4;
-  const size_t win_bytes = wt->entries.size() * sizeof(SEntry);
-  bool win_shared = win_bytes + tile_bytes <= std::min<size_t>(pr.smem_optin, 160 * 1024);
-  if (!win_shared && tile_bytes > pr.smem_optin) {
-    loader = kDirect;
-    tile_bytes = 0;
+  const uint32_t win_bytes = round1024(wt->entries.size() * sizeof(SEntry));
+  bool win_shared = win_bytes <= 96 * 1024;
+  Staging stg = plan_staging(x, m, a, ld, layout, 1, g.stages, win_shared ? win_bytes : 0, pr);
+  if (win_shared && win_bytes + 1024 + stg.tile_smem() > pr.smem_optin) {
+    win_shared = false;
+    stg = plan_staging(x, m, a, ld, layout, 1, g.stages, 0, pr);
   }
-  const size_t smem = (win_shared ? win_bytes : 0) + (loader == kDirect ? 0 : tile_bytes);
-  const uint32_t bps = g.blocks_per_sm;
-  if (loader == kVec) {
+  sa.win_bytes = win_shared ? win_bytes : 0;
+  if (stg.loader == kDirect) stg.ns = 1, stg.stage_bytes = 0;
+  sa.ns = stg.ns;
+  sa.stage_bytes = stg.stage_bytes;
+  const size_t smem = 1024 + sa.win_bytes + (size_t)kWarpsPerCta * stg.ns * (stg.stage_bytes + 8u) +
+                      (size_t)kWarpsPerCta * 3 * 128;  // + per-warp label/counter rows
+  const uint32_t bps = g.blocks_per_sm;  // speculative is issue-bound: keep every resident CTA
+  if (stg.loader == kTma && ct_arity(a)) {
     switch (a) {
-      case 8: return launch_spec_t<8, kVec>(win_shared, sa, smem, dev, bps, s);
-      case 16: return launch_spec_t<16, kVec>(win_shared, sa, smem, dev, bps, s);
-      case 19: return launch_spec_t<19, kVec>(win_shared, sa, smem, dev, bps, s);
-      case 32: return launch_spec_t<32, kVec>(win_shared, sa, smem, dev, bps, s);
-      case 64: return launch_spec_t<64, kVec>(win_shared, sa, smem, dev, bps, s);
+      case 8: return launch_spec_t<8, kTma>(win_shared, sa, stg, smem, dev, bps, s);
+      case 16: return launch_spec_t<16, kTma>(win_shared, sa, stg, smem, dev, bps, s);
+      case 32: return launch_spec_t<32, kTma>(win_shared, sa, stg, smem, dev, bps, s);
+      case 64: return launch_spec_t<64, kTma>(win_shared, sa, stg, smem, dev, bps, s);
     }
   }
-  switch (loader) {
-    case kSoa: return launch_spec_t<0, kSoa>(win_shared, sa, smem, dev, bps, s);
-    case kDirect: return launch_spec_t<0, kDirect>(win_shared, sa, smem, dev, bps, s);
-    default: return launch_spec_t<0, kScalar>(win_shared, sa, smem, dev, bps, s);
+  switch (stg.loader) {
+    case kTma: return launch_spec_t<0, kTma>(win_shared, sa, stg, smem, dev, bps, s);
+    case kDirect: return launch_spec_t<0, kDirect>(win_shared, sa, stg, smem, dev, bps, s);
+    default: return launch_spec_t<0, kScalar>(win_shared, sa, stg, smem, dev, bps, s);
   }
 }
 
@@ -713,16 +842,19 @@ void eval_device_impl(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
 
 // ---- forest ----------------------------------------------------------------
 template <int A, int LOADER>
-void launch_forest_t(bool packed, const ForestArgs& fa, size_t smem, int dev, cudaStream_t s) {
-  const uint64_t n_tiles = (fa.m + 31) / 32;
+void launch_forest_t(bool packed, const ForestArgs& fa, const Staging& stg, size_t smem, int dev,
+                     cudaStream_t s) {
+  const uint64_t n_tiles = (fa.p.m + 31) / 32;
   if (packed) {
     auto fn = k_forest<A, LOADER, true>;
     const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles);
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(fa);
+    clear_stale_error();
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(fa, stg.tmap);
   } else {
     auto fn = k_forest<A, LOADER, false>;
     const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles);
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(fa);
+    clear_stale_error();
+    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(fa, stg.tmap);
   }
   check_launch();
 }
@@ -737,10 +869,7 @@ void forest_device_impl(st_forest* f, const float* x, uint64_t m, uint32_t a, ui
   const DevProps pr = dev_props(dev);
   st_forest::Dev& dv = f->device(dev);
   ForestArgs fa{};
-  fa.x = x;
-  fa.m = m;
-  fa.a = a;
-  fa.ld = (uint32_t)ld;
+  fa.p = pipe_args(x, m, a, ld, layout);
   fa.nodes = dv.nodes;
   fa.offsets = dv.offsets;
   fa.t_count = f->t_count;
@@ -748,30 +877,23 @@ void forest_device_impl(st_forest* f, const float* x, uint64_t m, uint32_t a, ui
   fa.abits = f->abits;
   fa.labels = labels;
   const bool packed = f->n_classes <= 8 && f->t_count <= 255;
-  const bool vec = layout == ST_LAYOUT_AOS && ld == a && vec_arity(a) &&
-                   (reinterpret_cast<uintptr_t>(x) % 16) == 0;
-  int loader = layout == ST_LAYOUT_SOA ? kSoa : vec ? kVec : kScalar;
-  const uint32_t p = pitch_rt(a, loader == kVec);
-  size_t tile_bytes = (size_t)kWarpsPerCta * 32 * p * 4;
   const size_t cnt_bytes = packed ? 0 : (size_t)kWarpsPerCta * 32 * f->n_classes * 4;
-  if (tile_bytes + cnt_bytes > pr.smem_optin) {
-    loader = kDirect;
-    tile_bytes = 0;
-  }
-  const size_t smem = tile_bytes + cnt_bytes;
-  if (loader == kVec) {
+  Staging stg = plan_staging(x, m, a, ld, layout, 1, 0, cnt_bytes, pr);
+  fa.ns = stg.ns;
+  fa.stage_bytes = stg.stage_bytes;
+  const size_t smem = 1024 + stg.tile_smem() + cnt_bytes;
+  if (stg.loader == kTma && ct_arity(a)) {
     switch (a) {
-      case 8: return launch_forest_t<8, kVec>(packed, fa, smem, dev, s);
-      case 16: return launch_forest_t<16, kVec>(packed, fa, smem, dev, s);
-      case 19: return launch_forest_t<19, kVec>(packed, fa, smem, dev, s);
-      case 32: return launch_forest_t<32, kVec>(packed, fa, smem, dev, s);
-      case 64: return launch_forest_t<64, kVec>(packed, fa, smem, dev, s);
+      case 8: return launch_forest_t<8, kTma>(packed, fa, stg, smem, dev, s);
+      case 16: return launch_forest_t<16, kTma>(packed, fa, stg, smem, dev, s);
+      case 32: return launch_forest_t<32, kTma>(packed, fa, stg, smem, dev, s);
+      case 64: return launch_forest_t<64, kTma>(packed, fa, stg, smem, dev, s);
     }
   }
-  switch (loader) {
-    case kSoa: return launch_forest_t<0, kSoa>(packed, fa, smem, dev, s);
-    case kDirect: return launch_forest_t<0, kDirect>(packed, fa, smem, dev, s);
-    default: return launch_forest_t<0, kScalar>(packed, fa, smem, dev, s);
+  switch (stg.loader) {
+    case kTma: return launch_forest_t<0, kTma>(packed, fa, stg, smem, dev, s);
+    case kDirect: return launch_forest_t<0, kDirect>(packed, fa, stg, smem, dev, s);
+    default: return launch_forest_t<0, kScalar>(packed, fa, stg, smem, dev, s);
   }
 }
 
@@ -927,10 +1049,9 @@ int st_forest_create(const st_node* const* trees, const uint32_t* sizes, uint32_
       total += sizes[k];
     }
     f->max_attribute = maxattr;
-    f->abits = bits_for(maxattr);
     uint32_t maxn = 0;
     for (uint32_t k = 0; k < t; ++k) maxn = std::max(maxn, sizes[k]);
-    if (((uint64_t)maxn << f->abits) >= (1ull << 31) || total >= (1ull << 32))
+    if (!compact_fits(maxn, maxattr, &f->abits) || total >= (1ull << 32))
       fail(ST_ERR_ARGUMENT, "forest too large for the compact device format");
     f->compact.reserve(total);
     f->offsets.push_back(0);
@@ -940,7 +1061,7 @@ int st_forest_create(const st_node* const* trees, const uint32_t* sizes, uint32_
         if (nd.class_id != ST_NO_CLASS)
           f->compact.push_back(CNode{nd.threshold, kLeafBit | nd.class_id});
         else
-          f->compact.push_back(CNode{nd.threshold, (nd.child << f->abits) | nd.attribute});
+          f->compact.push_back(CNode{nd.threshold, ((8u * nd.child) << f->abits) | (4u * nd.attribute)});
       }
       f->offsets.push_back((uint32_t)f->compact.size());
     }

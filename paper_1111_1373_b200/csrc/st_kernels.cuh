@@ -8,18 +8,25 @@
 //               and resolves the path by shfl pointer-jumping.
 //   k_forest -- T trees per record with a per-record majority vote.
 //
-// All three share the record-tile stager: each warp streams tiles of 32*S
-// records HBM -> registers (coalesced 128-bit ld.global.nc, one tile of
-// prefetch in flight while the previous tile is walked) -> a per-warp shared
-// memory tile whose word-level XOR swizzle makes both the staging stores and
-// "all lanes read the same attribute" (every root visit) bank-conflict free.
+// Record staging (shared by all three): every warp owns a private ring of NS
+// shared-memory stages.  Lane 0 streams whole tiles of 32*S records from HBM
+// with TMA (cp.async.bulk.tensor.2d over the record matrix viewed as rows of
+// 32 floats, SWIZZLE_128B) completing on a per-stage mbarrier; the warp walks
+// stage i while stages i+1..i+NS-1 are in flight.  No registers hold
+// prefetched data and no instructions are spent on staging.  The 128B swizzle
+// spreads "all lanes read the same attribute of 32 records" (every root
+// visit) over 8 bank groups.  Non-TMA inputs (strided rows, SoA, unaligned
+// base, the partial last tile) are stored by the warp into the same swizzled
+// layout, so the walk code is identical.
 //
 // Semantics (bit-exact with the reference): successor = child + (x > thr)
 // with an ordered IEEE compare and no flush-to-zero (tree.hpp:51-54); build
 // without --use_fast_math / -ftz=true.
 #pragma once
-#include <cstdint>
+#include <cuda.h>  // CUtensorMap (type only; encoded on the host via the runtime entry point)
 #include <cuda_runtime.h>
+
+#include <cstdint>
 
 namespace stk {
 
@@ -28,18 +35,19 @@ constexpr uint32_t kExitBit = 0x40000000u;  // speculative code: exit to window
 constexpr uint32_t kNoClass = 0xFFFFFFFFu;
 constexpr int kWarpsPerCta = 8;
 
-// Compact 8-byte device node.  internal: meta = child << abits | attr (bit 31
-// clear); leaf: meta = kLeafBit | class (or | leaf ordinal when a class does
-// not fit in 31 bits; the host then passes a leaf-class table).
+// Compact 8-byte device node.  internal: meta = (8*child) << abits | 4*attr
+// (bit 31 clear; byte offsets so the walk does no scaling); leaf: meta =
+// kLeafBit | class (or | leaf ordinal when a class does not fit in 31 bits;
+// the host then passes a leaf-class table).
 struct __align__(8) CNode {
   float thr;
   uint32_t meta;
 };
 
 // Speculative window entry (16 B): lane j of a window evaluates one internal
-// node.  y = attr | steps << 24 (steps = doubling count that resolves this
-// window); z/w = left/right successor codes: < 32 lane index inside the
-// window, kExitBit | base of the next window, or kLeafBit | class/ordinal.
+// node.  attr_steps = 4*attr | steps << 24 (steps = doubling count that
+// resolves this window); left/right = successor codes: < 32 lane index inside
+// the window, kExitBit | base of the next window, kLeafBit | class/ordinal.
 struct __align__(16) SEntry {
   float thr;
   uint32_t attr_steps;
@@ -47,143 +55,201 @@ struct __align__(16) SEntry {
   uint32_t right;
 };
 
-enum Loader { kVec = 0, kScalar = 1, kSoa = 2, kDirect = 3 };
+enum Loader { kTma = 0, kScalar = 1, kSoa = 2, kDirect = 3 };
 enum TreeLoc { kShared = 1, kConst = 2, kGlobal = 3, kWide = 4 };
 
 // ---------------------------------------------------------------------------
-// Tile geometry.  A > 0: compile-time arity; A == 0: runtime arity.
+// PTX helpers (32-bit shared addresses)
 // ---------------------------------------------------------------------------
-template <int A>
-struct TileGeom {
-  static constexpr bool kPow2Small = A > 0 && (A & (A - 1)) == 0 && A <= 32;
-  static constexpr bool kMult32 = A > 0 && (A % 32) == 0;
-  static constexpr int kLog2 = A == 1 ? 0 : A == 2 ? 1 : A == 4 ? 2 : A == 8 ? 3 : A == 16 ? 4 : 5;
-  // row pitch in words
-  static __host__ __device__ __forceinline__ uint32_t pitch(uint32_t a_rt) {
-    if constexpr (kPow2Small || kMult32) return (uint32_t)A;
-    else if constexpr (A > 0) return (A & 1) ? A : A + 1;
-    else return a_rt | 1u;
-  }
-  // word offset of (row r, attribute a) inside a tile
-  static __device__ __forceinline__ uint32_t addr(uint32_t r, uint32_t a, uint32_t p) {
-    if constexpr (kPow2Small) {
-      return r * A + (a ^ ((r >> (5 - kLog2)) & (A - 1)));
-    } else if constexpr (kMult32) {
-      const uint32_t g = r * (A / 32) + (a >> 5);
-      return r * A + (a & ~31u) + ((a & 31u) ^ ((g + (g >> 5)) & 31u));
-    } else {
-      return r * p + a;
-    }
-  }
-};
-
-// Streaming 128-bit read-only load that does not allocate in L1.
-__device__ __forceinline__ float4 ld_stream(const float4* p) {
-  float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
   return v;
+}
+__device__ __forceinline__ uint2 lds_u2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_u4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// Byte offset of flat float f of a tile under SWIZZLE_128B (tile base
+// 1024-aligned): 16-byte chunk bits [4:6] XOR row bits [7:9].
+__device__ __forceinline__ uint32_t swz(uint32_t byte_off) {
+  return byte_off ^ ((byte_off >> 3) & 0x70u);
 }
 
 // ---------------------------------------------------------------------------
-// Per-warp tile stager.  Tile t covers records [t*R, t*R + R), R = 32*S.
+// Per-record feature accessor over a staged tile (or global for kDirect).
+// get(attr4) takes the attribute as a byte offset (4 * attribute).
 // ---------------------------------------------------------------------------
-template <int A, int S, int LOADER>
-struct Stager {
-  static constexpr int R = 32 * S;
-  // float4 per lane for a full vector tile (A compile-time only)
-  static constexpr int V = A > 0 ? (R * A / 4 + 31) / 32 : 1;
-  float4 buf[LOADER == kVec ? V : 1];
-
-  const float* __restrict__ x;
-  uint64_t m;
-  uint32_t a, ld, p;
-
-  __device__ __forceinline__ bool full(uint64_t t) const { return (t + 1) * (uint64_t)R <= m; }
-
-  // Issue the global loads of tile t into registers (vector path, full tiles).
-  __device__ __forceinline__ void prefetch(uint64_t t, int lane) {
-    if constexpr (LOADER == kVec) {
-      if (full(t)) {
-        const float4* src = reinterpret_cast<const float4*>(x + t * (uint64_t)R * A);
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          const int f4 = lane + 32 * k;
-          if ((R * A / 4) % 32 == 0 || f4 < R * A / 4) buf[k] = ld_stream(src + f4);
-        }
-      }
-    }
-  }
-
-  // Write tile t into the shared tile `s` (after prefetch for the vector path).
-  __device__ __forceinline__ void commit(uint64_t t, float* __restrict__ s, int lane) {
-    using Gm = TileGeom<A>;
-    if constexpr (LOADER == kVec) {
-      if (full(t)) {
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          const int f4 = lane + 32 * k;
-          if ((R * A / 4) % 32 == 0 || f4 < R * A / 4) {
-            const float vals[4] = {buf[k].x, buf[k].y, buf[k].z, buf[k].w};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const uint32_t f = 4u * f4 + c;
-              const uint32_t r = f / A, aa = f % A;
-              s[Gm::addr(r, aa, p)] = vals[c];
-            }
-          }
-        }
-        return;
-      }
-    }
-    if constexpr (LOADER == kSoa) {
-      // x[attr * ld + record]: one coalesced 128 B load per attribute and lane-row
-      const uint64_t r0 = t * (uint64_t)R;
-#pragma unroll
-      for (int q = 0; q < S; ++q) {
-        const uint32_t r = q * 32 + lane;
-        const bool ok = r0 + r < m;
-        for (uint32_t aa = 0; aa < a; ++aa)
-          s[Gm::addr(r, aa, p)] = ok ? __ldg(x + (uint64_t)aa * ld + r0 + r) : 0.0f;
-      }
-      return;
-    }
-    // scalar AoS path (runtime arity / strided rows / the partial last tile)
-    {
-      const uint64_t r0 = t * (uint64_t)R;
-      const uint32_t rows = (uint32_t)((m - r0) < (uint64_t)R ? (m - r0) : (uint64_t)R);
-      const uint32_t total = rows * a;
-      if (ld == a) {
-        const float* src = x + r0 * a;
-        for (uint32_t f = lane; f < total; f += 32) {
-          const uint32_t r = f / a, aa = f - r * a;
-          s[Gm::addr(r, aa, p)] = __ldg(src + f);
-        }
-      } else {
-        for (uint32_t f = lane; f < total; f += 32) {
-          const uint32_t r = f / a, aa = f - r * a;
-          s[Gm::addr(r, aa, p)] = __ldg(x + (r0 + r) * (uint64_t)ld + aa);
-        }
-      }
-    }
-  }
-};
-
-// Feature accessor for one record inside the staged tile (or in global
-// memory for the direct loader).
 template <int A, int LOADER>
-struct Feat {
-  const float* __restrict__ base;  // tile (shared) or record row (global)
-  uint32_t r, p;
-  __device__ __forceinline__ float operator()(uint32_t a) const {
-    if constexpr (LOADER == kDirect) return __ldg(base + a);
-    else return base[TileGeom<A>::addr(r, a, p)];
+struct Rec {
+  static constexpr bool kRowLocal = A > 0 && A <= 32 && (32 % A) == 0;  // record inside one 128 B row
+  uint32_t base, xm;
+  const char* gp;
+
+  __device__ __forceinline__ void init(uint32_t tile, uint32_t r, uint32_t a_rt, const float* x,
+                                       uint64_t row, uint32_t ld) {
+    if constexpr (LOADER == kDirect) {
+      gp = reinterpret_cast<const char*>(x + row * (uint64_t)ld);
+    } else if constexpr (kRowLocal) {
+      const uint32_t ra4 = r * (uint32_t)A * 4u;
+      const uint32_t rowb = ra4 & ~127u;
+      base = tile + rowb;
+      xm = ((rowb >> 3) & 0x70u) ^ (ra4 & 127u);
+    } else {
+      base = tile + r * (A > 0 ? (uint32_t)A : a_rt) * 4u;
+    }
+  }
+  __device__ __forceinline__ float get(uint32_t attr4) const {
+    if constexpr (LOADER == kDirect) {
+      return __ldg(reinterpret_cast<const float*>(gp + attr4));
+    } else if constexpr (kRowLocal) {
+      return lds_f32(base + (attr4 ^ xm));
+    } else {
+      const uint32_t f = base + attr4;
+      return lds_f32(f ^ ((f >> 3) & 0x70u));
+    }
   }
 };
 
 // ---------------------------------------------------------------------------
-// Tree access
+// Per-warp record pipeline.  Tile t covers records [t*R, t*R + R), R = 32*S.
+// ---------------------------------------------------------------------------
+struct PipeArgs {
+  const float* x;
+  uint64_t m;
+  uint32_t a, ld;
+  uint32_t layout_soa;
+};
+
+template <int A, int S, int LOADER>
+struct Pipe {
+  static constexpr int R = 32 * S;
+  uint32_t tiles, bars, stride_bytes, ns;
+  const CUtensorMap* tmap;
+  PipeArgs p;
+  int lane;
+
+  __device__ __forceinline__ uint32_t arity() const { return A > 0 ? (uint32_t)A : p.a; }
+  __device__ __forceinline__ bool full(uint64_t t) const { return (t + 1) * (uint64_t)R <= p.m; }
+  __device__ __forceinline__ uint32_t stage(uint32_t s) const { return tiles + s * stride_bytes; }
+
+  __device__ __forceinline__ void issue(uint64_t t, uint32_t s) {  // lane 0
+    const uint32_t bytes = R * arity() * 4u;
+    const uint32_t bar = bars + 8u * s;
+    mbar_arrive_expect_tx(bar, bytes);
+    tma_load_2d(stage(s), tmap, 0, (int)(t * (uint64_t)R * arity() / 32u), bar);
+  }
+
+  __device__ __forceinline__ void start(uint64_t first, uint64_t step, uint64_t n_tiles) {
+    if constexpr (LOADER == kTma) {
+      if (lane == 0) {
+        tma_prefetch_desc(tmap);
+        for (uint32_t s = 0; s < ns; ++s) mbar_init(bars + 8u * s, 1);
+        fence_barrier_init();
+        for (uint32_t s = 0; s < ns; ++s) {
+          const uint64_t t = first + s * step;
+          if (t < n_tiles && full(t)) issue(t, s);
+        }
+      }
+      __syncwarp();
+    }
+  }
+
+  // Make this warp's i-th tile (global index t) resident; returns its stage.
+  __device__ __forceinline__ uint32_t acquire(uint64_t i, uint64_t t) {
+    if constexpr (LOADER == kDirect) return 0;
+    const uint32_t s = (uint32_t)(i % ns);
+    const uint32_t dst = stage(s);
+    if constexpr (LOADER == kTma) {
+      if (full(t)) {
+        mbar_wait(bars + 8u * s, (uint32_t)((i / ns) & 1u));
+        return dst;
+      }
+    }
+    // warp-cooperative store into the swizzled layout (scalar / SoA / tail)
+    const uint32_t a = arity();
+    const uint64_t r0 = t * (uint64_t)R;
+    const uint32_t rows = (uint32_t)((p.m - r0) < (uint64_t)R ? (p.m - r0) : (uint64_t)R);
+    __syncwarp();
+    if (p.layout_soa) {
+      for (uint32_t aa = 0; aa < a; ++aa)
+        for (uint32_t r = lane; r < R; r += 32)
+          sts_f32(dst + swz((r * a + aa) * 4u),
+                  r < rows ? __ldg(p.x + (uint64_t)aa * p.ld + r0 + r) : 0.0f);
+    } else {
+      const uint32_t total = rows * a;
+      for (uint32_t f = lane; f < total; f += 32) {
+        const uint32_t r = f / a, aa = f - r * a;
+        sts_f32(dst + swz(f * 4u), __ldg(p.x + (r0 + r) * (uint64_t)p.ld + aa));
+      }
+    }
+    __syncwarp();
+    return dst;
+  }
+
+  // Done with this warp's i-th tile: refill its stage with tile t + ns*step.
+  __device__ __forceinline__ void release(uint64_t i, uint64_t t, uint64_t step, uint64_t n_tiles) {
+    __syncwarp();
+    if constexpr (LOADER == kTma) {
+      if (lane == 0) {
+        const uint64_t tn = t + ns * step;
+        if (tn < n_tiles && full(tn)) issue(tn, (uint32_t)(i % ns));
+      }
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Tree access (byte offsets: root at 0, child at meta >> abits)
 // ---------------------------------------------------------------------------
 template <int CAP>
 struct ConstTree {
@@ -192,118 +258,142 @@ struct ConstTree {
 
 template <int TLOC, int CAP>
 struct TreeRef {
-  const CNode* __restrict__ s;  // shared or global compact nodes
+  uint32_t s;                   // shared address of node 0
+  const char* g;                // global node array
   const ConstTree<CAP>* c;      // constant-bank copy
-  __device__ __forceinline__ CNode get(uint32_t i) const {
-    if constexpr (TLOC == kConst) return c->n[i];
-    else if constexpr (TLOC == kGlobal) {
-      const uint2 v = __ldg(reinterpret_cast<const uint2*>(s) + i);
-      return CNode{__uint_as_float(v.x), v.y};
+  __device__ __forceinline__ uint2 get(uint32_t off) const {
+    if constexpr (TLOC == kConst) {
+      const CNode n = *reinterpret_cast<const CNode*>(reinterpret_cast<const char*>(c->n) + off);
+      return make_uint2(__float_as_uint(n.thr), n.meta);
+    } else if constexpr (TLOC == kGlobal) {
+      return __ldg(reinterpret_cast<const uint2*>(g + off));
     } else {
-      return s[i];
+      return lds_u2(s + off);
     }
   }
 };
 
 struct DataArgs {
-  const float* x;
-  uint64_t m;
-  uint32_t a, ld;
+  PipeArgs p;
   const CNode* nodes;          // compact nodes (device global)
   const uint4* wide;           // original 16-byte nodes (kWide)
   uint32_t n_nodes;
-  uint32_t abits;              // attr field width in compact meta
+  uint32_t abits;              // attr field width (bytes) in compact meta
   const uint32_t* leaf_class;  // null: leaf meta carries the class
   uint32_t* labels;
+  uint32_t ns;                 // pipeline stages
+  uint32_t tree_bytes;         // shared bytes reserved for the node array (kShared)
+  uint32_t stage_bytes;        // stride between stages
 };
+
+// Shared-memory carve-out shared by the kernels:
+//   [tree | windows (1024-aligned)] [warps x ns stages] [warps x ns mbarriers]
+__device__ __forceinline__ uint32_t align1024(uint32_t a) { return (a + 1023u) & ~1023u; }
 
 // ---------------------------------------------------------------------------
 // K1: data decomposition
 // ---------------------------------------------------------------------------
 template <int A, int S, int TLOC, int LOADER, int CAP>
 __global__ void __launch_bounds__(kWarpsPerCta * 32)
-    k_data(const DataArgs args, const __grid_constant__ ConstTree<CAP> ctree) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  using Gm = TileGeom<A>;
+    k_data(const DataArgs args, const __grid_constant__ CUtensorMap tmap,
+           const __grid_constant__ ConstTree<CAP> ctree) {
+  extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int R = 32 * S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t p = Gm::pitch(args.a);
+  const uint32_t sbase = align1024(smem_u32(smem));
 
   // ---- stage the node array once per CTA --------------------------------
-  const CNode* tree_s = args.nodes;
-  size_t tree_bytes = 0;
   if constexpr (TLOC == kShared) {
-    tree_bytes = ((size_t)args.n_nodes * sizeof(CNode) + 15) & ~size_t(15);
     const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
-    uint4* dst = reinterpret_cast<uint4*>(smem);
-    const uint32_t n16 = (uint32_t)(tree_bytes / 16);
-    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
-    tree_s = reinterpret_cast<const CNode*>(smem);
+    const uint32_t n16 = (args.n_nodes * 8u + 15u) / 16u;
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
+      const uint4 v = __ldg(src + i);
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
+                   "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
+    }
     __syncthreads();
   }
-  TreeRef<TLOC, CAP> tree{tree_s, &ctree};
-  float* tile = reinterpret_cast<float*>(smem + tree_bytes) + (size_t)warp * R * p;
+  TreeRef<TLOC, CAP> tree{sbase, reinterpret_cast<const char*>(args.nodes), &ctree};
 
-  Stager<A, S, LOADER> st;
-  st.x = args.x;
-  st.m = args.m;
-  st.a = args.a;
-  st.ld = args.ld;
-  st.p = p;
+  Pipe<A, S, LOADER> pipe;
+  const uint32_t tiles0 = sbase + args.tree_bytes;
+  pipe.tiles = tiles0 + (uint32_t)warp * args.ns * args.stage_bytes;
+  pipe.bars = tiles0 + kWarpsPerCta * args.ns * args.stage_bytes + (uint32_t)warp * args.ns * 8u;
+  pipe.stride_bytes = args.stage_bytes;
+  pipe.ns = args.ns;
+  pipe.tmap = &tmap;
+  pipe.p = args.p;
+  pipe.lane = lane;
 
-  const uint64_t n_tiles = (args.m + R - 1) / R;
-  const uint64_t wstride = (uint64_t)gridDim.x * kWarpsPerCta;
-  uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
-  if (LOADER != kDirect && t < n_tiles) st.prefetch(t, lane);
+  const uint64_t m = args.p.m;
+  const uint64_t n_tiles = (m + R - 1) / R;
+  const uint64_t step = (uint64_t)gridDim.x * kWarpsPerCta;
+  const uint64_t first = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  pipe.start(first, step, n_tiles);
   const uint32_t amask = (1u << args.abits) - 1u;
 
-  for (; t < n_tiles; t += wstride) {
+  uint64_t i = 0;
+  for (uint64_t t = first; t < n_tiles; t += step, ++i) {
     const uint64_t r0 = t * (uint64_t)R;
-    if constexpr (LOADER != kDirect) {
-      __syncwarp();
-      st.commit(t, tile, lane);
-      __syncwarp();
-      if (t + wstride < n_tiles) st.prefetch(t + wstride, lane);
-    }
+    const uint32_t tile = pipe.acquire(i, t);
     if constexpr (TLOC == kWide) {
-      // generic 16-byte node path: the reference loop verbatim
+      // generic 16-byte node path: the reference loop (eval_serial.cpp:21-29)
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         const uint32_t r = q * 32 + lane;
-        Feat<A, LOADER> f{LOADER == kDirect ? args.x + (r0 + r) * (uint64_t)args.ld : tile, r, p};
-        if (r0 + r >= args.m) continue;
-        uint32_t i = 0;
+        if (r0 + r >= m) continue;
+        Rec<A, LOADER> rec;
+        rec.init(tile, r, args.p.a, args.p.x, r0 + r, args.p.ld);
         uint4 nd = __ldg(args.wide);
         while (nd.w == kNoClass) {
-          i = nd.z + (uint32_t)(f(nd.x) > __uint_as_float(nd.y));
-          nd = __ldg(args.wide + i);
+          const uint32_t c = nd.z + (uint32_t)(rec.get(nd.x * 4u) > __uint_as_float(nd.y));
+          nd = __ldg(args.wide + c);
         }
         args.labels[r0 + r] = nd.w;
       }
+    } else if constexpr (S == 1) {
+      const uint32_t r = lane;
+      const bool valid = r0 + r < m;
+      Rec<A, LOADER> rec;
+      rec.init(tile, r, args.p.a, args.p.x, r0 + (valid ? r : 0), args.p.ld);
+      uint2 nd = tree.get(0);
+      uint32_t meta = valid ? nd.y : kLeafBit;
+      float thr = __uint_as_float(nd.x);
+      // Branch-free successor per level: child + (x > thr), as byte offsets.
+      while (!(meta & kLeafBit)) {
+        const float v = rec.get(meta & amask);
+        nd = tree.get((meta >> args.abits) + (v > thr ? 8u : 0u));
+        thr = __uint_as_float(nd.x);
+        meta = nd.y;
+      }
+      if (valid) {
+        const uint32_t c = meta & ~kLeafBit;
+        args.labels[r0 + r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+      }
     } else {
+      Rec<A, LOADER> rec[S];
       float thr[S];
       uint32_t meta[S];
-      const CNode root = tree.get(0);
+      const uint2 root = tree.get(0);
 #pragma unroll
       for (int q = 0; q < S; ++q) {
-        thr[q] = root.thr;
-        meta[q] = root.meta;
-        if (r0 + q * 32 + lane >= args.m) meta[q] = kLeafBit;  // idle lane-slot
+        const uint32_t r = q * 32 + lane;
+        rec[q].init(tile, r, args.p.a, args.p.x, r0 + (r0 + r < m ? r : 0), args.p.ld);
+        thr[q] = __uint_as_float(root.x);
+        meta[q] = (r0 + r < m) ? root.y : kLeafBit;  // idle slot in the tail tile
       }
-      // Branch-free successor per level; a lane leaves the loop once all its
-      // S walks sit on leaves (warp pays its slowest record per tile).
+      // Branch-free successor per level: child + (x > thr), as byte offsets.
       while (true) {
         bool any = false;
 #pragma unroll
         for (int q = 0; q < S; ++q) {
           if (!(meta[q] & kLeafBit)) {
-            const uint32_t r = q * 32 + lane;
-            Feat<A, LOADER> f{LOADER == kDirect ? args.x + (r0 + r) * (uint64_t)args.ld : tile, r, p};
-            const float v = f(meta[q] & amask);
-            const uint32_t i = (meta[q] >> args.abits) + (uint32_t)(v > thr[q]);
-            const CNode nd = tree.get(i);
-            thr[q] = nd.thr;
-            meta[q] = nd.meta;
+            const float v = rec[q].get(meta[q] & amask);
+            const uint32_t off = (meta[q] >> args.abits) + (v > thr[q] ? 8u : 0u);
+            const uint2 nd = tree.get(off);
+            thr[q] = __uint_as_float(nd.x);
+            meta[q] = nd.y;
             any = true;
           }
         }
@@ -312,12 +402,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         const uint64_t r = r0 + q * 32 + lane;
-        if (r < args.m) {
+        if (r < m) {
           const uint32_t c = meta[q] & ~kLeafBit;
           args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
         }
       }
     }
+    pipe.release(i, t, step, n_tiles);
   }
 }
 
@@ -325,133 +416,174 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 // K2: speculative decomposition with shfl pointer-jumping
 // ---------------------------------------------------------------------------
 struct SpecArgs {
-  const float* x;
-  uint64_t m;
-  uint32_t a, ld;
+  PipeArgs p;
   const SEntry* win;     // window table (device global), padded by 32 entries
   uint32_t n_entries;    // incl. padding
-  uint32_t root_code;    // code of the root: kExitBit|0, or kLeafBit|class for N == 1
+  uint32_t root_code;    // kExitBit | 0 (root window), or kLeafBit|class for N == 1
   uint32_t G;            // lanes per record group (power of two <= 32)
-  uint32_t k;            // 0: fixed per-window steps; >=1: check root every k steps
+  uint32_t smax;         // doubling steps that resolve every window (fast path)
+  uint32_t k;            // EXACT path: check the root after every k doublings
   const uint32_t* leaf_class;
   uint32_t* labels;
-  uint32_t* iters;       // nullable per-record counters
+  uint32_t* iters;       // EXACT path: per-record counters
   uint32_t* steps;
+  uint32_t ns, win_bytes, stage_bytes;
 };
 
-template <int A, int LOADER, bool WIN_SHARED>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_spec(const SpecArgs args) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  using Gm = TileGeom<A>;
+// Window codes: lane index (< 32), kExitBit | byte offset of the next
+// window's first entry, or kLeafBit | class.  Every lane of a record group
+// evaluates its window node's predicate (speculatively: all of them, not
+// just the ones on the path), then ceil(log2 h) __shfl_sync pointer-jumping
+// steps contract the successor chains inside the group (a single shfl reads
+// every source before any lane writes: the snapshot semantics of
+// path_double_step, eval_speculative.cpp:38-51); group lane 0 then holds the
+// exit.  EXACT reproduces the reference barrier-separated loop and its
+// per-record counters: while the root is unresolved apply k doublings
+// (eval_speculative.cpp:170-181).
+template <int A, int LOADER, bool WIN_SHARED, bool EXACT, int STEPS>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    k_spec(const SpecArgs args, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int R = 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t p = Gm::pitch(args.a);
+  const uint32_t sbase = align1024(smem_u32(smem));
 
-  const SEntry* win = args.win;
-  size_t win_bytes = 0;
   if constexpr (WIN_SHARED) {
-    win_bytes = (size_t)args.n_entries * sizeof(SEntry);
     const uint4* src = reinterpret_cast<const uint4*>(args.win);
-    uint4* dst = reinterpret_cast<uint4*>(smem);
-    for (uint32_t i = threadIdx.x; i < args.n_entries; i += blockDim.x) dst[i] = __ldg(src + i);
-    win = reinterpret_cast<const SEntry*>(smem);
+    for (uint32_t i = threadIdx.x; i < args.n_entries; i += blockDim.x) {
+      const uint4 v = __ldg(src + i);
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
+                   "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
+    }
     __syncthreads();
   }
-  float* tile = reinterpret_cast<float*>(smem + win_bytes) + (size_t)warp * R * p;
 
-  Stager<A, 1, LOADER> st;
-  st.x = args.x;
-  st.m = args.m;
-  st.a = args.a;
-  st.ld = args.ld;
-  st.p = p;
+  Pipe<A, 1, LOADER> pipe;
+  const uint32_t tiles0 = sbase + args.win_bytes;
+  pipe.tiles = tiles0 + (uint32_t)warp * args.ns * args.stage_bytes;
+  pipe.bars = tiles0 + kWarpsPerCta * args.ns * args.stage_bytes + (uint32_t)warp * args.ns * 8u;
+  pipe.stride_bytes = args.stage_bytes;
+  pipe.ns = args.ns;
+  pipe.tmap = &tmap;
+  pipe.p = args.p;
+  pipe.lane = lane;
+  // per-warp label (and counter) buffer: one row of 32 records, written
+  // coalesced to HBM once per tile
+  const uint32_t lbuf = tiles0 + kWarpsPerCta * args.ns * (args.stage_bytes + 8u) +
+                        (uint32_t)warp * 3u * 128u;
 
   const uint32_t G = args.G;
-  const uint32_t NG = 32u / G;       // record groups per warp
-  const uint32_t g = lane / G;       // my group
-  const uint32_t j = lane & (G - 1); // my lane in the group = window-local node
-  const uint32_t gbase = g * G;
-  const bool counting = args.iters != nullptr;
+  const uint32_t NG = 32u / G;        // record groups per warp
+  const uint32_t g = lane / G;        // my group
+  const uint32_t j = lane & (G - 1);  // my lane in the group = window-local node
+  const uint32_t gmask = G - 1;
+  // byte address of my entry in window 0 (codes carry window byte offsets)
+  const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + 16u * j;
+  const char* wglob = reinterpret_cast<const char*>(args.win) + 16u * j;
+  const bool root_leaf = (args.root_code & kLeafBit) != 0;
 
-  const uint64_t n_tiles = (args.m + R - 1) / R;
-  const uint64_t wstride = (uint64_t)gridDim.x * kWarpsPerCta;
-  uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
-  if (LOADER != kDirect && t < n_tiles) st.prefetch(t, lane);
+  const uint64_t m = args.p.m;
+  const uint64_t n_tiles = (m + R - 1) / R;
+  const uint64_t step = (uint64_t)gridDim.x * kWarpsPerCta;
+  const uint64_t first = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  pipe.start(first, step, n_tiles);
 
-  for (; t < n_tiles; t += wstride) {
+  uint64_t i = 0;
+  for (uint64_t t = first; t < n_tiles; t += step, ++i) {
     const uint64_t r0 = t * (uint64_t)R;
-    if constexpr (LOADER != kDirect) {
-      __syncwarp();
-      st.commit(t, tile, lane);
-      __syncwarp();
-      if (t + wstride < n_tiles) st.prefetch(t + wstride, lane);
-    }
-    const uint32_t rows = (uint32_t)((args.m - r0) < (uint64_t)R ? (args.m - r0) : (uint64_t)R);
-    // Group g classifies tile rows g, g+NG, ...; a finished group refills
-    // with its next row immediately, so skewed depths do not idle it.
-    uint32_t r = g;
-    uint32_t code = args.root_code;  // current window (exit code) or leaf
-    bool active = r < rows;
-    uint32_t n_it = 0, n_st = 0;
-    while (__any_sync(0xffffffffu, active)) {
-      const uint32_t rr = active ? r : 0u;
-      const uint32_t base = code & ~(kExitBit | kLeafBit);
-      const bool evaluating = active && !(code & kLeafBit);
-      // -- node evaluation: every window lane computes its successor --------
-      const SEntry e = win[(evaluating ? base : 0u) + j];
-      Feat<A, LOADER> f{LOADER == kDirect ? args.x + (r0 + rr) * (uint64_t)args.ld : tile, rr, p};
-      const float v = f(e.attr_steps & 0x00FFFFFFu);
-      uint32_t c = (v > e.thr) ? e.right : e.left;
-      // -- path reduction: shfl pointer-jumping inside the group ------------
-      const uint32_t wsteps = __shfl_sync(0xffffffffu, e.attr_steps >> 24, gbase);
-      if (args.k == 0) {
-        const uint32_t smax = __reduce_max_sync(0xffffffffu, evaluating ? wsteps : 0u);
-        for (uint32_t s = 0; s < smax; ++s) {
-          const uint32_t u = __shfl_sync(0xffffffffu, c, c & (G - 1), G);
-          if (c < 32u) c = u;
-        }
-        if (counting && evaluating) {
-          n_it += 1;
-          n_st += wsteps;
-        }
-      } else {
-        // reference barrier_separated loop: while root unresolved, k doublings
-        while (true) {
-          const uint32_t root = __shfl_sync(0xffffffffu, c, gbase);
-          const bool need = evaluating && root < 32u;
-          if (!__any_sync(0xffffffffu, need)) break;
-          for (uint32_t s = 0; s < args.k; ++s) {
-            const uint32_t u = __shfl_sync(0xffffffffu, c, c & (G - 1), G);
-            if (need && c < 32u) c = u;
-          }
-          if (need) {
-            n_it += 1;
-            n_st += args.k;
-          }
+    const uint32_t tile = pipe.acquire(i, t);
+    const uint32_t rows = (uint32_t)((m - r0) < (uint64_t)R ? (m - r0) : (uint64_t)R);
+    if (root_leaf) {  // N == 1: every record is the root's class, zero reductions
+      if (lane < rows) {
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * lane), "r"(args.root_code) : "memory");
+        if constexpr (EXACT) {
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 128u + 4u * lane), "r"(0u) : "memory");
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 256u + 4u * lane), "r"(0u) : "memory");
         }
       }
-      const uint32_t root = __shfl_sync(0xffffffffu, c, gbase);
-      if (active) {
-        const uint32_t next = evaluating ? root : code;
-        if (next & kLeafBit) {
-          if (j == 0) {
-            const uint32_t cls = next & ~kLeafBit;
-            const uint64_t out = r0 + r;
-            args.labels[out] = args.leaf_class ? __ldg(args.leaf_class + cls) : cls;
-            if (counting) {
-              args.iters[out] = n_it;
-              args.steps[out] = n_st;
+    } else {
+      // Group g classifies tile rows g, g+NG, ...; a finished group refills
+      // with its next row immediately, so skewed depths do not idle it.
+      uint32_t r = g;
+      bool active = r < rows;
+      uint32_t woff = 0;  // byte offset of the current window
+      uint32_t n_it = 0, n_st = 0;
+      Rec<A, LOADER> rec;
+      rec.init(tile, active ? r : 0u, args.p.a, args.p.x, r0 + (active ? r : 0u), args.p.ld);
+      do {
+        // -- node evaluation: every window lane computes its successor ------
+        uint4 e;
+        if constexpr (WIN_SHARED) e = lds_u4(jaddr + woff);
+        else e = __ldg(reinterpret_cast<const uint4*>(wglob + woff));
+        const float v = rec.get(e.y & 0x00FFFFFFu);
+        uint32_t c = (v > __uint_as_float(e.x)) ? e.w : e.z;
+        // -- path reduction: shfl pointer-jumping inside the group ----------
+        if constexpr (!EXACT) {
+          if constexpr (STEPS >= 0) {
+#pragma unroll
+            for (int s = 0; s < STEPS; ++s) {
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              c = (c < 32u) ? u : c;
+            }
+          } else {
+            for (uint32_t s = 0; s < args.smax; ++s) {
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              c = (c < 32u) ? u : c;
+            }
+          }
+        } else {
+          // Every group (idle ones included) doubles until its root is
+          // resolved, so its exit code is a valid window offset; only active
+          // groups count.
+          while (true) {
+            const uint32_t rt = __shfl_sync(0xffffffffu, c, 0, G);
+            const bool need = rt < 32u;
+            if (!__any_sync(0xffffffffu, need)) break;
+            for (uint32_t s = 0; s < args.k; ++s) {
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              if (need && c < 32u) c = u;
+            }
+            if (need && active) {
+              n_it += 1;
+              n_st += args.k;
+            }
+          }
+        }
+        const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
+        if (root & kLeafBit) {
+          if (active && j == 0) {
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(root) : "memory");
+            if constexpr (EXACT) {
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 128u + 4u * r), "r"(n_it) : "memory");
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 256u + 4u * r), "r"(n_st) : "memory");
             }
           }
           n_it = n_st = 0;
           r += NG;
-          code = args.root_code;
           active = r < rows;
+          woff = 0;
+          rec.init(tile, active ? r : 0u, args.p.a, args.p.x, r0 + (active ? r : 0u), args.p.ld);
         } else {
-          code = next;
+          woff = root & ~kExitBit;
         }
+      } while (__any_sync(0xffffffffu, active));
+    }
+    __syncwarp();
+    if (lane < rows) {
+      uint32_t code;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(code) : "r"(lbuf + 4u * lane));
+      const uint32_t cls = code & ~kLeafBit;
+      args.labels[r0 + lane] = args.leaf_class ? __ldg(args.leaf_class + cls) : cls;
+      if constexpr (EXACT) {
+        uint32_t a, b;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a) : "r"(lbuf + 128u + 4u * lane));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(b) : "r"(lbuf + 256u + 4u * lane));
+        args.iters[r0 + lane] = a;
+        args.steps[r0 + lane] = b;
       }
     }
+    pipe.release(i, t, step, n_tiles);
   }
 }
 
@@ -459,82 +591,90 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_spec(const SpecArgs args)
 // K3: random forest with per-record majority vote
 // ---------------------------------------------------------------------------
 struct ForestArgs {
-  const float* x;
-  uint64_t m;
-  uint32_t a, ld;
-  const CNode* nodes;         // all trees, compact
+  PipeArgs p;
+  const CNode* nodes;         // all trees, compact (child offsets relative to each tree)
   const uint32_t* offsets;    // t+1 node offsets
   uint32_t t_count, n_classes, abits;
   uint32_t* labels;
+  uint32_t ns, stage_bytes;
 };
 
 // PACKED: n_classes <= 8 and t_count <= 255 -> two registers of 8-bit
 // counters per record; otherwise per-warp shared counters.
 template <int A, int LOADER, bool PACKED>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_forest(const ForestArgs args) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  using Gm = TileGeom<A>;
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+    k_forest(const ForestArgs args, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int R = 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t p = Gm::pitch(args.a);
-  float* tile = reinterpret_cast<float*>(smem) + (size_t)warp * R * p;
-  uint32_t* counts = reinterpret_cast<uint32_t*>(reinterpret_cast<float*>(smem) +
-                                                 (size_t)kWarpsPerCta * R * p) +
-                     (size_t)warp * args.n_classes * 32;
+  const uint32_t sbase = align1024(smem_u32(smem));
 
-  Stager<A, 1, LOADER> st;
-  st.x = args.x;
-  st.m = args.m;
-  st.a = args.a;
-  st.ld = args.ld;
-  st.p = p;
+  Pipe<A, 1, LOADER> pipe;
+  pipe.tiles = sbase + (uint32_t)warp * args.ns * args.stage_bytes;
+  pipe.bars = sbase + kWarpsPerCta * args.ns * args.stage_bytes + (uint32_t)warp * args.ns * 8u;
+  pipe.stride_bytes = args.stage_bytes;
+  pipe.ns = args.ns;
+  pipe.tmap = &tmap;
+  pipe.p = args.p;
+  pipe.lane = lane;
+  const uint32_t counts = sbase + kWarpsPerCta * args.ns * (args.stage_bytes + 8u) +
+                          (uint32_t)warp * args.n_classes * 32u * 4u;
+
   const uint32_t amask = (1u << args.abits) - 1u;
-  const uint64_t n_tiles = (args.m + R - 1) / R;
-  const uint64_t wstride = (uint64_t)gridDim.x * kWarpsPerCta;
-  uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
-  if (LOADER != kDirect && t < n_tiles) st.prefetch(t, lane);
+  const uint64_t m = args.p.m;
+  const uint64_t n_tiles = (m + R - 1) / R;
+  const uint64_t step = (uint64_t)gridDim.x * kWarpsPerCta;
+  const uint64_t first = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  pipe.start(first, step, n_tiles);
 
-  for (; t < n_tiles; t += wstride) {
+  uint64_t i = 0;
+  for (uint64_t t = first; t < n_tiles; t += step, ++i) {
     const uint64_t r0 = t * (uint64_t)R;
-    if constexpr (LOADER != kDirect) {
-      __syncwarp();
-      st.commit(t, tile, lane);
-      __syncwarp();
-      if (t + wstride < n_tiles) st.prefetch(t + wstride, lane);
-    }
-    const bool valid = r0 + lane < args.m;
+    const uint32_t tile = pipe.acquire(i, t);
+    const bool valid = r0 + lane < m;
     const uint32_t rr = valid ? lane : 0u;
-    Feat<A, LOADER> f{LOADER == kDirect ? args.x + (r0 + rr) * (uint64_t)args.ld : tile, rr, p};
+    Rec<A, LOADER> rec;
+    rec.init(tile, rr, args.p.a, args.p.x, r0 + rr, args.p.ld);
     uint32_t h0 = 0, h1 = 0;
     if constexpr (!PACKED)
-      for (uint32_t c = 0; c < args.n_classes; ++c) counts[c * 32 + lane] = 0;
+      for (uint32_t c = 0; c < args.n_classes; ++c)
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(counts + (c * 32u + lane) * 4u), "r"(0u)
+                     : "memory");
     for (uint32_t tr = 0; tr < args.t_count; ++tr) {
-      const uint2* tn = reinterpret_cast<const uint2*>(args.nodes + __ldg(args.offsets + tr));
-      uint2 nd = __ldg(tn);
+      const char* tn = reinterpret_cast<const char*>(args.nodes + __ldg(args.offsets + tr));
+      uint2 nd = __ldg(reinterpret_cast<const uint2*>(tn));
       while (!(nd.y & kLeafBit)) {
-        const float v = f(nd.y & amask);
-        nd = __ldg(tn + (nd.y >> args.abits) + (uint32_t)(v > __uint_as_float(nd.x)));
+        const float v = rec.get(nd.y & amask);
+        nd = __ldg(reinterpret_cast<const uint2*>(
+            tn + (nd.y >> args.abits) + (v > __uint_as_float(nd.x) ? 8u : 0u)));
       }
       const uint32_t c = nd.y & ~kLeafBit;
       if constexpr (PACKED) {
         if (c < 4) h0 += 1u << (8 * c);
         else h1 += 1u << (8 * (c - 4));
       } else {
-        counts[c * 32 + lane] += 1;
+        const uint32_t a = counts + (c * 32u + lane) * 4u;
+        uint32_t cur;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cur) : "r"(a));
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(cur + 1u) : "memory");
       }
     }
     // argmax, smallest class id wins ties
     uint32_t best = 0, bestc = 0;
     for (uint32_t c = 0; c < args.n_classes; ++c) {
       uint32_t cnt;
-      if constexpr (PACKED) cnt = ((c < 4 ? h0 : h1) >> (8 * (c & 3))) & 0xFFu;
-      else cnt = counts[c * 32 + lane];
+      if constexpr (PACKED) {
+        cnt = ((c < 4 ? h0 : h1) >> (8 * (c & 3))) & 0xFFu;
+      } else {
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(cnt) : "r"(counts + (c * 32u + lane) * 4u));
+      }
       if (cnt > bestc) {
         bestc = cnt;
         best = c;
       }
     }
     if (valid) args.labels[r0 + lane] = best;
+    pipe.release(i, t, step, n_tiles);
   }
 }
 

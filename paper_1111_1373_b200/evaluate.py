@@ -53,6 +53,7 @@ class GpuGeom:
     window_levels: int = 0          # speculative window height
     reductions: int = 0             # 0 = fixed per-window doublings; k = check root every k
     blocks_per_sm: int = 0
+    stages: int = 0                 # TMA record-pipeline stages per warp
 
     def to_c(self) -> st_geom:
         g = st_geom()
@@ -67,6 +68,7 @@ class GpuGeom:
         g.window_levels = self.window_levels
         g.reductions = self.reductions
         g.blocks_per_sm = self.blocks_per_sm
+        g.stages = self.stages
         return g
 
 

@@ -1,0 +1,52 @@
+"""Geometry sweep on one workload (development aid): CUDA-event timing of
+every (algo, geometry) on device-resident records."""
+import argparse, json, os, sys, itertools
+import numpy as np, torch
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1111_1373_b200 as st
+import bench
+
+def timeit(fn, iters=30, warm=5):
+    for _ in range(warm): fn()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters): fn()
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) / iters
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="C2")
+ap.add_argument("--grid", default="data")
+ap.add_argument("--iters", type=int, default=30)
+args = ap.parse_args()
+W = bench.WORKLOADS[args.workload]
+m, a = W["m"], W["a"]
+tree = st.generate_synthetic_tree(*W["tree"])
+x = st.generate_synthetic_dataset(m, a, W["seed"])
+xd = torch.from_numpy(x).cuda(); out = torch.empty(m, dtype=torch.int32, device="cuda")
+peak, _ = bench.peaks()
+geoms = []
+if "data" in args.grid:
+    for tl, S, ns, bps in itertools.product(["shared", "global"], [0, 1, 2, 4], [2, 3, 4, 6], [0, 1, 2, 3]):
+        geoms.append(st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=S, stages=ns, blocks_per_sm=bps))
+if "spec" in args.grid:
+    for G, ns, bps in itertools.product([2, 4, 8, 16], [2, 3], [0, 2, 3, 4]):
+        geoms.append(st.GpuGeom(algo="speculative", group_lanes=G, stages=ns, blocks_per_sm=bps))
+res = []
+want = None
+for g in geoms:
+    try:
+        st.eval_device(tree, xd, out, g); torch.cuda.synchronize()
+        got = st.fnv1a64(out.cpu().numpy())
+        ok = got == W["labels_fnv"]
+        ms = timeit(lambda: st.eval_device(tree, xd, out, g), args.iters)
+    except Exception as e:
+        print("ERR", g, e, flush=True); continue
+    r = dict(g.__dict__, ok=ok, ms=round(ms, 4), frac=round(4 * a * m / (ms * 1e-3) / 1e9 / peak, 3))
+    res.append(r); print(json.dumps(r), flush=True)
+res.sort(key=lambda r: r["ms"])
+print("BEST", json.dumps(res[:5], indent=0))
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+json.dump(res, open(os.path.join(ROOT, "gpurun_out", f"sweep_{args.workload}_{args.grid}.json"), "w"), indent=0)
