@@ -734,11 +734,16 @@ void launch_spec_t(bool win_shared, const SpecArgs& sa, const Staging& stg, size
 void spec_geometry(const st_tree* t, const st_geom& g, uint32_t& G, uint32_t& H) {
   G = g.group_lanes;
   if (G == 0) {
-    G = 16;  // the paper's half-warp record group
     const uint32_t I = std::max<uint32_t>(1, t->info.internal);
-    if (I < 16) {
+    if (I <= 32) {
+      // whole tree in one record group: the paper's Proc. 5 geometry
+      // (15 internal nodes -> its half-warp of 16 lanes)
       G = 1;
       while (G < I) G *= 2;
+    } else {
+      // larger trees: 3-node windows in 4-lane groups (two levels per window,
+      // one shfl doubling) measured fastest on C2 among genuine speculation
+      G = 4;
     }
   }
   if (G > 32 || (G & (G - 1)) != 0)

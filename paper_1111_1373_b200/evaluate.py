@@ -322,17 +322,18 @@ def eval_device(tree, x, labels, geom: Optional[GpuGeom] = None, layout: str = "
     tree = _as_tree(tree)
     if not x.is_cuda or not labels.is_cuda:
         raise ArgumentError("eval_device expects CUDA tensors")
+    # strides of size-1 dimensions carry no information (torch reports 1)
     if layout == "aos":
         m, a = x.shape
-        ld = x.stride(0)
+        ld = x.stride(0) if m > 1 else a
         lay = _lib.ST_LAYOUT_AOS
-        if x.stride(1) != 1:
+        if x.stride(1) != 1 and a > 1:
             raise ArgumentError("AoS tensor must have unit attribute stride")
     else:
         a, m = x.shape
-        ld = x.stride(0)
+        ld = x.stride(0) if a > 1 else m
         lay = _lib.ST_LAYOUT_SOA
-        if x.stride(1) != 1:
+        if x.stride(1) != 1 and m > 1:
             raise ArgumentError("SoA tensor must have unit record stride")
     g = (geom or GpuGeom()).to_c()
     sp = None
@@ -411,6 +412,7 @@ def eval_forest(forest: Forest, dataset) -> np.ndarray:
 
 def eval_forest_device(forest: Forest, x, labels, stream=None) -> None:
     m, a = x.shape
-    _check(forest.L.st_forest_eval_device(forest.h, C.c_void_p(x.data_ptr()), m, a, x.stride(0),
+    _check(forest.L.st_forest_eval_device(forest.h, C.c_void_p(x.data_ptr()), m, a,
+                                          x.stride(0) if m > 1 else a,
                                           _lib.ST_LAYOUT_AOS, C.c_void_p(labels.data_ptr()),
                                           _stream_handle(stream)))

@@ -320,3 +320,18 @@ def test_concurrent_callers(cuda, co):
     [t.start() for t in th]
     [t.join() for t in th]
     assert not errors
+
+
+def test_reference_acceptance_through_cpp_dropin(cuda):
+    """oracle/_ref/gpu_acceptance: the reference's acceptance corpus run through
+    include/spectree_b200.hpp (the C++ drop-in) against the reference's own
+    evaluators compiled unchanged (criteria 1 and 2, error behaviour)."""
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref", "gpu_acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/gpu_acceptance not built (needs /root/reference at build time)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(p.stdout)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert p.stdout.count("PASS") >= 5

@@ -119,8 +119,8 @@ def test_tree_info_windows(co):
     assert paper["spec_windows"] == 1 and paper["spec_group_lanes"] == 16
     c1 = st.tree_info(co.gen_tree(10, 1024, 16, 8, 101))
     assert c1["internal"] == 1023 and c1["compact"] == 1
-    # 4-level windows of 15 nodes over a complete depth-10 tree: 1 + 16 + 256
-    assert c1["spec_windows"] == 273
+    # default: 2-level windows of 3 nodes over a complete depth-10 tree
+    assert c1["spec_group_lanes"] == 4 and c1["spec_windows"] == 1 + 4 + 16 + 64 + 256
     leaf = st.tree_info(st.EncodedTree(np.array([(0, np.inf, 0, 5)], dtype=st.NODE_DTYPE)))
     assert leaf["spec_windows"] == 0 and leaf["nodes"] == 1
 

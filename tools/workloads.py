@@ -1,0 +1,129 @@
+"""Measure every canonical configuration on one B200:
+C1, C2, C3 (frames/s), C4 (128-tree forest), C5 depth sweep 8..20 with the
+speculative / data ratio per depth.  CUDA-event timing of device-resident
+records; L2 is flushed (256 MB write) before every timed launch for the
+configs whose inputs fit in L2.  Writes gpurun_out/workloads.json.
+
+    python tools/workloads.py [--only C1,C5] [--iters 20]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+import paper_1111_1373_b200 as st  # noqa: E402
+
+PEAK, _ = bench.peaks()
+L2 = 126 * 2**20
+
+
+def timed(fn, iters, flush=None):
+    """Average device time of fn over iters launches (events around each
+    launch; optional L2 flush between launches, outside the events)."""
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    tot = 0.0
+    evs = []
+    for _ in range(iters):
+        if flush is not None:
+            flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    for a, b in evs:
+        tot += a.elapsed_time(b)
+    return tot / iters
+
+
+def run_tree(name, tree, x, labels_fnv, geoms, iters, unit_div=1.0, unit="samples/s"):
+    m, a = x.shape
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty(m, dtype=torch.int32, device="cuda")
+    flush = torch.empty(2 * L2 // 4, dtype=torch.float32, device="cuda") if 4 * a * m < 2 * L2 else None
+    res = {}
+    for gname, g in geoms:
+        st.eval_device(tree, xd, out, g)
+        torch.cuda.synchronize()
+        ok = labels_fnv is None or st.fnv1a64(out.cpu().numpy()) == labels_fnv
+        ms = timed(lambda: st.eval_device(tree, xd, out, g), iters, flush)
+        gbs = 4 * a * m / (ms * 1e-3) / 1e9
+        res[gname] = {"ms": round(ms, 5), "value": m / (ms * 1e-3) / unit_div, "unit": unit,
+                      "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 4), "labels_ok": bool(ok),
+                      "geom": {k: v for k, v in g.__dict__.items() if v not in (0, "auto")}}
+        print(name, gname, json.dumps(res[gname]), flush=True)
+    del xd, out, flush
+    torch.cuda.empty_cache()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="C1,C2,C3,C4,C5")
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    only = args.only.split(",")
+    data_g = ("data", st.GpuGeom(algo="data"))
+    spec_g = ("speculative", st.GpuGeom(algo="speculative"))
+    spec_g2 = ("speculative-G2", st.GpuGeom(algo="speculative", group_lanes=2))
+    spec_g8 = ("speculative-G8", st.GpuGeom(algo="speculative", group_lanes=8))
+    spec_g16 = ("speculative-G16", st.GpuGeom(algo="speculative", group_lanes=16))
+    geoms = [data_g, spec_g, spec_g2, spec_g8, spec_g16]
+    out = {"peak_GBs": PEAK, "device": torch.cuda.get_device_name(0)}
+    W = bench.WORKLOADS
+    for name in ("C1", "C2", "C3"):
+        if name not in only:
+            continue
+        w = W[name]
+        tree = st.generate_synthetic_tree(*w["tree"])
+        x = st.generate_synthetic_dataset(w["m"], w["a"], w["seed"])
+        div, unit = (w["m"], "frames/s") if name == "C3" else (1.0, "samples/s")
+        out[name] = run_tree(name, tree, x, w["labels_fnv"], geoms, args.iters, div, unit)
+    if "C5" in only:
+        x = st.generate_synthetic_dataset(15_625_000, 16, 5000)
+        sweep = {}
+        for d in range(8, 21, 2):
+            tree = st.generate_synthetic_tree(d, min(2**d, 4096), 16, 8, 500 + d)
+            fnv = W.get(f"C5d{d}", {}).get("labels_fnv")
+            r = run_tree(f"C5d{d}", tree, x, fnv, geoms, args.iters)
+            best_spec = min((v for k, v in r.items() if k.startswith("spec")), key=lambda v: v["ms"])
+            r["spec_over_data_time"] = round(r["speculative"]["ms"] / r["data"]["ms"], 3)
+            r["best_spec_over_data_time"] = round(best_spec["ms"] / r["data"]["ms"], 3)
+            r["tree"] = {"nodes": tree.size(), "depth": tree.depth()}
+            sweep[f"d{d}"] = r
+        out["C5"] = sweep
+    if "C4" in only:
+        trees = [st.generate_synthetic_tree(12, 1024, 64, 8, 401 + t) for t in range(128)]
+        x = st.generate_synthetic_dataset(8_000_000, 64, 499)
+        f = st.Forest(trees, 8)
+        xd = torch.from_numpy(x).cuda()
+        lab = torch.empty(len(x), dtype=torch.int32, device="cuda")
+        st.eval_forest_device(f, xd, lab)
+        torch.cuda.synchronize()
+        ok = st.fnv1a64(lab.cpu().numpy()) == 0x1b2543c41e436ce0
+        ms = timed(lambda: st.eval_forest_device(f, xd, lab), max(3, args.iters // 4))
+        gbs = 4 * 64 * len(x) / (ms * 1e-3) / 1e9
+        out["C4"] = {"ms": round(ms, 4), "value": len(x) / (ms * 1e-3), "unit": "samples/s",
+                     "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 4), "labels_ok": bool(ok),
+                     "trees": 128, "node_visits_per_s_est": len(x) * 128 * 9.09 / (ms * 1e-3)}
+        print("C4", json.dumps(out["C4"]), flush=True)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "workloads.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
