@@ -81,7 +81,8 @@ typedef struct st_geom {
                                   (reference ReductionMode::barrier_separated, k = reductions_per_iteration) */
   uint32_t blocks_per_sm;      /* 0 = occupancy-derived persistent grid */
   uint32_t stages;             /* TMA record-pipeline stages per warp (0 = auto, 2-4) */
-  uint32_t reserved[4];
+  uint32_t warps_per_cta;      /* CTA width in warps, 1-32 (0 = auto) */
+  uint32_t reserved[3];
 } st_geom;
 
 /* Optional per-record speculative counters (SpeculativeStats,

@@ -40,7 +40,8 @@ class st_geom(C.Structure):
         ("reductions", C.c_uint32),
         ("blocks_per_sm", C.c_uint32),
         ("stages", C.c_uint32),
-        ("reserved", C.c_uint32 * 4),
+        ("warps_per_cta", C.c_uint32),
+        ("reserved", C.c_uint32 * 3),
     ]
 
 

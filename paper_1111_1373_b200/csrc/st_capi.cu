@@ -418,10 +418,11 @@ std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
 // ---------------------------------------------------------------------------
 // Launch helpers
 // ---------------------------------------------------------------------------
-int blocks_for(const void* fn, size_t smem, int dev, uint32_t blocks_per_sm, uint64_t n_tiles) {
+int blocks_for(const void* fn, size_t smem, int dev, uint32_t blocks_per_sm, uint64_t n_tiles,
+               uint32_t warps = kWarpsPerCta) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, bool> attr_set;
-  static std::map<std::tuple<const void*, size_t, int>, int> occ_cache;
+  static std::map<std::tuple<const void*, size_t, int, uint32_t>, int> occ_cache;
   const DevProps pr = dev_props(dev);
   if (smem > pr.smem_optin)
     fail(ST_ERR_ARGUMENT, "kernel needs " + std::to_string(smem) + " B of shared memory (max " +
@@ -436,18 +437,18 @@ int blocks_for(const void* fn, size_t smem, int dev, uint32_t blocks_per_sm, uin
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pr.smem_optin));
       attr_set[akey] = true;
     }
-    auto key = std::make_tuple(fn, smem, dev);
+    auto key = std::make_tuple(fn, smem, dev, warps);
     auto it = occ_cache.find(key);
     if (it != occ_cache.end()) {
       occ = it->second;
     } else {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarpsPerCta * 32, smem));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)warps * 32, smem));
       if (occ < 1) fail(ST_ERR_ARGUMENT, "kernel configuration does not fit on an SM");
       occ_cache[key] = occ;
     }
   }
   uint64_t blocks = (uint64_t)pr.sms * (blocks_per_sm ? std::min<uint32_t>(blocks_per_sm, occ) : occ);
-  const uint64_t need = (n_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+  const uint64_t need = (n_tiles + warps - 1) / warps;
   return (int)std::max<uint64_t>(1, std::min(blocks, need));
 }
 
@@ -500,9 +501,10 @@ struct Staging {
   uint32_t S = 1;           // records per lane per tile (tile = 32*S records)
   uint32_t ns = 1;          // pipeline stages per warp
   uint32_t stage_bytes = 0;
+  uint32_t warps = kWarpsPerCta;  // CTA width
   CUtensorMap tmap{};
   size_t tile_smem() const {  // all warps' stages + their mbarriers
-    return loader == kDirect ? 0 : (size_t)kWarpsPerCta * ns * (stage_bytes + 8u);
+    return loader == kDirect ? 0 : (size_t)warps * ns * (stage_bytes + 8u);
   }
 };
 
@@ -558,6 +560,22 @@ Staging plan_staging(const float* x, uint64_t m, uint32_t a, uint64_t ld, int la
   return st;
 }
 
+uint32_t pick_warps(uint32_t want, const Staging& st, size_t fixed, const DevProps& pr) {
+  auto fits = [&](uint32_t w) {
+    return fixed + 1024 + (st.loader == kDirect ? 0 : (size_t)w * st.ns * (st.stage_bytes + 8u)) +
+               (size_t)w * 3 * 128 <= pr.smem_optin;
+  };
+  if (want) {
+    const uint32_t w = std::max<uint32_t>(1, std::min<uint32_t>(want, 32));
+    if (!fits(w)) fail(ST_ERR_ARGUMENT, "warps_per_cta " + std::to_string(w) + " does not fit in shared memory");
+    return w;
+  }
+  if (fixed > 16 * 1024)
+    for (uint32_t w : {32u, 16u})
+      if (fits(w)) return w;
+  return kWarpsPerCta;
+}
+
 // Persistent-grid width: on large TMA-streamed inputs 2 CTAs (16 warps) per SM
 // saturate HBM and beat the occupancy maximum (C2 sweep, profiles/); small
 // inputs use every resident CTA to hide latency.
@@ -565,7 +583,7 @@ uint32_t default_bps(uint32_t want, const Staging& st, uint64_t m, const DevProp
   if (want) return want;
   if (st.loader != kTma) return 0;
   const uint64_t tiles = m / (32ull * st.S);
-  return tiles >= (uint64_t)pr.sms * 2 * kWarpsPerCta * 16 ? 2u : 0u;
+  return tiles >= (uint64_t)pr.sms * 2 * st.warps * 16 ? 2u : 0u;
 }
 
 PipeArgs pipe_args(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout) {
@@ -584,13 +602,13 @@ void launch_data_t(const DataArgs& d, const Staging& stg, const ConstTree<CAP>* 
                    int dev, uint32_t bps, cudaStream_t s) {
   auto fn = k_data<A, S, TLOC, LOADER, CAP>;
   const uint64_t n_tiles = (d.p.m + 32 * S - 1) / (32 * S);
-  const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles);
+  const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles, stg.warps);
   static const ConstTree<1> dummy{};
   clear_stale_error();
   if constexpr (CAP == 1) {
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(d, stg.tmap, ct ? *ct : dummy);
+    fn<<<blocks, stg.warps * 32, smem, s>>>(d, stg.tmap, ct ? *ct : dummy);
   } else {
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(d, stg.tmap, *ct);
+    fn<<<blocks, stg.warps * 32, smem, s>>>(d, stg.tmap, *ct);
   }
   check_launch();
 }
@@ -672,6 +690,9 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     stg = plan_staging(x, m, a, ld, layout, S0, g.stages, 0, pr);
   }
   if (tloc == ST_TREE_CONSTANT && stg.loader != kTma) tloc = ST_TREE_GLOBAL;
+  // A large shared-memory tree is staged once per CTA: widen the CTA so that
+  // one copy serves up to 32 warps instead of capping the SM at one 8-warp CTA.
+  stg.warps = pick_warps(g.warps_per_cta, stg, tloc == ST_TREE_SHARED ? tree_bytes : 0, pr);
   d.ns = stg.ns;
   d.stage_bytes = stg.stage_bytes;
   d.tree_bytes = tloc == ST_TREE_SHARED ? tree_bytes : 0;
@@ -702,9 +723,9 @@ void launch_spec_k(const SpecArgs& sa, const Staging& stg, size_t smem, int dev,
                    cudaStream_t s) {
   auto fn = k_spec<A, LOADER, WS, EXACT, STEPS>;
   const uint64_t n_tiles = (sa.p.m + 31) / 32;
-  const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles);
+  const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles, stg.warps);
   clear_stale_error();
-  fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(sa, stg.tmap);
+  fn<<<blocks, stg.warps * 32, smem, s>>>(sa, stg.tmap);
   check_launch();
 }
 
@@ -800,10 +821,11 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   }
   sa.win_bytes = win_shared ? win_bytes : 0;
   if (stg.loader == kDirect) stg.ns = 1, stg.stage_bytes = 0;
+  stg.warps = pick_warps(g.warps_per_cta, stg, sa.win_bytes, pr);
   sa.ns = stg.ns;
   sa.stage_bytes = stg.stage_bytes;
-  const size_t smem = 1024 + sa.win_bytes + (size_t)kWarpsPerCta * stg.ns * (stg.stage_bytes + 8u) +
-                      (size_t)kWarpsPerCta * 3 * 128;  // + per-warp label/counter rows
+  const size_t smem = 1024 + sa.win_bytes + (size_t)stg.warps * stg.ns * (stg.stage_bytes + 8u) +
+                      (size_t)stg.warps * 3 * 128;  // + per-warp label/counter rows
   const uint32_t bps = g.blocks_per_sm;  // speculative is issue-bound: keep every resident CTA
   if (stg.loader == kTma && ct_arity(a)) {
     switch (a) {
@@ -852,14 +874,14 @@ void launch_forest_t(bool packed, const ForestArgs& fa, const Staging& stg, size
   const uint64_t n_tiles = (fa.p.m + 31) / 32;
   if (packed) {
     auto fn = k_forest<A, LOADER, true>;
-    const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles);
+    const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles, stg.warps);
     clear_stale_error();
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(fa, stg.tmap);
+    fn<<<blocks, stg.warps * 32, smem, s>>>(fa, stg.tmap);
   } else {
     auto fn = k_forest<A, LOADER, false>;
-    const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles);
+    const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles, stg.warps);
     clear_stale_error();
-    fn<<<blocks, kWarpsPerCta * 32, smem, s>>>(fa, stg.tmap);
+    fn<<<blocks, stg.warps * 32, smem, s>>>(fa, stg.tmap);
   }
   check_launch();
 }
@@ -882,7 +904,7 @@ void forest_device_impl(st_forest* f, const float* x, uint64_t m, uint32_t a, ui
   fa.abits = f->abits;
   fa.labels = labels;
   const bool packed = f->n_classes <= 8 && f->t_count <= 255;
-  const size_t cnt_bytes = packed ? 0 : (size_t)kWarpsPerCta * 32 * f->n_classes * 4;
+  const size_t cnt_bytes = packed ? 0 : (size_t)kWarpsPerCta * 32 * f->n_classes * 4;  // 8-warp CTAs
   Staging stg = plan_staging(x, m, a, ld, layout, 1, 0, cnt_bytes, pr);
   fa.ns = stg.ns;
   fa.stage_bytes = stg.stage_bytes;

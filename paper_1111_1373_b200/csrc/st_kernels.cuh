@@ -33,7 +33,8 @@ namespace stk {
 constexpr uint32_t kLeafBit = 0x80000000u;  // compact-node meta: leaf marker
 constexpr uint32_t kExitBit = 0x40000000u;  // speculative code: exit to window
 constexpr uint32_t kNoClass = 0xFFFFFFFFu;
-constexpr int kWarpsPerCta = 8;
+constexpr int kWarpsPerCta = 8;    // default CTA width (warps); launches may use up to 32
+constexpr int kMaxThreads = 1024;
 
 // Compact 8-byte device node.  internal: meta = (8*child) << abits | 4*attr
 // (bit 31 clear; byte offsets so the walk does no scaling); leaf: meta =
@@ -133,12 +134,15 @@ template <int A, int LOADER>
 struct Rec {
   static constexpr bool kRowLocal = A > 0 && A <= 32 && (32 % A) == 0;  // record inside one 128 B row
   uint32_t base, xm;
-  const char* gp;
+  const float* gp;   // kDirect: the record's first feature
+  uint32_t astride;  // kDirect: floats between consecutive attributes (1 AoS, ld SoA)
 
+  // `ld` is the layout's leading dimension; soa selects x[a*ld + row].
   __device__ __forceinline__ void init(uint32_t tile, uint32_t r, uint32_t a_rt, const float* x,
-                                       uint64_t row, uint32_t ld) {
+                                       uint64_t row, uint32_t ld, uint32_t soa = 0) {
     if constexpr (LOADER == kDirect) {
-      gp = reinterpret_cast<const char*>(x + row * (uint64_t)ld);
+      gp = soa ? x + row : x + row * (uint64_t)ld;
+      astride = soa ? ld : 1u;
     } else if constexpr (kRowLocal) {
       const uint32_t ra4 = r * (uint32_t)A * 4u;
       const uint32_t rowb = ra4 & ~127u;
@@ -150,7 +154,7 @@ struct Rec {
   }
   __device__ __forceinline__ float get(uint32_t attr4) const {
     if constexpr (LOADER == kDirect) {
-      return __ldg(reinterpret_cast<const float*>(gp + attr4));
+      return __ldg(gp + (uint64_t)(attr4 >> 2) * astride);
     } else if constexpr (kRowLocal) {
       return lds_f32(base + (attr4 ^ xm));
     } else {
@@ -294,12 +298,13 @@ __device__ __forceinline__ uint32_t align1024(uint32_t a) { return (a + 1023u) &
 // K1: data decomposition
 // ---------------------------------------------------------------------------
 template <int A, int S, int TLOC, int LOADER, int CAP>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__global__ void __launch_bounds__(kMaxThreads)
     k_data(const DataArgs args, const __grid_constant__ CUtensorMap tmap,
            const __grid_constant__ ConstTree<CAP> ctree) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int R = 32 * S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nw = blockDim.x >> 5;  // warps in this CTA
   const uint32_t sbase = align1024(smem_u32(smem));
 
   // ---- stage the node array once per CTA --------------------------------
@@ -319,7 +324,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   Pipe<A, S, LOADER> pipe;
   const uint32_t tiles0 = sbase + args.tree_bytes;
   pipe.tiles = tiles0 + (uint32_t)warp * args.ns * args.stage_bytes;
-  pipe.bars = tiles0 + kWarpsPerCta * args.ns * args.stage_bytes + (uint32_t)warp * args.ns * 8u;
+  pipe.bars = tiles0 + nw * args.ns * args.stage_bytes + (uint32_t)warp * args.ns * 8u;
   pipe.stride_bytes = args.stage_bytes;
   pipe.ns = args.ns;
   pipe.tmap = &tmap;
@@ -328,8 +333,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 
   const uint64_t m = args.p.m;
   const uint64_t n_tiles = (m + R - 1) / R;
-  const uint64_t step = (uint64_t)gridDim.x * kWarpsPerCta;
-  const uint64_t first = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const uint64_t step = (uint64_t)gridDim.x * nw;
+  const uint64_t first = (uint64_t)blockIdx.x * nw + warp;
   pipe.start(first, step, n_tiles);
   const uint32_t amask = (1u << args.abits) - 1u;
 
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
         const uint32_t r = q * 32 + lane;
         if (r0 + r >= m) continue;
         Rec<A, LOADER> rec;
-        rec.init(tile, r, args.p.a, args.p.x, r0 + r, args.p.ld);
+        rec.init(tile, r, args.p.a, args.p.x, r0 + r, args.p.ld, args.p.layout_soa);
         uint4 nd = __ldg(args.wide);
         while (nd.w == kNoClass) {
           const uint32_t c = nd.z + (uint32_t)(rec.get(nd.x * 4u) > __uint_as_float(nd.y));
@@ -356,7 +361,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       const uint32_t r = lane;
       const bool valid = r0 + r < m;
       Rec<A, LOADER> rec;
-      rec.init(tile, r, args.p.a, args.p.x, r0 + (valid ? r : 0), args.p.ld);
+      rec.init(tile, r, args.p.a, args.p.x, r0 + (valid ? r : 0), args.p.ld, args.p.layout_soa);
       uint2 nd = tree.get(0);
       uint32_t meta = valid ? nd.y : kLeafBit;
       float thr = __uint_as_float(nd.x);
@@ -379,7 +384,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         const uint32_t r = q * 32 + lane;
-        rec[q].init(tile, r, args.p.a, args.p.x, r0 + (r0 + r < m ? r : 0), args.p.ld);
+        rec[q].init(tile, r, args.p.a, args.p.x, r0 + (r0 + r < m ? r : 0), args.p.ld, args.p.layout_soa);
         thr[q] = __uint_as_float(root.x);
         meta[q] = (r0 + r < m) ? root.y : kLeafBit;  // idle slot in the tail tile
       }
@@ -441,11 +446,12 @@ struct SpecArgs {
 // per-record counters: while the root is unresolved apply k doublings
 // (eval_speculative.cpp:170-181).
 template <int A, int LOADER, bool WIN_SHARED, bool EXACT, int STEPS>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__global__ void __launch_bounds__(kMaxThreads)
     k_spec(const SpecArgs args, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int R = 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nw = blockDim.x >> 5;  // warps in this CTA
   const uint32_t sbase = align1024(smem_u32(smem));
 
   if constexpr (WIN_SHARED) {
@@ -462,7 +468,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   Pipe<A, 1, LOADER> pipe;
   const uint32_t tiles0 = sbase + args.win_bytes;
   pipe.tiles = tiles0 + (uint32_t)warp * args.ns * args.stage_bytes;
-  pipe.bars = tiles0 + kWarpsPerCta * args.ns * args.stage_bytes + (uint32_t)warp * args.ns * 8u;
+  pipe.bars = tiles0 + nw * args.ns * args.stage_bytes + (uint32_t)warp * args.ns * 8u;
   pipe.stride_bytes = args.stage_bytes;
   pipe.ns = args.ns;
   pipe.tmap = &tmap;
@@ -470,7 +476,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
   pipe.lane = lane;
   // per-warp label (and counter) buffer: one row of 32 records, written
   // coalesced to HBM once per tile
-  const uint32_t lbuf = tiles0 + kWarpsPerCta * args.ns * (args.stage_bytes + 8u) +
+  const uint32_t lbuf = tiles0 + nw * args.ns * (args.stage_bytes + 8u) +
                         (uint32_t)warp * 3u * 128u;
 
   const uint32_t G = args.G;
@@ -485,8 +491,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
 
   const uint64_t m = args.p.m;
   const uint64_t n_tiles = (m + R - 1) / R;
-  const uint64_t step = (uint64_t)gridDim.x * kWarpsPerCta;
-  const uint64_t first = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const uint64_t step = (uint64_t)gridDim.x * nw;
+  const uint64_t first = (uint64_t)blockIdx.x * nw + warp;
   pipe.start(first, step, n_tiles);
 
   uint64_t i = 0;
@@ -510,7 +516,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
       uint32_t woff = 0;  // byte offset of the current window
       uint32_t n_it = 0, n_st = 0;
       Rec<A, LOADER> rec;
-      rec.init(tile, active ? r : 0u, args.p.a, args.p.x, r0 + (active ? r : 0u), args.p.ld);
+      rec.init(tile, active ? r : 0u, args.p.a, args.p.x, r0 + (active ? r : 0u), args.p.ld, args.p.layout_soa);
       do {
         // -- node evaluation: every window lane computes its successor ------
         uint4 e;
@@ -563,7 +569,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
           r += NG;
           active = r < rows;
           woff = 0;
-          rec.init(tile, active ? r : 0u, args.p.a, args.p.x, r0 + (active ? r : 0u), args.p.ld);
+          rec.init(tile, active ? r : 0u, args.p.a, args.p.x, r0 + (active ? r : 0u), args.p.ld, args.p.layout_soa);
         } else {
           woff = root & ~kExitBit;
         }
@@ -602,29 +608,30 @@ struct ForestArgs {
 // PACKED: n_classes <= 8 and t_count <= 255 -> two registers of 8-bit
 // counters per record; otherwise per-warp shared counters.
 template <int A, int LOADER, bool PACKED>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+__global__ void __launch_bounds__(kMaxThreads)
     k_forest(const ForestArgs args, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int R = 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nw = blockDim.x >> 5;  // warps in this CTA
   const uint32_t sbase = align1024(smem_u32(smem));
 
   Pipe<A, 1, LOADER> pipe;
   pipe.tiles = sbase + (uint32_t)warp * args.ns * args.stage_bytes;
-  pipe.bars = sbase + kWarpsPerCta * args.ns * args.stage_bytes + (uint32_t)warp * args.ns * 8u;
+  pipe.bars = sbase + nw * args.ns * args.stage_bytes + (uint32_t)warp * args.ns * 8u;
   pipe.stride_bytes = args.stage_bytes;
   pipe.ns = args.ns;
   pipe.tmap = &tmap;
   pipe.p = args.p;
   pipe.lane = lane;
-  const uint32_t counts = sbase + kWarpsPerCta * args.ns * (args.stage_bytes + 8u) +
+  const uint32_t counts = sbase + nw * args.ns * (args.stage_bytes + 8u) +
                           (uint32_t)warp * args.n_classes * 32u * 4u;
 
   const uint32_t amask = (1u << args.abits) - 1u;
   const uint64_t m = args.p.m;
   const uint64_t n_tiles = (m + R - 1) / R;
-  const uint64_t step = (uint64_t)gridDim.x * kWarpsPerCta;
-  const uint64_t first = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const uint64_t step = (uint64_t)gridDim.x * nw;
+  const uint64_t first = (uint64_t)blockIdx.x * nw + warp;
   pipe.start(first, step, n_tiles);
 
   uint64_t i = 0;
@@ -634,7 +641,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32)
     const bool valid = r0 + lane < m;
     const uint32_t rr = valid ? lane : 0u;
     Rec<A, LOADER> rec;
-    rec.init(tile, rr, args.p.a, args.p.x, r0 + rr, args.p.ld);
+    rec.init(tile, rr, args.p.a, args.p.x, r0 + rr, args.p.ld, args.p.layout_soa);
     uint32_t h0 = 0, h1 = 0;
     if constexpr (!PACKED)
       for (uint32_t c = 0; c < args.n_classes; ++c)

@@ -54,6 +54,7 @@ class GpuGeom:
     reductions: int = 0             # 0 = fixed per-window doublings; k = check root every k
     blocks_per_sm: int = 0
     stages: int = 0                 # TMA record-pipeline stages per warp
+    warps_per_cta: int = 0          # CTA width (warps)
 
     def to_c(self) -> st_geom:
         g = st_geom()
@@ -69,6 +70,7 @@ class GpuGeom:
         g.reductions = self.reductions
         g.blocks_per_sm = self.blocks_per_sm
         g.stages = self.stages
+        g.warps_per_cta = self.warps_per_cta
         return g
 
 

@@ -29,11 +29,15 @@ xd = torch.from_numpy(x).cuda(); out = torch.empty(m, dtype=torch.int32, device=
 peak, _ = bench.peaks()
 geoms = []
 if "data" in args.grid:
-    for tl, S, ns, bps in itertools.product(["shared", "global"], [0, 1, 2, 4], [2, 3, 4, 6], [0, 1, 2, 3]):
-        geoms.append(st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=S, stages=ns, blocks_per_sm=bps))
+    for tl, S, ns, bps, w in itertools.product(["shared", "global"], [1, 2, 4], [2, 3], [0, 2], [0, 8, 16, 32]):
+        geoms.append(st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=S, stages=ns, blocks_per_sm=bps,
+                                warps_per_cta=w))
 if "spec" in args.grid:
     for G, ns, bps in itertools.product([2, 4, 8, 16], [2, 3], [0, 2, 3, 4]):
         geoms.append(st.GpuGeom(algo="speculative", group_lanes=G, stages=ns, blocks_per_sm=bps))
+if "warps" in args.grid:
+    for tl, S, w in itertools.product(["shared", "global"], [0, 1, 2], [0, 8, 16, 32]):
+        geoms.append(st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=S, warps_per_cta=w))
 res = []
 want = None
 for g in geoms:
@@ -43,7 +47,9 @@ for g in geoms:
         ok = got == W["labels_fnv"]
         ms = timeit(lambda: st.eval_device(tree, xd, out, g), args.iters)
     except Exception as e:
-        print("ERR", g, e, flush=True); continue
+        print("ERR", g, e, flush=True)
+        import paper_1111_1373_b200._lib as L
+        continue
     r = dict(g.__dict__, ok=ok, ms=round(ms, 4), frac=round(4 * a * m / (ms * 1e-3) / 1e9 / peak, 3))
     res.append(r); print(json.dumps(r), flush=True)
 res.sort(key=lambda r: r["ms"])
