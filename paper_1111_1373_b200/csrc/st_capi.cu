@@ -306,13 +306,16 @@ struct st_tree {
 };
 
 struct st_forest {
-  std::vector<CNode> compact;
-  std::vector<uint32_t> offsets;
+  std::vector<CNode> compact;      // trees concatenated, each starting 16-byte aligned
+  std::vector<uint32_t> offsets;   // first node of each tree (+ end sentinel)
+  std::vector<uint32_t> tree_bytes;  // bytes per tree rounded up to 16 (bulk-copy size)
+  uint32_t max_tree_bytes = 0;
   uint32_t t_count = 0, n_classes = 0, abits = 1, max_attribute = 0;
   std::mutex mu;
   struct Dev {
     CNode* nodes = nullptr;
     uint32_t* offsets = nullptr;
+    uint32_t* tree_bytes = nullptr;
   };
   std::map<int, Dev> dev;
   ~st_forest() {
@@ -322,6 +325,7 @@ struct st_forest {
       if (cudaSetDevice(kv.first) != cudaSuccess) continue;
       cudaFree(kv.second.nodes);
       cudaFree(kv.second.offsets);
+      cudaFree(kv.second.tree_bytes);
     }
     if (cur >= 0) cudaSetDevice(cur);
   }
@@ -334,6 +338,8 @@ struct st_forest {
     CK(cudaMemcpy(dv.nodes, compact.data(), compact.size() * sizeof(CNode), cudaMemcpyHostToDevice));
     CK(cudaMalloc(&dv.offsets, offsets.size() * 4));
     CK(cudaMemcpy(dv.offsets, offsets.data(), offsets.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&dv.tree_bytes, tree_bytes.size() * 4));
+    CK(cudaMemcpy(dv.tree_bytes, tree_bytes.data(), tree_bytes.size() * 4, cudaMemcpyHostToDevice));
     return dev.emplace(d, dv).first->second;
   }
 };
@@ -570,6 +576,14 @@ uint32_t pick_warps(uint32_t want, const Staging& st, size_t fixed, const DevPro
     if (!fits(w)) fail(ST_ERR_ARGUMENT, "warps_per_cta " + std::to_string(w) + " does not fit in shared memory");
     return w;
   }
+  if (st.loader == kTma) {
+    // ~128 KB of record stages in flight per SM saturated HBM in every sweep
+    // (C2: 16 warps x 2 x 4 KB; C5: 32 warps x 2 x 2 KB); use one wide CTA so
+    // a shared-memory tree is staged once per SM.
+    uint32_t w = (uint32_t)std::min<size_t>(32, std::max<size_t>(8, (128u << 10) / ((size_t)st.ns * st.stage_bytes)));
+    while (w > 8 && !fits(w)) w -= 8;
+    if (fits(w)) return w;
+  }
   if (fixed > 16 * 1024)
     for (uint32_t w : {32u, 16u})
       if (fits(w)) return w;
@@ -582,8 +596,10 @@ uint32_t pick_warps(uint32_t want, const Staging& st, size_t fixed, const DevPro
 uint32_t default_bps(uint32_t want, const Staging& st, uint64_t m, const DevProps& pr) {
   if (want) return want;
   if (st.loader != kTma) return 0;
+  // one wide CTA per SM carries the ~128 KB of stages (pick_warps); more CTAs
+  // only pay on inputs too small to fill the SMs
   const uint64_t tiles = m / (32ull * st.S);
-  return tiles >= (uint64_t)pr.sms * 2 * st.warps * 16 ? 2u : 0u;
+  return tiles >= (uint64_t)pr.sms * st.warps * 16 ? std::max<uint32_t>(1, 16 / st.warps) : 0u;
 }
 
 PipeArgs pipe_args(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout) {
@@ -646,7 +662,9 @@ bool ct_arity(uint32_t a) { return a == 8 || a == 16 || a == 32 || a == 64; }
 uint32_t choose_S(uint32_t a, uint32_t want) {
   // instantiated: a=8 {1,2,4}, a=16 {1,2}, a=32 {1,2}, others {1}
   const uint32_t maxS = a == 8 ? 4 : (a == 16 || a == 32) ? 2 : 1;
-  if (want == 0) want = a <= 8 ? 4 : a <= 16 ? 2 : 1;
+  // one record per lane; more warps beat more walks per lane (sweeps in
+  // profiles/), except 8-attribute records whose 1 KB tiles are too small
+  if (want == 0) want = a <= 8 ? 2 : 1;
   uint32_t S = 1;
   while (S * 2 <= std::min(want, maxS)) S *= 2;
   return S;
@@ -886,6 +904,72 @@ void launch_forest_t(bool packed, const ForestArgs& fa, const Staging& stg, size
   check_launch();
 }
 
+template <int A, int S>
+void launch_forest_smem(const Forest2Args& fa, const Staging& stg, size_t smem, int dev,
+                        cudaStream_t s) {
+  auto fn = k_forest_smem<A, S>;
+  const uint64_t n_tiles = (fa.p.m + 32 * S - 1) / (32 * S);
+  const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles, stg.warps);
+  clear_stale_error();
+  fn<<<blocks, stg.warps * 32, smem, s>>>(fa, stg.tmap);
+  check_launch();
+}
+
+// Trees streamed through shared memory (packed votes, TMA-staged records).
+bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                      int layout, uint32_t* labels, cudaStream_t s, int dev, const DevProps& pr) {
+  if (!(f->n_classes <= 8 && f->t_count <= 255) || f->max_tree_bytes > 48 * 1024) return false;
+  uint32_t S = 1;
+  while (S < 4 && 2 * S * a <= 128) S *= 2;  // tile of 32*S records, <= 16 KB for a = 64
+  if (!ct_arity(a)) S = 1;
+  if (!tma_ok(x, m, a, ld, layout, S)) return false;
+  Staging stg;
+  stg.loader = kTma;
+  stg.S = S;
+  stg.ns = 1;
+  stg.stage_bytes = round1024(32ull * S * a * 4);
+  const size_t fixed = 1024 + 2ull * f->max_tree_bytes + 16;
+  stg.warps = 0;
+  for (uint32_t w : {16u, 8u, 4u, 2u, 1u})
+    if (fixed + (size_t)w * (stg.stage_bytes + 8u) <= pr.smem_optin) {
+      stg.warps = w;
+      break;
+    }
+  if (!stg.warps) return false;
+  make_tmap(stg, x, m, a);
+  st_forest::Dev& dv = f->device(dev);
+  Forest2Args fa{};
+  fa.p = pipe_args(x, m, a, ld, layout);
+  fa.nodes = dv.nodes;
+  fa.offsets = dv.offsets;
+  fa.t_count = f->t_count;
+  fa.n_classes = f->n_classes;
+  fa.abits = f->abits;
+  fa.labels = labels;
+  fa.stage_bytes = stg.stage_bytes;
+  fa.tree_buf_bytes = f->max_tree_bytes;
+  fa.tree_bytes = dv.tree_bytes;
+  const size_t smem = fixed + (size_t)stg.warps * (stg.stage_bytes + 8u);
+  switch (a) {
+    case 8:
+      if (S == 4) return launch_forest_smem<8, 4>(fa, stg, smem, dev, s), true;
+      if (S == 2) return launch_forest_smem<8, 2>(fa, stg, smem, dev, s), true;
+      return launch_forest_smem<8, 1>(fa, stg, smem, dev, s), true;
+    case 16:
+      if (S == 4) return launch_forest_smem<16, 4>(fa, stg, smem, dev, s), true;
+      if (S == 2) return launch_forest_smem<16, 2>(fa, stg, smem, dev, s), true;
+      return launch_forest_smem<16, 1>(fa, stg, smem, dev, s), true;
+    case 32:
+      if (S == 2) return launch_forest_smem<32, 2>(fa, stg, smem, dev, s), true;
+      return launch_forest_smem<32, 1>(fa, stg, smem, dev, s), true;
+    case 64:
+      if (S == 2) return launch_forest_smem<64, 2>(fa, stg, smem, dev, s), true;
+      return launch_forest_smem<64, 1>(fa, stg, smem, dev, s), true;
+    default:
+      return launch_forest_smem<0, 1>(fa, stg, smem, dev, s), true;
+  }
+}
+
 void forest_device_impl(st_forest* f, const float* x, uint64_t m, uint32_t a, uint64_t ld,
                         int layout, uint32_t* labels, cudaStream_t s) {
   if (!f) fail(ST_ERR_ARGUMENT, "null forest");
@@ -894,6 +978,7 @@ void forest_device_impl(st_forest* f, const float* x, uint64_t m, uint32_t a, ui
   if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
   const int dev = current_device();
   const DevProps pr = dev_props(dev);
+  if (forest_smem_path(f, x, m, a, ld, layout, labels, s, dev, pr)) return;
   st_forest::Dev& dv = f->device(dev);
   ForestArgs fa{};
   fa.p = pipe_args(x, m, a, ld, layout);
@@ -1080,9 +1165,13 @@ int st_forest_create(const st_node* const* trees, const uint32_t* sizes, uint32_
     for (uint32_t k = 0; k < t; ++k) maxn = std::max(maxn, sizes[k]);
     if (!compact_fits(maxn, maxattr, &f->abits) || total >= (1ull << 32))
       fail(ST_ERR_ARGUMENT, "forest too large for the compact device format");
-    f->compact.reserve(total);
-    f->offsets.push_back(0);
+    f->compact.reserve(total + t);
     for (uint32_t k = 0; k < t; ++k) {
+      if (f->compact.size() & 1u) f->compact.push_back(CNode{0.0f, kLeafBit});  // 16-byte align
+      f->offsets.push_back((uint32_t)f->compact.size());
+      const uint32_t tb = (uint32_t)((sizes[k] * sizeof(CNode) + 15) & ~size_t(15));
+      f->tree_bytes.push_back(tb);
+      f->max_tree_bytes = std::max(f->max_tree_bytes, tb);
       for (uint32_t i = 0; i < sizes[k]; ++i) {
         const st_node& nd = trees[k][i];
         if (nd.class_id != ST_NO_CLASS)
@@ -1090,8 +1179,10 @@ int st_forest_create(const st_node* const* trees, const uint32_t* sizes, uint32_
         else
           f->compact.push_back(CNode{nd.threshold, ((8u * nd.child) << f->abits) | (4u * nd.attribute)});
       }
-      f->offsets.push_back((uint32_t)f->compact.size());
     }
+    if (f->compact.size() & 1u) f->compact.push_back(CNode{0.0f, kLeafBit});
+    f->compact.push_back(CNode{0.0f, kLeafBit});  // tail padding for the last 16-byte copy
+    f->offsets.push_back((uint32_t)f->compact.size());
     *out = f.release();
   });
 }

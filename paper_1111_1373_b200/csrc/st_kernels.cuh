@@ -120,6 +120,14 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
+// 1-D bulk copy global -> shared completing on an mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 // Byte offset of flat float f of a tile under SWIZZLE_128B (tile base
 // 1024-aligned): 16-byte chunk bits [4:6] XOR row bits [7:9].
 __device__ __forceinline__ uint32_t swz(uint32_t byte_off) {
@@ -682,6 +690,129 @@ __global__ void __launch_bounds__(kMaxThreads)
     }
     if (valid) args.labels[r0 + lane] = best;
     pipe.release(i, t, step, n_tiles);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3b: forest vote with trees streamed through shared memory
+// ---------------------------------------------------------------------------
+// Every warp keeps one TMA-staged tile of 32*S records resident for the whole
+// tree loop; the CTA streams the T trees through a double buffer in shared
+// memory (one elected thread issues cp.async.bulk for tree i+1 while all warps
+// walk tree i; a CTA barrier per tree releases the buffer).  Votes live in
+// packed 8-bit registers (<= 8 classes, <= 255 trees).
+struct Forest2Args {
+  PipeArgs p;
+  const CNode* nodes;          // all trees, compact (child offsets relative to each tree)
+  const uint32_t* offsets;     // t+1 node offsets (device)
+  uint32_t t_count, n_classes, abits;
+  uint32_t* labels;
+  uint32_t stage_bytes;        // record tile (one stage per warp)
+  uint32_t tree_buf_bytes;     // per tree buffer (>= largest tree, 16-aligned)
+  const uint32_t* tree_bytes;  // per tree: bytes to copy (16-aligned, device)
+};
+
+template <int A, int S>
+__global__ void __launch_bounds__(kMaxThreads)
+    k_forest_smem(const Forest2Args args, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  constexpr int R = 32 * S;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nw = blockDim.x >> 5;
+  const uint32_t sbase = align1024(smem_u32(smem));
+  // [tree buf 0 | tree buf 1] [warp stages] [warp tile bars] [2 tree bars]
+  const uint32_t tbuf0 = sbase;
+  const uint32_t tiles0 = sbase + 2u * args.tree_buf_bytes;
+  Pipe<A, S, kTma> pipe;
+  pipe.tiles = tiles0 + (uint32_t)warp * args.stage_bytes;
+  pipe.bars = tiles0 + nw * args.stage_bytes + (uint32_t)warp * 8u;
+  pipe.stride_bytes = args.stage_bytes;
+  pipe.ns = 1;
+  pipe.tmap = &tmap;
+  pipe.p = args.p;
+  pipe.lane = lane;
+  const uint32_t tbar0 = tiles0 + nw * (args.stage_bytes + 8u);
+  const uint32_t T = args.t_count;
+
+  auto issue_tree = [&](uint64_t gi) {  // thread 0: tree (gi % T) into buffer gi & 1
+    const uint32_t tr = (uint32_t)(gi % T);
+    const uint32_t b = (uint32_t)(gi & 1u);
+    const uint32_t bytes = __ldg(args.tree_bytes + tr);
+    mbar_arrive_expect_tx(tbar0 + 8u * b, bytes);
+    bulk_load(tbuf0 + b * args.tree_buf_bytes, args.nodes + __ldg(args.offsets + tr), bytes,
+              tbar0 + 8u * b);
+  };
+
+  const uint64_t m = args.p.m;
+  const uint64_t n_tiles = (m + R - 1) / R;
+  const uint64_t step = (uint64_t)gridDim.x * nw;
+  // round k: warp w of this CTA takes tile (blockIdx.x + k*gridDim.x)*nw + w
+  const uint64_t rounds = (n_tiles + step - 1) / step;
+  const uint64_t my_rounds =
+      blockIdx.x * (uint64_t)nw < n_tiles ? (n_tiles - blockIdx.x * (uint64_t)nw + step - 1) / step : 0;
+  (void)rounds;
+  if (threadIdx.x == 0) {
+    mbar_init(tbar0, 1);
+    mbar_init(tbar0 + 8u, 1);
+    fence_barrier_init();
+  }
+  const uint64_t first = (uint64_t)blockIdx.x * nw + warp;
+  pipe.start(first, step, n_tiles);  // per-warp tile barrier + first tile
+  __syncthreads();
+  if (threadIdx.x == 0 && my_rounds > 0) issue_tree(0);
+  const uint32_t amask = (1u << args.abits) - 1u;
+
+  uint64_t gi = 0;  // global tree sequence number for this CTA
+  for (uint64_t k = 0; k < my_rounds; ++k) {
+    const uint64_t t = first + k * step;
+    const bool have = t < n_tiles;
+    uint32_t tile = 0;
+    if (have) tile = pipe.acquire(k, t);
+    const uint64_t r0 = t * (uint64_t)R;
+    Rec<A, kTma> rec[S];
+    uint32_t h0[S], h1[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) {
+      const uint32_t r = q * 32 + lane;
+      rec[q].init(tile, r, args.p.a, args.p.x, r0 + r, args.p.ld, 0);
+      h0[q] = h1[q] = 0;
+    }
+    for (uint32_t tr = 0; tr < T; ++tr, ++gi) {
+      if (threadIdx.x == 0 && (k + 1 < my_rounds || tr + 1 < T)) issue_tree(gi + 1);
+      const uint32_t b = (uint32_t)(gi & 1u);
+      mbar_wait(tbar0 + 8u * b, (uint32_t)((gi >> 1) & 1u));
+      if (have) {
+        const uint32_t tb = tbuf0 + b * args.tree_buf_bytes;
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          uint2 nd = lds_u2(tb);
+          while (!(nd.y & kLeafBit)) {
+            const float v = rec[q].get(nd.y & amask);
+            nd = lds_u2(tb + (nd.y >> args.abits) + (v > __uint_as_float(nd.x) ? 8u : 0u));
+          }
+          const uint32_t c = nd.y & ~kLeafBit;
+          if (c < 4) h0[q] += 1u << (8 * c);
+          else h1[q] += 1u << (8 * (c - 4));
+        }
+      }
+      __syncthreads();  // every warp is done with buffer b: it may be refilled
+    }
+    if (have) {
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint64_t r = r0 + q * 32 + lane;
+        uint32_t best = 0, bestc = 0;
+        for (uint32_t c = 0; c < args.n_classes; ++c) {
+          const uint32_t cnt = ((c < 4 ? h0[q] : h1[q]) >> (8 * (c & 3))) & 0xFFu;
+          if (cnt > bestc) {
+            bestc = cnt;
+            best = c;
+          }
+        }
+        if (r < m) args.labels[r] = best;
+      }
+      pipe.release(k, t, step, n_tiles);
+    }
   }
 }
 

@@ -49,3 +49,17 @@ def cuda():
         pytest.fail("GPU test selected but no CUDA device is visible")
     torch.cuda.set_device(0)
     return torch.device("cuda", 0)
+
+
+def pytest_runtest_teardown(item):
+    """ST_MEM_REPORT=1: print free device memory after every test (leak hunt)."""
+    if os.environ.get("ST_MEM_REPORT"):
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                free, total = torch.cuda.mem_get_info()
+                print(f"\n[mem] {item.nodeid}: free {free / 2**30:.1f} GiB / {total / 2**30:.1f}, "
+                      f"torch reserved {torch.cuda.memory_reserved() / 2**30:.1f} GiB", flush=True)
+        except Exception:
+            pass
