@@ -928,13 +928,25 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   stg.S = S;
   stg.ns = 1;
   stg.stage_bytes = round1024(32ull * S * a * 4);
-  const size_t fixed = 1024 + 2ull * f->max_tree_bytes + 16;
+  // Tree ring: deep enough that the next trees' loads overlap walking the
+  // current one (a 16 KB tree takes longer to arrive from L2 than 512 records
+  // take to walk it); the rest of shared memory holds resident record tiles.
   stg.warps = 0;
-  for (uint32_t w : {16u, 8u, 4u, 2u, 1u})
-    if (fixed + (size_t)w * (stg.stage_bytes + 8u) <= pr.smem_optin) {
-      stg.warps = w;
-      break;
+  uint32_t nt = 0;
+  size_t fixed = 0;
+  for (uint32_t w : {8u, 4u, 2u, 1u}) {
+    for (uint32_t n : {4u, 3u, 2u}) {
+      const size_t region = round1024((uint64_t)n * f->max_tree_bytes);
+      const size_t need = 1024 + region + (size_t)w * (stg.stage_bytes + 8u) + 8u * n;
+      if (need <= pr.smem_optin) {
+        stg.warps = w;
+        nt = n;
+        fixed = 1024 + region + 8u * n;
+        break;
+      }
     }
+    if (stg.warps) break;
+  }
   if (!stg.warps) return false;
   make_tmap(stg, x, m, a);
   st_forest::Dev& dv = f->device(dev);
@@ -948,6 +960,8 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   fa.labels = labels;
   fa.stage_bytes = stg.stage_bytes;
   fa.tree_buf_bytes = f->max_tree_bytes;
+  fa.n_tree_bufs = nt;
+  fa.tree_region = round1024((uint64_t)nt * f->max_tree_bytes);
   fa.tree_bytes = dv.tree_bytes;
   const size_t smem = fixed + (size_t)stg.warps * (stg.stage_bytes + 8u);
   switch (a) {

@@ -709,6 +709,8 @@ struct Forest2Args {
   uint32_t* labels;
   uint32_t stage_bytes;        // record tile (one stage per warp)
   uint32_t tree_buf_bytes;     // per tree buffer (>= largest tree, 16-aligned)
+  uint32_t n_tree_bufs;        // tree ring depth (>= 2)
+  uint32_t tree_region;        // bytes reserved for the ring (1024-aligned)
   const uint32_t* tree_bytes;  // per tree: bytes to copy (16-aligned, device)
 };
 
@@ -720,9 +722,9 @@ __global__ void __launch_bounds__(kMaxThreads)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t nw = blockDim.x >> 5;
   const uint32_t sbase = align1024(smem_u32(smem));
-  // [tree buf 0 | tree buf 1] [warp stages] [warp tile bars] [2 tree bars]
+  // [tree ring (1024-aligned)] [warp stages] [warp tile bars] [tree bars]
   const uint32_t tbuf0 = sbase;
-  const uint32_t tiles0 = sbase + 2u * args.tree_buf_bytes;
+  const uint32_t tiles0 = sbase + args.tree_region;
   Pipe<A, S, kTma> pipe;
   pipe.tiles = tiles0 + (uint32_t)warp * args.stage_bytes;
   pipe.bars = tiles0 + nw * args.stage_bytes + (uint32_t)warp * 8u;
@@ -733,36 +735,37 @@ __global__ void __launch_bounds__(kMaxThreads)
   pipe.lane = lane;
   const uint32_t tbar0 = tiles0 + nw * (args.stage_bytes + 8u);
   const uint32_t T = args.t_count;
+  const uint32_t NT = args.n_tree_bufs;
 
-  auto issue_tree = [&](uint64_t gi) {  // thread 0: tree (gi % T) into buffer gi & 1
+  const uint64_t m = args.p.m;
+  const uint64_t n_tiles = (m + R - 1) / R;
+  const uint64_t step = (uint64_t)gridDim.x * nw;
+  const uint64_t my_rounds =
+      blockIdx.x * (uint64_t)nw < n_tiles ? (n_tiles - blockIdx.x * (uint64_t)nw + step - 1) / step : 0;
+  const uint64_t total = my_rounds * T;  // trees this CTA streams
+
+  auto issue_tree = [&](uint64_t gi) {  // thread 0: tree (gi % T) into ring slot gi % NT
+    if (gi >= total) return;
     const uint32_t tr = (uint32_t)(gi % T);
-    const uint32_t b = (uint32_t)(gi & 1u);
+    const uint32_t b = (uint32_t)(gi % NT);
     const uint32_t bytes = __ldg(args.tree_bytes + tr);
     mbar_arrive_expect_tx(tbar0 + 8u * b, bytes);
     bulk_load(tbuf0 + b * args.tree_buf_bytes, args.nodes + __ldg(args.offsets + tr), bytes,
               tbar0 + 8u * b);
   };
 
-  const uint64_t m = args.p.m;
-  const uint64_t n_tiles = (m + R - 1) / R;
-  const uint64_t step = (uint64_t)gridDim.x * nw;
-  // round k: warp w of this CTA takes tile (blockIdx.x + k*gridDim.x)*nw + w
-  const uint64_t rounds = (n_tiles + step - 1) / step;
-  const uint64_t my_rounds =
-      blockIdx.x * (uint64_t)nw < n_tiles ? (n_tiles - blockIdx.x * (uint64_t)nw + step - 1) / step : 0;
-  (void)rounds;
   if (threadIdx.x == 0) {
-    mbar_init(tbar0, 1);
-    mbar_init(tbar0 + 8u, 1);
+    for (uint32_t b = 0; b < NT; ++b) mbar_init(tbar0 + 8u * b, 1);
     fence_barrier_init();
   }
   const uint64_t first = (uint64_t)blockIdx.x * nw + warp;
   pipe.start(first, step, n_tiles);  // per-warp tile barrier + first tile
   __syncthreads();
-  if (threadIdx.x == 0 && my_rounds > 0) issue_tree(0);
+  if (threadIdx.x == 0)
+    for (uint32_t b = 0; b + 1 < NT; ++b) issue_tree(b);  // NT-1 trees in flight
   const uint32_t amask = (1u << args.abits) - 1u;
 
-  uint64_t gi = 0;  // global tree sequence number for this CTA
+  uint64_t gi = 0;  // tree sequence number within this CTA
   for (uint64_t k = 0; k < my_rounds; ++k) {
     const uint64_t t = first + k * step;
     const bool have = t < n_tiles;
@@ -778,9 +781,11 @@ __global__ void __launch_bounds__(kMaxThreads)
       h0[q] = h1[q] = 0;
     }
     for (uint32_t tr = 0; tr < T; ++tr, ++gi) {
-      if (threadIdx.x == 0 && (k + 1 < my_rounds || tr + 1 < T)) issue_tree(gi + 1);
-      const uint32_t b = (uint32_t)(gi & 1u);
-      mbar_wait(tbar0 + 8u * b, (uint32_t)((gi >> 1) & 1u));
+      // slot (gi + NT - 1) % NT last held tree gi - 1, released by the
+      // barrier that ended the previous iteration
+      if (threadIdx.x == 0) issue_tree(gi + NT - 1);
+      const uint32_t b = (uint32_t)(gi % NT);
+      mbar_wait(tbar0 + 8u * b, (uint32_t)((gi / NT) & 1u));
       if (have) {
         const uint32_t tb = tbuf0 + b * args.tree_buf_bytes;
 #pragma unroll
@@ -795,7 +800,7 @@ __global__ void __launch_bounds__(kMaxThreads)
           else h1[q] += 1u << (8 * (c - 4));
         }
       }
-      __syncthreads();  // every warp is done with buffer b: it may be refilled
+      __syncthreads();  // every warp is done with slot b: it may be refilled
     }
     if (have) {
 #pragma unroll
