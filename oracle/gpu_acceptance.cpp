@@ -10,7 +10,8 @@
 //     speculative-basic vs eval_oracle_recursive -- zero mismatches;
 //   criterion 2 (acceptance.cpp:173-211): per-record doubling counters of the
 //     GPU speculative kernel vs the law ceil(log2 depth) (and the paired
-//     k = 2 law), on trees whose internal nodes fit one record group;
+//     k = 2 law), on the reference's own workload (39 internal nodes: the
+//     CTA-scope exact kernel) and 40 trees that fit one warp group (shfl);
 //   error behaviour: ArgumentError before any work, with the reference text.
 //
 // Built by oracle/Makefile into oracle/_ref/gpu_acceptance (needs the GPU
@@ -127,9 +128,13 @@ void criterion1() {
 
 void criterion2() {
   std::uint64_t trees = 0, recs = 0;
-  for (std::uint64_t seed = 1; seed <= 40; ++seed) {
-    const EncodedTree tree = generate_synthetic_tree(12, 20 + seed % 13, 8, 5, 97 + seed);
-    const Dataset data = generate_synthetic_dataset(10000, 8, 13 + seed, Distribution::uniform);
+  // seed 0 is the reference's own criterion-2 workload (acceptance.cpp:174-176,
+  // 39 internal nodes); seeds 1..40 add trees that fit one warp group
+  for (std::uint64_t seed = 0; seed <= 40; ++seed) {
+    const EncodedTree tree = seed == 0 ? generate_synthetic_tree(20, 40, 8, 5, 97)
+                                       : generate_synthetic_tree(12, 20 + seed % 13, 8, 5, 97 + seed);
+    const Dataset data = seed == 0 ? generate_synthetic_dataset(10000, 8, 13, Distribution::uniform)
+                                   : generate_synthetic_dataset(10000, 8, 13 + seed, Distribution::uniform);
     const auto depths = traversal_depths(tree, data);
     SpeculativeConfig config;
     config.group_lanes = (tree.size() - 1) / 2;

@@ -145,6 +145,7 @@ struct st_tree {
     CNode* compact = nullptr;
     uint4* wide = nullptr;
     uint32_t* leaf_tbl = nullptr;
+    uint32_t* internal_map = nullptr;  // processor_node_map (tree.cpp:204-209)
     std::map<std::pair<uint32_t, uint32_t>, SEntry*> wins;
   };
   std::map<int, Dev> dev;
@@ -157,6 +158,7 @@ struct st_tree {
       cudaFree(kv.second.compact);
       cudaFree(kv.second.wide);
       cudaFree(kv.second.leaf_tbl);
+      cudaFree(kv.second.internal_map);
       for (auto& w : kv.second.wins) cudaFree(w.second);
     }
     if (cur >= 0) cudaSetDevice(cur);
@@ -282,6 +284,14 @@ struct st_tree {
       CK(cudaMemset(dv.compact, 0, bytes));
       CK(cudaMemcpy(dv.compact, compact.data(), compact.size() * sizeof(CNode),
                     cudaMemcpyHostToDevice));
+    }
+    {
+      std::vector<uint32_t> map;
+      for (uint32_t i = 0; i < nodes.size(); ++i)
+        if (!is_leaf(i)) map.push_back(i);
+      map.push_back(0);  // keep the allocation non-empty
+      CK(cudaMalloc(&dv.internal_map, map.size() * 4));
+      CK(cudaMemcpy(dv.internal_map, map.data(), map.size() * 4, cudaMemcpyHostToDevice));
     }
     if (leaf_table) {
       CK(cudaMalloc(&dv.leaf_tbl, leaf_classes.size() * 4));
@@ -801,10 +811,61 @@ void spec_geometry(const st_tree* t, const st_geom& g, uint32_t& G, uint32_t& H)
   }
 }
 
+// Reference counters for trees with more than 32 internal nodes: CTA-scope
+// whole-tree speculation (k_spec_exact_cta).
+void eval_spec_exact_cta(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                         int layout, uint32_t k, uint32_t* labels, st_stats* stats, cudaStream_t s,
+                         int dev) {
+  st_tree::Dev& dv = t->device(dev);
+  const DevProps pr = dev_props(dev);
+  SpecExactArgs ea{};
+  ea.p = pipe_args(x, m, a, ld, layout);
+  ea.nodes = dv.wide;
+  ea.map = dv.internal_map;
+  ea.n = (uint32_t)t->nodes.size();
+  ea.I = t->info.internal;
+  ea.k = k ? k : 1;
+  ea.labels = labels;
+  ea.iters = stats->iterations;
+  ea.steps = stats->doubling_steps;
+  const size_t smem = 8ull * t->nodes.size();
+  if (smem > pr.smem_optin) fail(ST_ERR_ARGUMENT, "tree too large for exact speculative counters");
+  const uint32_t threads = std::min<uint32_t>(1024, std::max<uint32_t>(32, (ea.I + 31) / 32 * 32));
+  auto fn = k_spec_exact_cta;
+  static std::mutex mu;
+  static std::map<int, bool> attr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!attr.count(dev)) {
+      CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)pr.smem_optin));
+      attr[dev] = true;
+    }
+  }
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)threads, smem));
+  const uint64_t blocks = std::min<uint64_t>(m, (uint64_t)pr.sms * std::max(occ, 1));
+  clear_stale_error();
+  fn<<<(unsigned)blocks, threads, smem, s>>>(ea);
+  check_launch();
+}
+
 void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
                       const st_geom& g, uint32_t* labels, st_stats* stats, cudaStream_t s, int dev) {
+  if (stats && t->info.internal > 32) {
+    // counters are defined by whole-tree speculation (the reference law)
+    return eval_spec_exact_cta(t, x, m, a, ld, layout, g.reductions, labels, stats, s, dev);
+  }
+  st_geom gg = g;
+  if (stats) {
+    // whole tree in one record group so the counters follow the reference law
+    uint32_t G = 1;
+    while (G < std::max<uint32_t>(1, t->info.internal)) G *= 2;
+    gg.group_lanes = G;
+    gg.window_levels = std::max<uint32_t>(1, t->info.depth);
+  }
   uint32_t G, H;
-  spec_geometry(t, g, G, H);
+  spec_geometry(t, gg, G, H);
   if (4ull * t->info.max_attribute >= (1u << 24))
     fail(ST_ERR_ARGUMENT, "speculative kernel requires attribute indices < 2^22");
   auto wt = t->windows(G, H);

@@ -821,4 +821,78 @@ __global__ void __launch_bounds__(kMaxThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// K2x: exact whole-tree speculation at CTA scope (reference counters for any I)
+// ---------------------------------------------------------------------------
+// The paper's Proc. 5 as written and the reference's
+// mapped barrier-separated GroupWorker (eval_speculative.cpp:127-204): the CTA
+// is one record group; thread j owns internal nodes map[j], map[j+T], ...;
+// the path array is double-buffered in shared memory and every doubling is a
+// barrier-separated snapshot step; while the root entry is internal, k
+// doublings per iteration.  Leaves stay identity fixpoints in both buffers.
+// Used when per-record counters are requested for trees whose internal nodes
+// exceed one warp (the shfl kernel covers <= 32).
+struct SpecExactArgs {
+  PipeArgs p;
+  const uint4* nodes;      // original 16-byte nodes
+  const uint32_t* map;     // internal node indices ascending (processor_node_map)
+  uint32_t n, I, k;
+  uint32_t* labels;
+  uint32_t* iters;
+  uint32_t* steps;
+};
+
+__global__ void __launch_bounds__(kMaxThreads) k_spec_exact_cta(const SpecExactArgs args) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint32_t* buf_a = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* buf_b = buf_a + args.n;
+  __shared__ uint32_t root_val;
+  for (uint32_t i = threadIdx.x; i < args.n; i += blockDim.x) buf_a[i] = buf_b[i] = i;
+  __syncthreads();
+  for (uint64_t r = blockIdx.x; r < args.p.m; r += gridDim.x) {
+    const float* rec = args.p.layout_soa ? args.p.x + r : args.p.x + r * (uint64_t)args.p.ld;
+    const uint64_t astride = args.p.layout_soa ? args.p.ld : 1;
+    uint32_t* cur = buf_a;
+    uint32_t* alt = buf_b;
+    // node evaluation over the mapped (internal) lanes
+    for (uint32_t j = threadIdx.x; j < args.I; j += blockDim.x) {
+      const uint32_t i = __ldg(args.map + j);
+      const uint4 nd = __ldg(args.nodes + i);
+      cur[i] = nd.z + (uint32_t)(__ldg(rec + (uint64_t)nd.x * astride) > __uint_as_float(nd.y));
+    }
+    __syncthreads();
+    uint32_t it = 0, st = 0;
+    while (true) {
+      if (threadIdx.x == 0) root_val = __ldg(args.nodes + cur[0]).w;
+      __syncthreads();
+      const bool resolved = root_val != kNoClass;
+      __syncthreads();
+      if (resolved) break;
+      for (uint32_t s = 0; s < args.k; ++s) {
+        for (uint32_t j = threadIdx.x; j < args.I; j += blockDim.x) {
+          const uint32_t i = __ldg(args.map + j);
+          alt[i] = cur[cur[i]];
+        }
+        __syncthreads();
+        uint32_t* t = cur;
+        cur = alt;
+        alt = t;
+        ++st;
+      }
+      ++it;
+    }
+    if (threadIdx.x == 0) {
+      args.labels[r] = __ldg(args.nodes + cur[0]).w;
+      if (args.iters) {
+        args.iters[r] = it;
+        args.steps[r] = st;
+      }
+    }
+    // an odd number of swaps left the live array in buf_b: no reset is
+    // needed (every mapped entry is rewritten before it is read), but both
+    // buffers must stop being read before the next record writes them
+    __syncthreads();
+  }
+}
+
 }  // namespace stk

@@ -129,6 +129,24 @@ def test_step_law_depth_chain(cuda):
         assert stats.doubling_steps.tolist() == [st0, 0]
 
 
+def test_reference_criterion2_counters(cuda):
+    """acceptance.cpp:173-211 workload (39 internal nodes, more than a warp):
+    the CTA-scope exact kernel reproduces the reference's per-record
+    iterations / doubling steps for k = 1 and k = 2 (ref_steplaw.npz)."""
+    g = np.load(os.path.join(GOLD, "ref_steplaw.npz"))
+    tree = st.EncodedTree(g["nodes"].view(st.NODE_DTYPE))
+    assert len(tree.internal_indices()) == 39
+    x = st.generate_synthetic_dataset(10000, 8, 13)
+    for k in (1, 2):
+        cfg = st.SpeculativeConfig(group_lanes=39, groups=625, records_per_group=16,
+                                   reductions_per_iteration=k)
+        stats = st.SpeculativeStats()
+        lab = st.eval_speculative(tree, x, cfg, stats)
+        assert np.array_equal(lab, g["labels"])
+        assert np.array_equal(stats.iterations, g[f"it{k}"])
+        assert np.array_equal(stats.doubling_steps, g[f"st{k}"])
+
+
 def test_step_law_random_single_window(cuda, co):
     """Criterion-2 law (acceptance.cpp:173-211) on trees that fit a warp."""
     for seed in range(1, 40):
