@@ -52,7 +52,14 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) {
     if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver)
       fail(ST_ERR_NO_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
-    fail(ST_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+    if (e == cudaErrorMemoryAllocation) {
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+        msg += " (device free " + std::to_string(fr >> 20) + " MiB of " + std::to_string(tot >> 20) + ")";
+      cudaGetLastError();
+    }
+    fail(ST_ERR_CUDA, msg);
   }
 }
 #define CK(x) cuda_check((x), #x)
@@ -900,7 +907,9 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   }
   sa.win_bytes = win_shared ? win_bytes : 0;
   if (stg.loader == kDirect) stg.ns = 1, stg.stage_bytes = 0;
-  stg.warps = pick_warps(g.warps_per_cta, stg, sa.win_bytes, pr);
+  // speculative is issue/latency-bound: several 8-warp CTAs per SM (the
+  // occupancy maximum) beat one wide CTA (C2: 0.52 vs 0.68 ms)
+  stg.warps = g.warps_per_cta ? pick_warps(g.warps_per_cta, stg, sa.win_bytes, pr) : kWarpsPerCta;
   sa.ns = stg.ns;
   sa.stage_bytes = stg.stage_bytes;
   const size_t smem = 1024 + sa.win_bytes + (size_t)stg.warps * stg.ns * (stg.stage_bytes + 8u) +
@@ -980,9 +989,9 @@ void launch_forest_smem(const Forest2Args& fa, const Staging& stg, size_t smem, 
 bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint64_t ld,
                       int layout, uint32_t* labels, cudaStream_t s, int dev, const DevProps& pr) {
   if (!(f->n_classes <= 8 && f->t_count <= 255) || f->max_tree_bytes > 48 * 1024) return false;
-  uint32_t S = 1;
-  while (S < 4 && 2 * S * a <= 128) S *= 2;  // tile of 32*S records, <= 16 KB for a = 64
-  if (!ct_arity(a)) S = 1;
+  // one record per lane (the tile is transposed to attribute-major once per
+  // round, which needs the record in registers); parallelism from wide CTAs
+  const uint32_t S = 1;
   if (!tma_ok(x, m, a, ld, layout, S)) return false;
   Staging stg;
   stg.loader = kTma;
@@ -995,7 +1004,7 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   stg.warps = 0;
   uint32_t nt = 0;
   size_t fixed = 0;
-  for (uint32_t w : {8u, 4u, 2u, 1u}) {
+  for (uint32_t w : {32u, 24u, 16u, 8u, 4u, 2u, 1u}) {
     for (uint32_t n : {4u, 3u, 2u}) {
       const size_t region = round1024((uint64_t)n * f->max_tree_bytes);
       const size_t need = 1024 + region + (size_t)w * (stg.stage_bytes + 8u) + 8u * n;

@@ -780,6 +780,22 @@ __global__ void __launch_bounds__(kMaxThreads)
       rec[q].init(tile, r, args.p.a, args.p.x, r0 + r, args.p.ld, 0);
       h0[q] = h1[q] = 0;
     }
+    // Transpose the tile in place to attribute-major (feature (a, lane) at
+    // tile + 4*(32a + lane)): every later feature read is bank-conflict free,
+    // and the record is read by all T trees, so the one-off cost vanishes.
+    constexpr bool kTranspose = (S == 1 && A > 0 && A <= 64);
+    if constexpr (kTranspose) {
+      if (have) {
+        float v[A > 0 ? A : 1];
+#pragma unroll
+        for (int a = 0; a < A; ++a) v[a] = rec[0].get(4u * a);
+        __syncwarp();
+#pragma unroll
+        for (int a = 0; a < A; ++a) sts_f32(tile + 4u * (32u * a + lane), v[a]);
+        __syncwarp();
+      }
+    }
+    const uint32_t soa = tile + 4u * lane;
     for (uint32_t tr = 0; tr < T; ++tr, ++gi) {
       // slot (gi + NT - 1) % NT last held tree gi - 1, released by the
       // barrier that ended the previous iteration
@@ -792,7 +808,9 @@ __global__ void __launch_bounds__(kMaxThreads)
         for (int q = 0; q < S; ++q) {
           uint2 nd = lds_u2(tb);
           while (!(nd.y & kLeafBit)) {
-            const float v = rec[q].get(nd.y & amask);
+            float v;
+            if constexpr (kTranspose) v = lds_f32(soa + ((nd.y & amask) << 5));
+            else v = rec[q].get(nd.y & amask);
             nd = lds_u2(tb + (nd.y >> args.abits) + (v > __uint_as_float(nd.x) ? 8u : 0u));
           }
           const uint32_t c = nd.y & ~kLeafBit;
