@@ -149,13 +149,19 @@ def dist_env():
 
 
 def ncu_traffic(workload, algo):
-    """dram bytes per launch from the committed ncu --set full summary."""
-    p = os.path.join(ROOT, "profiles", f"ncu_{workload}_{algo}.json")
-    try:
-        d = json.load(open(p))
-        return float(d["dram_bytes_per_launch"])
-    except Exception:
-        return None
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the newest
+    committed ncu --set full summary (profiles/r<N>_ncu_<workload>_<algo>.json)."""
+    import glob
+    import re
+
+    files = glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{workload}_{algo}.json"))
+    files.sort(key=lambda f: int(re.search(r"/r(\d+)_ncu_", f).group(1)))
+    for p in reversed(files):
+        try:
+            return float(json.load(open(p))["dram_bytes_per_launch"])
+        except Exception:
+            continue
+    return None
 
 
 # --------------------------------------------------------------- our arm ---

@@ -835,7 +835,7 @@ void eval_spec_exact_cta(st_tree* t, const float* x, uint64_t m, uint32_t a, uin
   ea.labels = labels;
   ea.iters = stats->iterations;
   ea.steps = stats->doubling_steps;
-  const size_t smem = 8ull * t->nodes.size();
+  const size_t smem = 8ull * t->nodes.size() + 16;
   if (smem > pr.smem_optin) fail(ST_ERR_ARGUMENT, "tree too large for exact speculative counters");
   const uint32_t threads = std::min<uint32_t>(1024, std::max<uint32_t>(32, (ea.I + 31) / 32 * 32));
   auto fn = k_spec_exact_cta;

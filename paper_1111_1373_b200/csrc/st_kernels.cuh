@@ -160,6 +160,24 @@ struct Rec {
       base = tile + r * (A > 0 ? (uint32_t)A : a_rt) * 4u;
     }
   }
+  // Move to record r_new of the same tile, dr records further on.
+  __device__ __forceinline__ void advance(uint32_t r_new, uint32_t dr, uint32_t a_rt, uint32_t tile,
+                                          const float* x, uint64_t row_new, uint32_t ld,
+                                          uint32_t soa) {
+    if constexpr (LOADER == kDirect) {
+      init(tile, r_new, a_rt, x, row_new, ld, soa);
+    } else if constexpr (kRowLocal) {
+      if constexpr ((A * 4) % 128 == 0) {
+        // whole rows per record: base moves by dr rows; xm only depends on r & 7
+        base += dr * (uint32_t)A * 4u;
+        xm = (((r_new * (uint32_t)A * 4u) >> 3) & 0x70u);
+      } else {
+        init(tile, r_new, a_rt, x, row_new, ld, soa);
+      }
+    } else {
+      base += dr * (A > 0 ? (uint32_t)A : a_rt) * 4u;
+    }
+  }
   __device__ __forceinline__ float get(uint32_t attr4) const {
     if constexpr (LOADER == kDirect) {
       return __ldg(gp + (uint64_t)(attr4 >> 2) * astride);
@@ -577,7 +595,8 @@ __global__ void __launch_bounds__(kMaxThreads)
           r += NG;
           active = r < rows;
           woff = 0;
-          rec.init(tile, active ? r : 0u, args.p.a, args.p.x, r0 + (active ? r : 0u), args.p.ld, args.p.layout_soa);
+          // idle groups keep walking their last record (finite, never stored)
+          if (active) rec.advance(r, NG, args.p.a, tile, args.p.x, r0 + r, args.p.ld, args.p.layout_soa);
         } else {
           woff = root & ~kExitBit;
         }
@@ -864,7 +883,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_spec_exact_cta(const SpecExactA
   extern __shared__ __align__(1024) unsigned char smem[];
   uint32_t* buf_a = reinterpret_cast<uint32_t*>(smem);
   uint32_t* buf_b = buf_a + args.n;
-  __shared__ uint32_t root_val;
+  uint32_t& root_val = buf_b[args.n];  // dynamic smem only: opt-in size stays valid
   for (uint32_t i = threadIdx.x; i < args.n; i += blockDim.x) buf_a[i] = buf_b[i] = i;
   __syncthreads();
   for (uint64_t r = blockIdx.x; r < args.p.m; r += gridDim.x) {
