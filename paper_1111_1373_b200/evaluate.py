@@ -142,7 +142,8 @@ def eval_gpu(tree, dataset, geom: Optional[GpuGeom] = None, stats: Optional["Spe
         sp = st_stats(stats.iterations.ctypes.data_as(C.c_void_p),
                       stats.doubling_steps.ctypes.data_as(C.c_void_p))
     L = _lib.load()
-    _check(L.st_eval(tree.handle().h, x.ctypes.data_as(C.c_void_p) if m else None, m,
+    h = tree.handle()  # keep the native tree alive for the whole call
+    _check(L.st_eval(h.h, x.ctypes.data_as(C.c_void_p) if m else None, m,
                      dataset.arity(), 0, lay, C.byref(g), out.ctypes.data_as(C.c_void_p) if m else None,
                      C.byref(sp) if sp is not None else None))
     if stats is not None:
@@ -342,7 +343,8 @@ def eval_device(tree, x, labels, geom: Optional[GpuGeom] = None, layout: str = "
     if stats is not None:
         sp = st_stats(C.c_void_p(stats[0].data_ptr()), C.c_void_p(stats[1].data_ptr()))
     L = _lib.load()
-    _check(L.st_eval_device(tree.handle().h, C.c_void_p(x.data_ptr()), m, a, ld, lay, C.byref(g),
+    h = tree.handle()
+    _check(L.st_eval_device(h.h, C.c_void_p(x.data_ptr()), m, a, ld, lay, C.byref(g),
                             C.c_void_p(labels.data_ptr()), C.byref(sp) if sp is not None else None,
                             _stream_handle(stream)))
 
@@ -358,7 +360,8 @@ def eval_sharded(tree, dataset, devices: Sequence[int], geom: Optional[GpuGeom] 
     g = (geom or GpuGeom()).to_c()
     x = dataset.values()
     L = _lib.load()
-    _check(L.st_eval_sharded(tree.handle().h, x.ctypes.data_as(C.c_void_p) if m else None, m,
+    h = tree.handle()
+    _check(L.st_eval_sharded(h.h, x.ctypes.data_as(C.c_void_p) if m else None, m,
                              dataset.arity(), 0, _lib.ST_LAYOUT_AOS, C.byref(g), devs, len(devices),
                              out.ctypes.data_as(C.c_void_p) if m else None))
     return out

@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import json
 import math
+import threading
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -80,6 +81,7 @@ class EncodedTree:
                     depth[c + 1] = depth[i] + 1
         self._depth = d
         self._handle = None
+        self._handle_lock = threading.Lock()
 
     # --- reference accessors ------------------------------------------------
     def size(self) -> int:
@@ -111,11 +113,17 @@ class EncodedTree:
 
     # --- device handle (created lazily, owned by this object) ---------------
     def handle(self):
-        if self._handle is None:
-            from .evaluate import _TreeHandle
+        """The native st_tree, created once (thread-safe: concurrent first
+        calls must not create and then free competing handles)."""
+        h = self._handle
+        if h is None:
+            with self._handle_lock:
+                if self._handle is None:
+                    from .evaluate import _TreeHandle
 
-            self._handle = _TreeHandle(self._nodes)
-        return self._handle
+                    self._handle = _TreeHandle(self._nodes)
+                h = self._handle
+        return h
 
 
 def encode_breadth_first(root: LinkedNode) -> EncodedTree:
