@@ -979,7 +979,9 @@ void launch_forest_smem(const Forest2Args& fa, const Staging& stg, size_t smem, 
                         cudaStream_t s) {
   auto fn = k_forest_smem<A, S>;
   const uint64_t n_tiles = (fa.p.m + 32 * S - 1) / (32 * S);
-  const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles, stg.warps);
+  // warp 0 of each CTA is the tree producer: tiles are spread over warps - 1
+  const int blocks = blocks_for((const void*)fn, smem, dev, 0,
+                                n_tiles * stg.warps / std::max<uint32_t>(1, stg.warps - 1), stg.warps);
   clear_stale_error();
   fn<<<blocks, stg.warps * 32, smem, s>>>(fa, stg.tmap);
   check_launch();
@@ -1004,14 +1006,14 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   stg.warps = 0;
   uint32_t nt = 0;
   size_t fixed = 0;
-  for (uint32_t w : {32u, 24u, 16u, 8u, 4u, 2u, 1u}) {
+  for (uint32_t w : {32u, 25u, 17u, 9u, 5u, 3u, 2u}) {  // 1 producer + w-1 consumer warps
     for (uint32_t n : {4u, 3u, 2u}) {
       const size_t region = round1024((uint64_t)n * f->max_tree_bytes);
-      const size_t need = 1024 + region + (size_t)w * (stg.stage_bytes + 8u) + 8u * n;
+      const size_t need = 1024 + region + (size_t)(w - 1) * (stg.stage_bytes + 8u) + 16u * n;
       if (need <= pr.smem_optin) {
         stg.warps = w;
         nt = n;
-        fixed = 1024 + region + 8u * n;
+        fixed = 1024 + region + 16u * n;
         break;
       }
     }
@@ -1033,7 +1035,7 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   fa.n_tree_bufs = nt;
   fa.tree_region = round1024((uint64_t)nt * f->max_tree_bytes);
   fa.tree_bytes = dv.tree_bytes;
-  const size_t smem = fixed + (size_t)stg.warps * (stg.stage_bytes + 8u);
+  const size_t smem = fixed + (size_t)(stg.warps - 1) * (stg.stage_bytes + 8u);
   switch (a) {
     case 8:
       if (S == 4) return launch_forest_smem<8, 4>(fa, stg, smem, dev, s), true;

@@ -733,6 +733,16 @@ struct Forest2Args {
   const uint32_t* tree_bytes;  // per tree: bytes to copy (16-aligned, device)
 };
 
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// Warp-specialised: warp 0 is the tree producer (one elected lane issues
+// cp.async.bulk into a ring of NT slots, gated by per-slot "empty" mbarriers
+// that every consumer warp arrives on); warps 1..nw-1 are consumers that walk
+// their resident record tile through each tree as soon as its "full" barrier
+// flips -- consumers drift up to NT trees apart instead of meeting at a CTA
+// barrier per tree.
 template <int A, int S>
 __global__ void __launch_bounds__(kMaxThreads)
     k_forest_smem(const Forest2Args args, const __grid_constant__ CUtensorMap tmap) {
@@ -740,51 +750,61 @@ __global__ void __launch_bounds__(kMaxThreads)
   constexpr int R = 32 * S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t nw = blockDim.x >> 5;
+  const uint32_t nc = nw - 1;  // consumer warps
   const uint32_t sbase = align1024(smem_u32(smem));
-  // [tree ring (1024-aligned)] [warp stages] [warp tile bars] [tree bars]
+  // [tree ring (1024-aligned)] [consumer stages] [consumer tile bars] [full bars] [empty bars]
   const uint32_t tbuf0 = sbase;
   const uint32_t tiles0 = sbase + args.tree_region;
+  const uint32_t NT = args.n_tree_bufs;
+  const uint32_t full0 = tiles0 + nc * (args.stage_bytes + 8u);
+  const uint32_t empty0 = full0 + 8u * NT;
+  const uint32_t T = args.t_count;
+
+  const uint64_t m = args.p.m;
+  const uint64_t n_tiles = (m + R - 1) / R;
+  const uint64_t step = (uint64_t)gridDim.x * nc;
+  const uint64_t base_tile = (uint64_t)blockIdx.x * nc;
+  const uint64_t my_rounds = base_tile < n_tiles ? (n_tiles - base_tile + step - 1) / step : 0;
+  const uint64_t total = my_rounds * T;  // trees this CTA streams
+
+  if (threadIdx.x == 0) {
+    for (uint32_t b = 0; b < NT; ++b) {
+      mbar_init(full0 + 8u * b, 1);
+      mbar_init(empty0 + 8u * b, nc);
+    }
+    fence_barrier_init();
+  }
   Pipe<A, S, kTma> pipe;
-  pipe.tiles = tiles0 + (uint32_t)warp * args.stage_bytes;
-  pipe.bars = tiles0 + nw * args.stage_bytes + (uint32_t)warp * 8u;
+  const uint32_t cw = warp > 0 ? (uint32_t)warp - 1 : 0u;
+  pipe.tiles = tiles0 + cw * args.stage_bytes;
+  pipe.bars = tiles0 + nc * args.stage_bytes + cw * 8u;
   pipe.stride_bytes = args.stage_bytes;
   pipe.ns = 1;
   pipe.tmap = &tmap;
   pipe.p = args.p;
   pipe.lane = lane;
-  const uint32_t tbar0 = tiles0 + nw * (args.stage_bytes + 8u);
-  const uint32_t T = args.t_count;
-  const uint32_t NT = args.n_tree_bufs;
-
-  const uint64_t m = args.p.m;
-  const uint64_t n_tiles = (m + R - 1) / R;
-  const uint64_t step = (uint64_t)gridDim.x * nw;
-  const uint64_t my_rounds =
-      blockIdx.x * (uint64_t)nw < n_tiles ? (n_tiles - blockIdx.x * (uint64_t)nw + step - 1) / step : 0;
-  const uint64_t total = my_rounds * T;  // trees this CTA streams
-
-  auto issue_tree = [&](uint64_t gi) {  // thread 0: tree (gi % T) into ring slot gi % NT
-    if (gi >= total) return;
-    const uint32_t tr = (uint32_t)(gi % T);
-    const uint32_t b = (uint32_t)(gi % NT);
-    const uint32_t bytes = __ldg(args.tree_bytes + tr);
-    mbar_arrive_expect_tx(tbar0 + 8u * b, bytes);
-    bulk_load(tbuf0 + b * args.tree_buf_bytes, args.nodes + __ldg(args.offsets + tr), bytes,
-              tbar0 + 8u * b);
-  };
-
-  if (threadIdx.x == 0) {
-    for (uint32_t b = 0; b < NT; ++b) mbar_init(tbar0 + 8u * b, 1);
-    fence_barrier_init();
-  }
-  const uint64_t first = (uint64_t)blockIdx.x * nw + warp;
-  pipe.start(first, step, n_tiles);  // per-warp tile barrier + first tile
+  const uint64_t first = base_tile + cw;
+  if (warp > 0) pipe.start(first, step, n_tiles);  // consumer tile barrier + first tile
   __syncthreads();
-  if (threadIdx.x == 0)
-    for (uint32_t b = 0; b + 1 < NT; ++b) issue_tree(b);  // NT-1 trees in flight
-  const uint32_t amask = (1u << args.abits) - 1u;
 
-  uint64_t gi = 0;  // tree sequence number within this CTA
+  if (warp == 0) {  // ---- producer -----------------------------------------
+    if (lane == 0) {
+      for (uint64_t gi = 0; gi < total; ++gi) {
+        const uint32_t b = (uint32_t)(gi % NT);
+        if (gi >= NT) mbar_wait(empty0 + 8u * b, (uint32_t)((gi / NT - 1) & 1u));
+        const uint32_t tr = (uint32_t)(gi % T);
+        const uint32_t bytes = __ldg(args.tree_bytes + tr);
+        mbar_arrive_expect_tx(full0 + 8u * b, bytes);
+        bulk_load(tbuf0 + b * args.tree_buf_bytes, args.nodes + __ldg(args.offsets + tr), bytes,
+                  full0 + 8u * b);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers -----------------------------------------------------------
+  const uint32_t amask = (1u << args.abits) - 1u;
+  uint64_t gi = 0;
   for (uint64_t k = 0; k < my_rounds; ++k) {
     const uint64_t t = first + k * step;
     const bool have = t < n_tiles;
@@ -816,11 +836,8 @@ __global__ void __launch_bounds__(kMaxThreads)
     }
     const uint32_t soa = tile + 4u * lane;
     for (uint32_t tr = 0; tr < T; ++tr, ++gi) {
-      // slot (gi + NT - 1) % NT last held tree gi - 1, released by the
-      // barrier that ended the previous iteration
-      if (threadIdx.x == 0) issue_tree(gi + NT - 1);
       const uint32_t b = (uint32_t)(gi % NT);
-      mbar_wait(tbar0 + 8u * b, (uint32_t)((gi / NT) & 1u));
+      mbar_wait(full0 + 8u * b, (uint32_t)((gi / NT) & 1u));
       if (have) {
         const uint32_t tb = tbuf0 + b * args.tree_buf_bytes;
 #pragma unroll
@@ -837,7 +854,8 @@ __global__ void __launch_bounds__(kMaxThreads)
           else h1[q] += 1u << (8 * (c - 4));
         }
       }
-      __syncthreads();  // every warp is done with slot b: it may be refilled
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty0 + 8u * b);  // this warp is done with slot b
     }
     if (have) {
 #pragma unroll
