@@ -1106,72 +1106,142 @@ bool is_pinned_or_device(const void* p) {
          at.type == cudaMemoryTypeManaged;
 }
 
-// Runs `kernel(x_dev, rows, ld_dev, labels_dev, stream)` over chunks of the
-// host records with H2D / kernel / D2H overlapped across two streams.
+// Per-device staging slots reused across host-path calls (a slot = stream +
+// device record/label buffers + pinned label staging), so the H2D/kernel/D2H
+// pipeline does not pay cudaMalloc/cudaFree per call.
+struct Slot {
+  cudaStream_t stream = nullptr;
+  float* x = nullptr;
+  size_t x_cap = 0;
+  uint32_t* out[3] = {nullptr, nullptr, nullptr};  // labels + up to 2 counters
+  uint32_t* pinned[3] = {nullptr, nullptr, nullptr};
+  size_t out_cap = 0;
+  bool busy = false;
+};
+
+class SlotPool {
+ public:
+  std::vector<Slot*> acquire(int dev, int n, size_t x_bytes, size_t rows) {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto& v = pools_[dev];
+    std::vector<Slot*> got;
+    for (auto& sp : v)
+      if (!sp->busy && (int)got.size() < n) got.push_back(sp.get());
+    while ((int)got.size() < n) {
+      v.push_back(std::make_unique<Slot>());
+      got.push_back(v.back().get());
+    }
+    for (Slot* sl : got) {
+      sl->busy = true;
+      try {
+        if (!sl->stream) CK(cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking));
+        if (sl->x_cap < x_bytes) {
+          cudaFree(sl->x);
+          sl->x = nullptr;
+          sl->x_cap = 0;
+          CK(cudaMalloc(&sl->x, x_bytes));
+          sl->x_cap = x_bytes;
+        }
+        if (sl->out_cap < rows) {
+          for (int k = 0; k < 3; ++k) {
+            cudaFree(sl->out[k]);
+            cudaFreeHost(sl->pinned[k]);
+            sl->out[k] = nullptr;
+            sl->pinned[k] = nullptr;
+          }
+          sl->out_cap = 0;
+          for (int k = 0; k < 3; ++k) {
+            CK(cudaMalloc(&sl->out[k], rows * 4));
+            CK(cudaMallocHost(&sl->pinned[k], rows * 4));
+          }
+          sl->out_cap = rows;
+        }
+      } catch (...) {
+        for (Slot* q : got) q->busy = false;
+        throw;
+      }
+    }
+    return got;
+  }
+  void release(const std::vector<Slot*>& s) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (Slot* sl : s) sl->busy = false;
+  }
+
+ private:
+  std::mutex mu_;
+  std::map<int, std::vector<std::unique_ptr<Slot>>> pools_;
+};
+
+SlotPool& slot_pool() {
+  static SlotPool* p = new SlotPool();  // intentionally leaked: outlives static destructors
+  return *p;
+}
+
+// Runs `kernel(x_dev, rows, ld_dev, labels_dev, extra_dev, stream)` over
+// chunks of the host records with H2D / kernel / D2H overlapped across
+// several streams.  Labels (and counters) come back through pinned staging
+// when the caller's buffers are pageable.
 template <class K>
 void host_pipeline(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
                    uint32_t* labels, std::vector<std::pair<uint32_t*, uint32_t*>> extra_out,
                    K&& kernel) {
-  constexpr int kStreams = 2;
+  constexpr int kStreams = 3;
   const uint64_t row_bytes = (uint64_t)a * 4;
-  uint64_t chunk = std::max<uint64_t>(256, (256ull << 20) / row_bytes);
+  uint64_t chunk = std::max<uint64_t>(256, (64ull << 20) / row_bytes);  // ~64 MB of records
   chunk = (chunk + 255) / 256 * 256;
   chunk = std::min<uint64_t>(chunk, m);
   const uint64_t n_chunks = (m + chunk - 1) / chunk;
   const int ns = (int)std::min<uint64_t>(kStreams, n_chunks);
-  cudaStream_t st[kStreams] = {};
-  float* xd[kStreams] = {};
-  uint32_t* ld_out[kStreams] = {};
-  std::vector<uint32_t*> extra_dev[kStreams];
-  struct Cleanup {
-    cudaStream_t* st;
-    float** xd;
-    uint32_t** lo;
-    std::vector<uint32_t*>* ex;
-    int n;
-    ~Cleanup() {
-      for (int i = 0; i < n; ++i) {
-        if (st[i]) cudaStreamSynchronize(st[i]);
-        cudaFree(xd[i]);
-        cudaFree(lo[i]);
-        for (auto p : ex[i]) cudaFree(p);
-        if (st[i]) cudaStreamDestroy(st[i]);
-      }
+  const int dev = current_device();
+  std::vector<Slot*> slots = slot_pool().acquire(dev, ns, chunk * row_bytes, chunk);
+  struct Release {
+    std::vector<Slot*>& s;
+    ~Release() {
+      for (Slot* sl : s) cudaStreamSynchronize(sl->stream);
+      slot_pool().release(s);
     }
-  } cleanup{st, xd, ld_out, extra_dev, ns};
-  const bool pin_in = is_pinned_or_device(x);
-  (void)pin_in;
-  for (int i = 0; i < ns; ++i) {
-    CK(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
-    CK(cudaMalloc(&xd[i], chunk * row_bytes));
-    CK(cudaMalloc(&ld_out[i], chunk * 4));
-    for (size_t e = 0; e < extra_out.size(); ++e) {
-      uint32_t* p = nullptr;
-      CK(cudaMalloc(&p, chunk * 4));
-      extra_dev[i].push_back(p);
-    }
-  }
+  } release{slots};
+  const bool pinned_labels = is_pinned_or_device(labels);
+  std::vector<uint32_t*> outs{labels};
+  for (auto& e : extra_out) outs.push_back(e.first);
+  // pending host copies out of pinned staging, per slot
+  std::vector<std::pair<uint64_t, uint64_t>> pending(ns, {0, 0});
+  auto drain = [&](int i) {
+    if (pinned_labels || pending[i].second == 0) return;
+    CK(cudaStreamSynchronize(slots[i]->stream));
+    for (size_t k = 0; k < outs.size(); ++k)
+      std::memcpy(outs[k] + pending[i].first, slots[i]->pinned[k], pending[i].second * 4);
+    pending[i] = {0, 0};
+  };
   for (uint64_t c = 0; c < n_chunks; ++c) {
     const int i = (int)(c % ns);
+    Slot* sl = slots[i];
+    drain(i);
     const uint64_t r0 = c * chunk;
     const uint64_t rows = std::min(chunk, m - r0);
     if (layout == ST_LAYOUT_AOS) {
       if (ld == a)
-        CK(cudaMemcpyAsync(xd[i], x + r0 * a, rows * row_bytes, cudaMemcpyHostToDevice, st[i]));
+        CK(cudaMemcpyAsync(sl->x, x + r0 * a, rows * row_bytes, cudaMemcpyDefault, sl->stream));
       else
-        CK(cudaMemcpy2DAsync(xd[i], row_bytes, x + r0 * ld, ld * 4, row_bytes, rows,
-                             cudaMemcpyHostToDevice, st[i]));
+        CK(cudaMemcpy2DAsync(sl->x, row_bytes, x + r0 * ld, ld * 4, row_bytes, rows,
+                             cudaMemcpyDefault, sl->stream));
     } else {
-      CK(cudaMemcpy2DAsync(xd[i], rows * 4, x + r0, ld * 4, rows * 4, a, cudaMemcpyHostToDevice,
-                           st[i]));
+      CK(cudaMemcpy2DAsync(sl->x, rows * 4, x + r0, ld * 4, rows * 4, a, cudaMemcpyDefault,
+                           sl->stream));
     }
-    kernel(xd[i], rows, layout == ST_LAYOUT_AOS ? (uint64_t)a : rows, ld_out[i], extra_dev[i], st[i]);
-    CK(cudaMemcpyAsync(labels + r0, ld_out[i], rows * 4, cudaMemcpyDeviceToHost, st[i]));
-    for (size_t e = 0; e < extra_out.size(); ++e)
-      CK(cudaMemcpyAsync(extra_out[e].first + r0, extra_dev[i][e], rows * 4, cudaMemcpyDeviceToHost,
-                         st[i]));
+    std::vector<uint32_t*> ex(sl->out + 1, sl->out + 1 + extra_out.size());
+    kernel(sl->x, rows, layout == ST_LAYOUT_AOS ? (uint64_t)a : rows, sl->out[0], ex, sl->stream);
+    for (size_t k = 0; k < outs.size(); ++k) {
+      uint32_t* dst = pinned_labels ? outs[k] + r0 : sl->pinned[k];
+      CK(cudaMemcpyAsync(dst, sl->out[k], rows * 4, cudaMemcpyDefault, sl->stream));
+    }
+    if (!pinned_labels) pending[i] = {r0, rows};
   }
-  for (int i = 0; i < ns; ++i) CK(cudaStreamSynchronize(st[i]));
+  for (int i = 0; i < ns; ++i) {
+    CK(cudaStreamSynchronize(slots[i]->stream));
+    drain(i);
+  }
 }
 
 }  // namespace
