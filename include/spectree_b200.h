@@ -82,7 +82,9 @@ typedef struct st_geom {
   uint32_t blocks_per_sm;      /* 0 = occupancy-derived persistent grid */
   uint32_t stages;             /* TMA record-pipeline stages per warp (0 = auto, 2-4) */
   uint32_t warps_per_cta;      /* CTA width in warps, 1-32 (0 = auto) */
-  uint32_t reserved[3];
+  uint32_t pipeline;           /* record staging: 0 = auto, 1 = per-warp TMA ring,
+                                  2 = CTA-shared TMA ring with a producer warp (speculative) */
+  uint32_t reserved[2];
 } st_geom;
 
 /* Optional per-record speculative counters (SpeculativeStats,

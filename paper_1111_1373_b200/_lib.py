@@ -41,7 +41,8 @@ class st_geom(C.Structure):
         ("blocks_per_sm", C.c_uint32),
         ("stages", C.c_uint32),
         ("warps_per_cta", C.c_uint32),
-        ("reserved", C.c_uint32 * 3),
+        ("pipeline", C.c_uint32),
+        ("reserved", C.c_uint32 * 2),
     ]
 
 

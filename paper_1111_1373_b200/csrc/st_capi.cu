@@ -780,6 +780,40 @@ void launch_spec_steps(const SpecArgs& sa, const Staging& stg, size_t smem, int 
   }
 }
 
+template <int A, bool WS, int STEPS>
+void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
+                        uint32_t warps, cudaStream_t s) {
+  auto fn = k_spec_ring<A, WS, STEPS>;
+  const uint64_t n_tiles = (ra.s.p.m + 31) / 32;
+  const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles * warps, warps);
+  clear_stale_error();
+  fn<<<blocks, warps * 32, smem, s>>>(ra, stg.tmap);
+  check_launch();
+}
+
+template <int A>
+void launch_spec_ring(bool ws, const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
+                      uint32_t warps, cudaStream_t s) {
+#define ST_RING(WSV, ST) return launch_spec_ring_k<A, WSV, ST>(ra, stg, smem, dev, warps, s)
+  if (ws) {
+    switch (ra.s.smax) {
+      case 0: ST_RING(true, 0);
+      case 1: ST_RING(true, 1);
+      case 2: ST_RING(true, 2);
+      case 3: ST_RING(true, 3);
+      default: ST_RING(true, -1);
+    }
+  }
+  switch (ra.s.smax) {
+    case 0: ST_RING(false, 0);
+    case 1: ST_RING(false, 1);
+    case 2: ST_RING(false, 2);
+    case 3: ST_RING(false, 3);
+    default: ST_RING(false, -1);
+  }
+#undef ST_RING
+}
+
 template <int A, int LOADER>
 void launch_spec_t(bool win_shared, const SpecArgs& sa, const Staging& stg, size_t smem, int dev,
                    uint32_t bps, cudaStream_t s) {
@@ -914,7 +948,30 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   sa.stage_bytes = stg.stage_bytes;
   const size_t smem = 1024 + sa.win_bytes + (size_t)stg.warps * stg.ns * (stg.stage_bytes + 8u) +
                       (size_t)stg.warps * 3 * 128;  // + per-warp label/counter rows
-  const uint32_t bps = g.blocks_per_sm;  // speculative is issue-bound: keep every resident CTA
+  const uint32_t bps = g.blocks_per_sm;  // speculative is latency-bound: keep every resident CTA
+  // CTA-shared ring (default for the fast path): one producer warp + up to 31
+  // consumer warps on one SM; ~12 tiles in flight cover DRAM latency.
+  if (stg.loader == kTma && !stats && g.pipeline != 1) {
+    const size_t lb = 2048;  // ticket + per-warp label rows
+    const size_t budget = pr.smem_optin - 1024 - sa.win_bytes - lb;
+    const size_t max_slots = budget / (stg.stage_bytes + 16u);
+    const uint32_t consumers = (uint32_t)std::min<size_t>(31, max_slots > 12 ? max_slots - 12 : 0);
+    if (consumers >= 4) {
+      SpecRingArgs ra{};
+      ra.s = sa;
+      ra.n_slots = (uint32_t)std::min<size_t>(max_slots, consumers + 12);
+      const uint32_t warps = consumers + 1;
+      const size_t rsmem = 1024 + sa.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 16u) + 16 +
+                           (size_t)warps * 128;
+      switch (ct_arity(a) ? a : 0) {
+        case 8: return launch_spec_ring<8>(win_shared, ra, stg, rsmem, dev, warps, s);
+        case 16: return launch_spec_ring<16>(win_shared, ra, stg, rsmem, dev, warps, s);
+        case 32: return launch_spec_ring<32>(win_shared, ra, stg, rsmem, dev, warps, s);
+        case 64: return launch_spec_ring<64>(win_shared, ra, stg, rsmem, dev, warps, s);
+        default: return launch_spec_ring<0>(win_shared, ra, stg, rsmem, dev, warps, s);
+      }
+    }
+  }
   if (stg.loader == kTma && ct_arity(a)) {
     switch (a) {
       case 8: return launch_spec_t<8, kTma>(win_shared, sa, stg, smem, dev, bps, s);

@@ -96,6 +96,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   do {
@@ -621,6 +624,161 @@ __global__ void __launch_bounds__(kMaxThreads)
 }
 
 // ---------------------------------------------------------------------------
+// K2r: speculative decomposition over a CTA-shared tile ring
+// ---------------------------------------------------------------------------
+// Same per-window algorithm as k_spec (fast fixed-step path), but the record
+// staging is decoupled from the warp count: warp 0 is a TMA producer filling
+// a ring of NS tile slots (full/empty mbarriers per slot); consumer warps take
+// tiles in ticket order (shared-memory counter), walk them, and release the
+// slot.  The speculative walk is latency-bound, so this buys ~1.7x the
+// resident warps for the same shared memory (only the tiles DRAM latency
+// needs are in flight, not two per warp).
+struct SpecRingArgs {
+  SpecArgs s;
+  uint32_t n_slots;       // NS
+};
+
+template <int A, bool WIN_SHARED, int STEPS>
+__global__ void __launch_bounds__(kMaxThreads)
+    k_spec_ring(const SpecRingArgs ra, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const SpecArgs& args = ra.s;
+  constexpr int R = 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t NS = ra.n_slots;
+  const uint32_t sbase = align1024(smem_u32(smem));
+
+  if constexpr (WIN_SHARED) {
+    const uint4* src = reinterpret_cast<const uint4*>(args.win);
+    for (uint32_t i = threadIdx.x; i < args.n_entries; i += blockDim.x) {
+      const uint4 v = __ldg(src + i);
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
+                   "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
+    }
+  }
+  // [windows] [NS slots] [full bars] [empty bars] [ticket] [per-warp label rows]
+  const uint32_t slots0 = sbase + args.win_bytes;
+  const uint32_t full0 = slots0 + NS * args.stage_bytes;
+  const uint32_t empty0 = full0 + 8u * NS;
+  const uint32_t ticket = empty0 + 8u * NS;
+  const uint32_t lbuf = ticket + 16u + (uint32_t)warp * 128u;
+
+  const uint64_t m = args.p.m;
+  const uint64_t n_tiles = (m + R - 1) / R;
+  const uint64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto tile_of = [&](uint64_t j) { return blockIdx.x + j * (uint64_t)gridDim.x; };
+  auto full_tile = [&](uint64_t t) { return (t + 1) * (uint64_t)R <= m; };
+  const uint32_t a_rt = A > 0 ? (uint32_t)A : args.p.a;
+
+  if (threadIdx.x == 0) {
+    for (uint32_t b = 0; b < NS; ++b) {
+      mbar_init(full0 + 8u * b, 1);
+      mbar_init(empty0 + 8u * b, 1);
+    }
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ticket), "r"(0u) : "memory");
+    fence_barrier_init();
+    tma_prefetch_desc(&tmap);
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // ---- producer ----------------------------------------
+    if (lane == 0) {
+      for (uint64_t j = 0; j < my_tiles; ++j) {
+        const uint64_t t = tile_of(j);
+        if (!full_tile(t)) break;  // the partial tail is staged by its consumer
+        const uint32_t b = (uint32_t)(j % NS);
+        if (j >= NS) mbar_wait(empty0 + 8u * b, (uint32_t)((j / NS - 1) & 1u));
+        const uint32_t bytes = R * a_rt * 4u;
+        mbar_arrive_expect_tx(full0 + 8u * b, bytes);
+        tma_load_2d(slots0 + b * args.stage_bytes, &tmap, 0, (int)(t * (uint64_t)R * a_rt / 32u),
+                    full0 + 8u * b);
+      }
+    }
+    return;
+  }
+
+  const uint32_t G = args.G;
+  const uint32_t NG = 32u / G;
+  const uint32_t g = lane / G;
+  const uint32_t j = lane & (G - 1);
+  const uint32_t gmask = G - 1;
+  const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + 16u * j;
+  const char* wglob = reinterpret_cast<const char*>(args.win) + 16u * j;
+
+  while (true) {
+    uint32_t tk = 0;
+    if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(tk) : "r"(ticket) : "memory");
+    tk = __shfl_sync(0xffffffffu, tk, 0);
+    if (tk >= my_tiles) break;
+    const uint64_t t = tile_of(tk);
+    const uint64_t r0 = t * (uint64_t)R;
+    const uint32_t b = tk % NS;
+    const uint32_t tile = slots0 + b * args.stage_bytes;
+    const uint32_t rows = (uint32_t)((m - r0) < (uint64_t)R ? (m - r0) : (uint64_t)R);
+    if (full_tile(t)) {
+      mbar_wait(full0 + 8u * b, (tk / NS) & 1u);
+    } else {  // tail tile: warp-cooperative store into the swizzled layout
+      if (tk >= NS) mbar_wait(empty0 + 8u * b, (uint32_t)((tk / NS - 1) & 1u));
+      for (uint32_t f = lane; f < rows * a_rt; f += 32) {
+        const uint32_t r = f / a_rt, aa = f - r * a_rt;
+        sts_f32(tile + swz(f * 4u), __ldg(args.p.x + (r0 + r) * (uint64_t)args.p.ld + aa));
+      }
+      __syncwarp();
+    }
+    if (args.root_code & kLeafBit) {  // N == 1
+      if (lane < rows)
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * lane), "r"(args.root_code) : "memory");
+    } else {
+      uint32_t r = g;
+      bool active = r < rows;
+      uint32_t woff = 0;
+      Rec<A, kTma> rec;
+      rec.init(tile, active ? r : 0u, args.p.a, args.p.x, 0, 0, 0);
+      do {
+        uint4 e;
+        if constexpr (WIN_SHARED) e = lds_u4(jaddr + woff);
+        else e = __ldg(reinterpret_cast<const uint4*>(wglob + woff));
+        const float v = rec.get(e.y & 0x00FFFFFFu);
+        uint32_t c = (v > __uint_as_float(e.x)) ? e.w : e.z;
+        if constexpr (STEPS >= 0) {
+#pragma unroll
+          for (int s = 0; s < STEPS; ++s) {
+            const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+            c = (c < 32u) ? u : c;
+          }
+        } else {
+          for (uint32_t s = 0; s < args.smax; ++s) {
+            const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+            c = (c < 32u) ? u : c;
+          }
+        }
+        const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
+        if (root & kLeafBit) {
+          if (active && j == 0)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(root) : "memory");
+          r += NG;
+          active = r < rows;
+          woff = 0;
+          if (active) rec.advance(r, NG, args.p.a, tile, args.p.x, 0, 0, 0);
+        } else {
+          woff = root & ~kExitBit;
+        }
+      } while (__any_sync(0xffffffffu, active));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8u * b);  // slot b may be refilled
+    if (lane < rows) {
+      uint32_t code;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(code) : "r"(lbuf + 4u * lane));
+      const uint32_t cls = code & ~kLeafBit;
+      args.labels[r0 + lane] = args.leaf_class ? __ldg(args.leaf_class + cls) : cls;
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3: random forest with per-record majority vote
 // ---------------------------------------------------------------------------
 struct ForestArgs {
@@ -732,10 +890,6 @@ struct Forest2Args {
   uint32_t tree_region;        // bytes reserved for the ring (1024-aligned)
   const uint32_t* tree_bytes;  // per tree: bytes to copy (16-aligned, device)
 };
-
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
 
 // Warp-specialised: warp 0 is the tree producer (one elected lane issues
 // cp.async.bulk into a ring of NT slots, gated by per-slot "empty" mbarriers

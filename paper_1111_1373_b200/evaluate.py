@@ -55,6 +55,7 @@ class GpuGeom:
     blocks_per_sm: int = 0
     stages: int = 0                 # TMA record-pipeline stages per warp
     warps_per_cta: int = 0          # CTA width (warps)
+    pipeline: int = 0               # 0 auto, 1 per-warp TMA ring, 2 CTA-shared ring (spec)
 
     def to_c(self) -> st_geom:
         g = st_geom()
@@ -71,6 +72,7 @@ class GpuGeom:
         g.blocks_per_sm = self.blocks_per_sm
         g.stages = self.stages
         g.warps_per_cta = self.warps_per_cta
+        g.pipeline = self.pipeline
         return g
 
 

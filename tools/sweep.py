@@ -33,8 +33,8 @@ if "data" in args.grid:
         geoms.append(st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=S, stages=ns, blocks_per_sm=bps,
                                 warps_per_cta=w))
 if "spec" in args.grid:
-    for G, ns, bps in itertools.product([2, 4, 8, 16], [2, 3], [0, 2, 3, 4]):
-        geoms.append(st.GpuGeom(algo="speculative", group_lanes=G, stages=ns, blocks_per_sm=bps))
+    for G, pl in itertools.product([2, 4, 8, 16], [1, 2]):
+        geoms.append(st.GpuGeom(algo="speculative", group_lanes=G, pipeline=pl))
 if "warps" in args.grid:
     for tl, S, w in itertools.product(["shared", "global"], [0, 1, 2], [0, 8, 16, 32]):
         geoms.append(st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=S, warps_per_cta=w))
