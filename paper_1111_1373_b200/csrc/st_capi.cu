@@ -949,19 +949,18 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   const size_t smem = 1024 + sa.win_bytes + (size_t)stg.warps * stg.ns * (stg.stage_bytes + 8u) +
                       (size_t)stg.warps * 3 * 128;  // + per-warp label/counter rows
   const uint32_t bps = g.blocks_per_sm;  // speculative is latency-bound: keep every resident CTA
-  // CTA-shared ring (default for the fast path): one producer warp + up to 31
-  // consumer warps on one SM; ~12 tiles in flight cover DRAM latency.
+  // CTA-shared ring (default for the fast path): up to 32 warps on one SM
+  // share NS = warps + 12 tile slots; ~12 tiles in flight cover DRAM latency.
   if (stg.loader == kTma && !stats && g.pipeline != 1) {
     const size_t lb = 2048;  // ticket + per-warp label rows
     const size_t budget = pr.smem_optin - 1024 - sa.win_bytes - lb;
     const size_t max_slots = budget / (stg.stage_bytes + 16u);
-    const uint32_t consumers = (uint32_t)std::min<size_t>(31, max_slots > 12 ? max_slots - 12 : 0);
-    if (consumers >= 4) {
+    const uint32_t warps = (uint32_t)std::min<size_t>(32, max_slots > 12 ? max_slots - 12 : 0);
+    if (warps >= 4) {
       SpecRingArgs ra{};
       ra.s = sa;
-      ra.n_slots = (uint32_t)std::min<size_t>(max_slots, consumers + 12);
-      const uint32_t warps = consumers + 1;
-      const size_t rsmem = 1024 + sa.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 16u) + 16 +
+      ra.n_slots = (uint32_t)std::min<size_t>(max_slots, warps + 12);
+      const size_t rsmem = 1024 + sa.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 8u) + 16 +
                            (size_t)warps * 128;
       switch (ct_arity(a) ? a : 0) {
         case 8: return launch_spec_ring<8>(win_shared, ra, stg, rsmem, dev, warps, s);

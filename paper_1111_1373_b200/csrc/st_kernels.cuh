@@ -627,12 +627,13 @@ __global__ void __launch_bounds__(kMaxThreads)
 // K2r: speculative decomposition over a CTA-shared tile ring
 // ---------------------------------------------------------------------------
 // Same per-window algorithm as k_spec (fast fixed-step path), but the record
-// staging is decoupled from the warp count: warp 0 is a TMA producer filling
-// a ring of NS tile slots (full/empty mbarriers per slot); consumer warps take
-// tiles in ticket order (shared-memory counter), walk them, and release the
-// slot.  The speculative walk is latency-bound, so this buys ~1.7x the
-// resident warps for the same shared memory (only the tiles DRAM latency
-// needs are in flight, not two per warp).
+// staging is decoupled from the warp count: the CTA owns a ring of NS tile
+// slots; warps take tiles in ticket order (shared-memory counter) and the warp
+// that finishes tile k refills the same slot with tile k + NS (TMA, or a
+// warp-cooperative store for the one partial tail tile) -- no producer to
+// block behind a slow tile.  The speculative walk is latency-bound, so this
+// buys ~1.7x the resident warps for the same shared memory (only the tiles
+// DRAM latency needs are in flight, not two per warp).
 struct SpecRingArgs {
   SpecArgs s;
   uint32_t n_slots;       // NS
@@ -657,46 +658,48 @@ __global__ void __launch_bounds__(kMaxThreads)
                    : "memory");
     }
   }
-  // [windows] [NS slots] [full bars] [empty bars] [ticket] [per-warp label rows]
+  // [windows] [NS slots] [full bars] [ticket] [per-warp label rows]
   const uint32_t slots0 = sbase + args.win_bytes;
   const uint32_t full0 = slots0 + NS * args.stage_bytes;
-  const uint32_t empty0 = full0 + 8u * NS;
-  const uint32_t ticket = empty0 + 8u * NS;
+  const uint32_t ticket = full0 + 8u * NS;
   const uint32_t lbuf = ticket + 16u + (uint32_t)warp * 128u;
 
   const uint64_t m = args.p.m;
   const uint64_t n_tiles = (m + R - 1) / R;
   const uint64_t my_tiles = blockIdx.x < n_tiles ? (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  auto tile_of = [&](uint64_t j) { return blockIdx.x + j * (uint64_t)gridDim.x; };
-  auto full_tile = [&](uint64_t t) { return (t + 1) * (uint64_t)R <= m; };
   const uint32_t a_rt = A > 0 ? (uint32_t)A : args.p.a;
+  auto tile_of = [&](uint64_t j) { return blockIdx.x + j * (uint64_t)gridDim.x; };
+  // Stage tile j into slot b: TMA for full tiles (lane 0), warp-cooperative
+  // swizzled stores + a plain arrive for the partial tail.
+  auto fill = [&](uint64_t jj) {
+    const uint64_t t = tile_of(jj);
+    const uint32_t b = (uint32_t)(jj % NS);
+    const uint32_t dst = slots0 + b * args.stage_bytes;
+    const uint64_t r0 = t * (uint64_t)R;
+    if ((t + 1) * (uint64_t)R <= m) {
+      if (lane == 0) {
+        mbar_arrive_expect_tx(full0 + 8u * b, R * a_rt * 4u);
+        tma_load_2d(dst, &tmap, 0, (int)(r0 * a_rt / 32u), full0 + 8u * b);
+      }
+    } else {
+      const uint32_t rows = (uint32_t)(m - r0);
+      for (uint32_t f = lane; f < rows * a_rt; f += 32) {
+        const uint32_t r = f / a_rt, aa = f - r * a_rt;
+        sts_f32(dst + swz(f * 4u), __ldg(args.p.x + (r0 + r) * (uint64_t)args.p.ld + aa));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(full0 + 8u * b);
+    }
+  };
 
   if (threadIdx.x == 0) {
-    for (uint32_t b = 0; b < NS; ++b) {
-      mbar_init(full0 + 8u * b, 1);
-      mbar_init(empty0 + 8u * b, 1);
-    }
+    for (uint32_t b = 0; b < NS; ++b) mbar_init(full0 + 8u * b, 1);
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(ticket), "r"(0u) : "memory");
     fence_barrier_init();
-    tma_prefetch_desc(&tmap);
   }
   __syncthreads();
-
-  if (warp == 0) {  // ---- producer ----------------------------------------
-    if (lane == 0) {
-      for (uint64_t j = 0; j < my_tiles; ++j) {
-        const uint64_t t = tile_of(j);
-        if (!full_tile(t)) break;  // the partial tail is staged by its consumer
-        const uint32_t b = (uint32_t)(j % NS);
-        if (j >= NS) mbar_wait(empty0 + 8u * b, (uint32_t)((j / NS - 1) & 1u));
-        const uint32_t bytes = R * a_rt * 4u;
-        mbar_arrive_expect_tx(full0 + 8u * b, bytes);
-        tma_load_2d(slots0 + b * args.stage_bytes, &tmap, 0, (int)(t * (uint64_t)R * a_rt / 32u),
-                    full0 + 8u * b);
-      }
-    }
-    return;
-  }
+  if (warp == 0)
+    for (uint64_t jj = 0; jj < NS && jj < my_tiles; ++jj) fill(jj);
 
   const uint32_t G = args.G;
   const uint32_t NG = 32u / G;
@@ -705,6 +708,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t gmask = G - 1;
   const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + 16u * j;
   const char* wglob = reinterpret_cast<const char*>(args.win) + 16u * j;
+  if constexpr (WIN_SHARED) __syncthreads();  // window table staged
 
   while (true) {
     uint32_t tk = 0;
@@ -716,16 +720,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     const uint32_t b = tk % NS;
     const uint32_t tile = slots0 + b * args.stage_bytes;
     const uint32_t rows = (uint32_t)((m - r0) < (uint64_t)R ? (m - r0) : (uint64_t)R);
-    if (full_tile(t)) {
-      mbar_wait(full0 + 8u * b, (tk / NS) & 1u);
-    } else {  // tail tile: warp-cooperative store into the swizzled layout
-      if (tk >= NS) mbar_wait(empty0 + 8u * b, (uint32_t)((tk / NS - 1) & 1u));
-      for (uint32_t f = lane; f < rows * a_rt; f += 32) {
-        const uint32_t r = f / a_rt, aa = f - r * a_rt;
-        sts_f32(tile + swz(f * 4u), __ldg(args.p.x + (r0 + r) * (uint64_t)args.p.ld + aa));
-      }
-      __syncwarp();
-    }
+    mbar_wait(full0 + 8u * b, (tk / NS) & 1u);
     if (args.root_code & kLeafBit) {  // N == 1
       if (lane < rows)
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * lane), "r"(args.root_code) : "memory");
@@ -767,7 +762,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       } while (__any_sync(0xffffffffu, active));
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8u * b);  // slot b may be refilled
+    if (tk + NS < my_tiles) fill(tk + NS);  // this warp freed slot b: refill it
     if (lane < rows) {
       uint32_t code;
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(code) : "r"(lbuf + 4u * lane));
