@@ -952,7 +952,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // CTA-shared ring (default for the fast path): up to 32 warps on one SM
   // share NS = warps + 12 tile slots; ~12 tiles in flight cover DRAM latency.
   if (stg.loader == kTma && !stats && g.pipeline != 1) {
-    const size_t lb = 2048;  // ticket + per-warp label rows
+    const size_t lb = 16 + 32 * 128;  // ticket + per-warp label rows (up to 32 warps)
     const size_t budget = pr.smem_optin - 1024 - sa.win_bytes - lb;
     const size_t max_slots = budget / (stg.stage_bytes + 16u);
     const uint32_t warps = (uint32_t)std::min<size_t>(32, max_slots > 12 ? max_slots - 12 : 0);
