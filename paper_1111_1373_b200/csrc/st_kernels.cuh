@@ -336,18 +336,6 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t nw = blockDim.x >> 5;  // warps in this CTA
   const uint32_t sbase = align1024(smem_u32(smem));
 
-  // ---- stage the node array once per CTA --------------------------------
-  if constexpr (TLOC == kShared) {
-    const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
-    const uint32_t n16 = (args.n_nodes * 8u + 15u) / 16u;
-    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
-      const uint4 v = __ldg(src + i);
-      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
-                   "r"(v.y), "r"(v.z), "r"(v.w)
-                   : "memory");
-    }
-    __syncthreads();
-  }
   TreeRef<TLOC, CAP> tree{sbase, reinterpret_cast<const char*>(args.nodes), &ctree};
 
   Pipe<A, S, LOADER> pipe;
@@ -364,8 +352,23 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint64_t n_tiles = (m + R - 1) / R;
   const uint64_t step = (uint64_t)gridDim.x * nw;
   const uint64_t first = (uint64_t)blockIdx.x * nw + warp;
+  // first record tiles in flight before the tree is staged (the TMA does not
+  // depend on it): the tree copy hides under the DRAM latency of the records
   pipe.start(first, step, n_tiles);
   const uint32_t amask = (1u << args.abits) - 1u;
+
+  // ---- stage the node array once per CTA --------------------------------
+  if constexpr (TLOC == kShared) {
+    const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
+    const uint32_t n16 = (args.n_nodes * 8u + 15u) / 16u;
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
+      const uint4 v = __ldg(src + i);
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
+                   "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
+    }
+    __syncthreads();
+  }
 
   uint64_t i = 0;
   for (uint64_t t = first; t < n_tiles; t += step, ++i) {
@@ -649,15 +652,6 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t NS = ra.n_slots;
   const uint32_t sbase = align1024(smem_u32(smem));
 
-  if constexpr (WIN_SHARED) {
-    const uint4* src = reinterpret_cast<const uint4*>(args.win);
-    for (uint32_t i = threadIdx.x; i < args.n_entries; i += blockDim.x) {
-      const uint4 v = __ldg(src + i);
-      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
-                   "r"(v.y), "r"(v.z), "r"(v.w)
-                   : "memory");
-    }
-  }
   // [windows] [NS slots] [full bars] [ticket] [per-warp label rows]
   const uint32_t slots0 = sbase + args.win_bytes;
   const uint32_t full0 = slots0 + NS * args.stage_bytes;
@@ -700,6 +694,16 @@ __global__ void __launch_bounds__(kMaxThreads)
   __syncthreads();
   if (warp == 0)
     for (uint64_t jj = 0; jj < NS && jj < my_tiles; ++jj) fill(jj);
+  // window table staged while the first tiles are in flight
+  if constexpr (WIN_SHARED) {
+    const uint4* src = reinterpret_cast<const uint4*>(args.win);
+    for (uint32_t i = threadIdx.x; i < args.n_entries; i += blockDim.x) {
+      const uint4 v = __ldg(src + i);
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
+                   "r"(v.y), "r"(v.z), "r"(v.w)
+                   : "memory");
+    }
+  }
 
   const uint32_t G = args.G;
   const uint32_t NG = 32u / G;

@@ -1,8 +1,11 @@
 """Measure every canonical configuration on one B200:
 C1, C2, C3 (frames/s), C4 (128-tree forest), C5 depth sweep 8..20 with the
 speculative / data ratio per depth.  CUDA-event timing of device-resident
-records; L2 is flushed (256 MB write) before every timed launch for the
-configs whose inputs fit in L2.  Writes gpurun_out/workloads.json.
+records; L2 is flushed before every timed launch for the configs whose inputs
+fit in L2: --flush read (default) reads a 256 MB buffer, leaving L2 full of
+clean lines; --flush write zeroes it, which leaves ~126 MB of dirty lines whose
+write-back then competes with the timed kernel's reads (reported for
+comparison).  Writes gpurun_out/workloads.json.
 
     python tools/workloads.py [--only C1,C5] [--iters 20]
 """
@@ -36,7 +39,7 @@ def timed(fn, iters, flush=None):
     evs = []
     for _ in range(iters):
         if flush is not None:
-            flush.zero_()
+            flush()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record()
@@ -64,12 +67,12 @@ def graph_time(fn, iters, flush=None):
     with torch.cuda.graph(g1):
         for _ in range(iters):
             if flush is not None:
-                flush.zero_()
+                flush()
             fn()
     with torch.cuda.graph(g0):
         for _ in range(iters):
             if flush is not None:
-                flush.zero_()
+                flush()
     def t(g):
         g.replay()
         torch.cuda.synchronize()
@@ -83,11 +86,22 @@ def graph_time(fn, iters, flush=None):
     return max(0.0, (t(g1) - t(g0)) / iters)
 
 
+FLUSH_MODE = "read"
+
+
+def make_flush():
+    buf = torch.ones(2 * L2 // 4, dtype=torch.float32, device="cuda")
+    acc = torch.empty((), dtype=torch.float32, device="cuda")
+    if FLUSH_MODE == "write":
+        return lambda: buf.zero_()
+    return lambda: torch.sum(buf, dim=0, out=acc)
+
+
 def run_tree(name, tree, x, labels_fnv, geoms, iters, unit_div=1.0, unit="samples/s"):
     m, a = x.shape
     xd = torch.from_numpy(x).cuda()
     out = torch.empty(m, dtype=torch.int32, device="cuda")
-    flush = torch.empty(2 * L2 // 4, dtype=torch.float32, device="cuda") if 4 * a * m < 2 * L2 else None
+    flush = make_flush() if 4 * a * m < 2 * L2 else None
     res = {}
     for gname, g in geoms:
         st.eval_device(tree, xd, out, g)
@@ -97,7 +111,7 @@ def run_tree(name, tree, x, labels_fnv, geoms, iters, unit_div=1.0, unit="sample
         timing = "events per launch (host launch latency included)"
         if flush is not None:  # small input: replay a CUDA graph to drop host overhead
             ms = graph_time(lambda: st.eval_device(tree, xd, out, g), iters, flush)
-            timing = "cuda-graph replay, L2 flushed before every launch"
+            timing = f"cuda-graph replay, L2 flushed ({FLUSH_MODE}) before every launch"
         gbs = 4 * a * m / (ms * 1e-3) / 1e9
         res[gname] = {"ms": round(ms, 5), "value": m / (ms * 1e-3) / unit_div, "unit": unit,
                       "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 4), "labels_ok": bool(ok),
@@ -113,7 +127,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="C1,C2,C3,C4,C5")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--flush", choices=("read", "write"), default="read")
     args = ap.parse_args()
+    global FLUSH_MODE
+    FLUSH_MODE = args.flush
     only = args.only.split(",")
     data_g = ("data", st.GpuGeom(algo="data"))
     spec_g = ("speculative", st.GpuGeom(algo="speculative"))
@@ -121,7 +138,7 @@ def main():
     spec_g8 = ("speculative-G8", st.GpuGeom(algo="speculative", group_lanes=8))
     spec_g16 = ("speculative-G16", st.GpuGeom(algo="speculative", group_lanes=16))
     geoms = [data_g, spec_g, spec_g2, spec_g8, spec_g16]
-    out = {"peak_GBs": PEAK, "device": torch.cuda.get_device_name(0)}
+    out = {"peak_GBs": PEAK, "device": torch.cuda.get_device_name(0), "flush": FLUSH_MODE}
     W = bench.WORKLOADS
     for name in ("C1", "C2", "C3"):
         if name not in only:
@@ -168,7 +185,7 @@ def main():
                      "trees": 128, "node_visits_per_s_est": len(x) * 128 * 9.09 / (ms * 1e-3)}
         print("C4", json.dumps(out["C4"]), flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "workloads.json"), "w") as fh:
+    with open(os.path.join(ROOT, "gpurun_out", f"workloads_{FLUSH_MODE}.json"), "w") as fh:
         json.dump(out, fh, indent=1)
 
 
