@@ -100,6 +100,7 @@ typedef struct st_tree_info {
   uint32_t compact;        /* 1 if the 8-byte device node format applies */
   uint32_t spec_windows;   /* speculative windows for the default geometry */
   uint32_t spec_group_lanes;
+  uint32_t max_class;      /* largest leaf class id (u8 label files need < 256) */
 } st_tree_info;
 
 typedef struct st_tree st_tree;
@@ -155,6 +156,68 @@ int st_forest_eval(const st_forest* forest, const float* x, uint64_t m, uint32_t
                    uint64_t ld, int layout, uint32_t* labels);
 int st_forest_eval_device(const st_forest* forest, const float* x, uint64_t m, uint32_t a,
                           uint64_t ld, int layout, uint32_t* labels, void* stream);
+
+/* One unpipelined host round trip with per-phase timing: the GPU edition of
+ * the reference bench windows (bench.hpp:50-56, bench.cpp:228-262) and of the
+ * paper's Table 1 (allocation, copy-in, kernel, copy-out, release):
+ *   outer_us = the whole call on the host steady clock (alloc + H2D + kernel
+ *              + D2H + free), the reference's "outer" window
+ *   inner_us = the evaluation kernel(s) only (CUDA events), the "inner" window
+ *   alloc_us = device buffer cudaMalloc + cudaFree (host clock), "alloc"
+ *   h2d_us / d2h_us = the record and label copies (CUDA events)
+ * Same arguments, validation and labels as st_eval (stats not supported). */
+typedef struct st_timing {
+  double outer_us, inner_us, alloc_us, h2d_us, d2h_us;
+} st_timing;
+int st_eval_timed(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                  int layout, const st_geom* geom, uint32_t* labels, st_timing* timing);
+
+/* ---- record and label files at scale ------------------
+ * The reference's CSV loader (io.cpp:80-117) is parse-bound; this is a raw
+ * little-endian float32 format that streams at disk / PCIe speed.
+ *
+ * Record file: 64-byte header, then count*arity float32 (AoS: record-major,
+ * SoA: attribute-major).
+ *   @0 char[8] "STREC001"   @8 u32 version = 1   @12 u32 layout (st_layout)
+ *   @16 u64 count           @24 u32 arity (>= 1, dataset.cpp:10-14)
+ *   @28 u32 flags (bit 0: checksum present)      @32 u64 checksum
+ *   @40..63 zero
+ * checksum = dataset_checksum (dataset.cpp:76-93) of the records in record
+ * order, so a file round-trips to the reference's own checksum.
+ * Label file: 32-byte header, then count labels of `width` bytes (4 = u32,
+ * 1 = u8 when every class < 256).
+ *   @0 char[8] "STLAB001"   @8 u32 version = 1   @12 u32 width (1 | 4)
+ *   @16 u64 count           @24..31 zero
+ * Malformed headers / short files return ST_ERR_IO (the reference's
+ * IoError / ParseError exit code 3). */
+typedef struct st_dataset_info {
+  uint64_t count;
+  uint32_t arity;
+  uint32_t layout;
+  uint32_t has_checksum;
+  uint64_t checksum;
+  uint64_t data_offset; /* byte offset of the first value */
+} st_dataset_info;
+
+int st_dataset_save(const char* path, const float* x, uint64_t m, uint32_t a, int layout,
+                    int with_checksum);
+int st_dataset_info_read(const char* path, st_dataset_info* out);
+/* Reads records [first, first+count) into `out` (count*arity floats, AoS,
+ * whatever the file layout).  verify != 0 re-computes the header checksum
+ * over the whole file first (ST_ERR_IO on mismatch). */
+int st_dataset_load(const char* path, uint64_t first, uint64_t count, float* out, int verify);
+int st_labels_save(const char* path, const uint32_t* labels, uint64_t m, uint32_t width);
+/* count of labels in the file (and width); out may be NULL to size. */
+int st_labels_load(const char* path, uint32_t* out, uint64_t cap, uint64_t* count, uint32_t* width);
+
+/* Streams a record file through the GPU: a reader thread fills pinned
+ * buffers with ~64 MB chunks while the previous chunks are copied in,
+ * evaluated (st_eval_device) and their labels copied out and appended to
+ * `labels_path` (width 1 narrows to u8 on the device; ST_ERR_ARGUMENT when a
+ * leaf class is >= 256).  The whole file never has to fit in host memory
+ * (C5: 10^9 records = 64 GB).  *records_out (nullable) = records classified. */
+int st_eval_file(const st_tree* tree, const char* data_path, const st_geom* geom,
+                 const char* labels_path, uint32_t width, uint64_t* records_out);
 
 /* Number of kernel launches the last successful evaluating call on this
  * thread enqueued (for bench.py's gpu_launches claim). */

@@ -16,6 +16,8 @@ from .evaluate import (DataParallelConfig, Forest, GpuGeom, ReductionMode, Specu
                        eval_forest_device, eval_gpu, eval_sharded, eval_speculative,
                        eval_speculative_basic, last_launch_count, tree_info,
                        validate_data_parallel, validate_speculative)
+from .files import (dataset_info, eval_file, load_dataset_bin, load_labels_bin,
+                    save_dataset_bin, save_labels_bin)
 from .synthetic import (dataset_checksum, fnv1a64, generate_synthetic_dataset,
                         generate_synthetic_tree)
 from .tree import (NO_CLASS, NODE_DTYPE, Diagnostic, EncodedTree, LinkedNode, decode,

@@ -60,7 +60,18 @@ class st_tree_info(C.Structure):
         ("compact", C.c_uint32),
         ("spec_windows", C.c_uint32),
         ("spec_group_lanes", C.c_uint32),
+        ("max_class", C.c_uint32),
     ]
+
+
+class st_timing(C.Structure):
+    _fields_ = [("outer_us", C.c_double), ("inner_us", C.c_double), ("alloc_us", C.c_double),
+                ("h2d_us", C.c_double), ("d2h_us", C.c_double)]
+
+
+class st_dataset_info(C.Structure):
+    _fields_ = [("count", C.c_uint64), ("arity", C.c_uint32), ("layout", C.c_uint32),
+                ("has_checksum", C.c_uint32), ("checksum", C.c_uint64), ("data_offset", C.c_uint64)]
 
 
 # Every symbol declared in include/spectree_b200.h (checked by tests).
@@ -71,6 +82,8 @@ EXPORTS = (
     "st_eval", "st_eval_device", "st_eval_sharded",
     "st_forest_eval", "st_forest_eval_device", "st_last_launch_count",
     "st_synthetic_tree", "st_synthetic_dataset", "st_dataset_checksum", "st_fnv1a64",
+    "st_eval_timed", "st_dataset_save", "st_dataset_info_read", "st_dataset_load",
+    "st_labels_save", "st_labels_load", "st_eval_file",
 )
 
 _lib = None
@@ -122,6 +135,22 @@ def load() -> C.CDLL:
     L.st_dataset_checksum.argtypes = [vp, u64, u32]
     L.st_fnv1a64.restype = u64
     L.st_fnv1a64.argtypes = [vp, u64]
+    cp = C.c_char_p
+    L.st_eval_timed.restype = i32
+    L.st_eval_timed.argtypes = [vp, vp, u64, u32, u64, i32, C.POINTER(st_geom), vp,
+                                C.POINTER(st_timing)]
+    L.st_dataset_save.restype = i32
+    L.st_dataset_save.argtypes = [cp, vp, u64, u32, i32, i32]
+    L.st_dataset_info_read.restype = i32
+    L.st_dataset_info_read.argtypes = [cp, C.POINTER(st_dataset_info)]
+    L.st_dataset_load.restype = i32
+    L.st_dataset_load.argtypes = [cp, u64, u64, vp, i32]
+    L.st_labels_save.restype = i32
+    L.st_labels_save.argtypes = [cp, vp, u64, u32]
+    L.st_labels_load.restype = i32
+    L.st_labels_load.argtypes = [cp, vp, u64, C.POINTER(u64), C.POINTER(u32)]
+    L.st_eval_file.restype = i32
+    L.st_eval_file.argtypes = [vp, cp, C.POINTER(st_geom), cp, u32, C.POINTER(u64)]
     _lib = L
     return L
 

@@ -13,7 +13,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRCS = [os.path.join(HERE, "csrc", "st_capi.cu"), os.path.join(HERE, "csrc", "st_synth.cpp")]
+SRCS = [os.path.join(HERE, "csrc", "st_capi.cu"), os.path.join(HERE, "csrc", "st_io.cu"),
+        os.path.join(HERE, "csrc", "st_synth.cpp")]
 DEPS = [*SRCS, os.path.join(HERE, "csrc", "st_kernels.cuh"),
         os.path.join(ROOT, "include", "spectree_b200.h")]
 OUT = os.path.join(HERE, "libspectree_b200.so")

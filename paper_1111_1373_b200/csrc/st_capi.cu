@@ -16,6 +16,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -134,6 +135,7 @@ struct WinTable {
 
 namespace st_internal {
 void set_error(const std::string& msg) { g_error = msg; }
+void set_launches(uint32_t n) { g_launches = n; }
 }  // namespace st_internal
 
 struct st_tree {
@@ -406,6 +408,7 @@ std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
     if (nd.class_id != ST_NO_CLASS) {
       ++in.leaves;
       in.depth = std::max(in.depth, depth[i]);
+      in.max_class = std::max(in.max_class, nd.class_id);
       if (nd.class_id >= kLeafBit) t->leaf_table = true;
     } else {
       ++in.internal;
@@ -1446,6 +1449,82 @@ int st_eval(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_
                     g_launches = 0;
                   });
     g_launches = launches;
+  });
+}
+
+int st_eval_timed(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                  int layout, const st_geom* geom, uint32_t* labels, st_timing* timing) {
+  return guarded([&] {
+    g_launches = 0;
+    using Clock = std::chrono::steady_clock;
+    auto us = [](Clock::duration d) { return std::chrono::duration<double, std::micro>(d).count(); };
+    st_tree* t = const_cast<st_tree*>(tree);
+    if (!t) fail(ST_ERR_ARGUMENT, "null tree");
+    if (!timing) fail(ST_ERR_ARGUMENT, "null timing output");
+    uint64_t ld2 = ld;
+    check_common(m, a, ld2, layout, t->info.max_attribute);
+    st_geom g{};
+    if (geom) g = *geom;
+    resolve_algo(t, g, false);
+    *timing = st_timing{};
+    if (m == 0) return;
+    if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
+    current_device();
+    t->device(current_device());  // device replica outside the timed windows
+    struct Ev {
+      cudaStream_t s = nullptr;
+      cudaEvent_t e[4] = {};
+      ~Ev() {
+        for (auto& x : e)
+          if (x) cudaEventDestroy(x);
+        if (s) cudaStreamDestroy(s);
+      }
+    } ev;
+    CK(cudaStreamCreateWithFlags(&ev.s, cudaStreamNonBlocking));
+    for (auto& e : ev.e) CK(cudaEventCreate(&e));
+    const uint64_t row_bytes = (uint64_t)a * 4;
+    const auto o0 = Clock::now();
+    float* xd = nullptr;
+    uint32_t* ld_out = nullptr;
+    CK(cudaMalloc(&xd, m * row_bytes));
+    struct Free {
+      void* p[2];
+      ~Free() {
+        for (void* q : p)
+          if (q) cudaFree(q);
+      }
+    } guard{{xd, nullptr}};
+    CK(cudaMalloc(&ld_out, m * 4));
+    guard.p[1] = ld_out;
+    const auto a1 = Clock::now();
+    CK(cudaEventRecord(ev.e[0], ev.s));
+    if (layout == ST_LAYOUT_AOS) {
+      if (ld2 == a)
+        CK(cudaMemcpyAsync(xd, x, m * row_bytes, cudaMemcpyDefault, ev.s));
+      else
+        CK(cudaMemcpy2DAsync(xd, row_bytes, x, ld2 * 4, row_bytes, m, cudaMemcpyDefault, ev.s));
+    } else {
+      CK(cudaMemcpy2DAsync(xd, m * 4, x, ld2 * 4, m * 4, a, cudaMemcpyDefault, ev.s));
+    }
+    CK(cudaEventRecord(ev.e[1], ev.s));
+    eval_device_impl(t, xd, m, a, layout == ST_LAYOUT_AOS ? (uint64_t)a : m, layout, &g, ld_out,
+                     nullptr, ev.s);
+    CK(cudaEventRecord(ev.e[2], ev.s));
+    CK(cudaMemcpyAsync(labels, ld_out, m * 4, cudaMemcpyDefault, ev.s));
+    CK(cudaEventRecord(ev.e[3], ev.s));
+    CK(cudaStreamSynchronize(ev.s));
+    const auto f0 = Clock::now();
+    guard.p[0] = guard.p[1] = nullptr;
+    CK(cudaFree(xd));
+    CK(cudaFree(ld_out));
+    const auto o1 = Clock::now();
+    float ms[3];
+    for (int k = 0; k < 3; ++k) CK(cudaEventElapsedTime(&ms[k], ev.e[k], ev.e[k + 1]));
+    timing->outer_us = us(o1 - o0);
+    timing->alloc_us = us(a1 - o0) + us(o1 - f0);
+    timing->h2d_us = 1e3 * ms[0];
+    timing->inner_us = 1e3 * ms[1];
+    timing->d2h_us = 1e3 * ms[2];
   });
 }
 
