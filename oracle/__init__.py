@@ -201,6 +201,10 @@ class RefOracle:
                                                                          vp, vp]
         L.ref_traversal_depths.restype = C.c_int
         L.ref_traversal_depths.argtypes = [vp, vp, vp]
+        L.ref_simulate_data_parallel.restype = C.c_int
+        L.ref_simulate_data_parallel.argtypes = [vp, vp, C.c_uint32, C.c_int, C.c_uint32, C.c_uint32, vp]
+        L.ref_simulate_speculative.restype = C.c_int
+        L.ref_simulate_speculative.argtypes = [vp, vp, C.c_uint32, C.c_int] + [C.c_uint32] * 4 + [C.c_int, vp]
         L.ref_load_tree_json.restype = C.c_int
         L.ref_load_tree_json.argtypes = [C.c_char_p, vp, C.c_uint32, C.POINTER(C.c_uint32)]
         L.ref_tree_to_json.restype = C.c_uint64
@@ -315,6 +319,25 @@ class RefTree:
             int(basic), os_threads, out.ctypes.data_as(C.c_void_p),
             it.ctypes.data_as(C.c_void_p), st.ctypes.data_as(C.c_void_p), C.byref(bar)))
         return out, it, st, bar.value
+
+    METRICS = ("divergent_branches", "serialized_passes", "barriers", "node_evals",
+               "reduction_iterations", "lane_idle_slots")
+
+    def simulate_data_parallel(self, d, workers, chunk, warp_width=32, half_warp=True) -> dict:
+        """warp_sim.cpp:30-99 (reference lockstep model) -> ExecMetrics dict."""
+        out = (C.c_uint64 * 6)()
+        self.ref._check(self.ref.L.ref_simulate_data_parallel(self.h, d.h, warp_width, int(half_warp),
+                                                              workers, chunk, out))
+        return dict(zip(self.METRICS, [int(v) for v in out]))
+
+    def simulate_speculative(self, d, group_lanes, groups, records_per_group, k=1, basic=False,
+                             warp_width=32, half_warp=True) -> dict:
+        """warp_sim.cpp:156-274 (reference lockstep model) -> ExecMetrics dict."""
+        out = (C.c_uint64 * 6)()
+        self.ref._check(self.ref.L.ref_simulate_speculative(self.h, d.h, warp_width, int(half_warp),
+                                                            group_lanes, groups, records_per_group, k,
+                                                            int(basic), out))
+        return dict(zip(self.METRICS, [int(v) for v in out]))
 
     def traversal_depths(self, d):
         out = np.empty(d.m, dtype=np.uint32)

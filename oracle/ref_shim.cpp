@@ -13,6 +13,7 @@
 //   dataset_checksum / tile_dataset                       (dataset.cpp:35-93)
 //   load_tree_json / tree_to_json                         (io.cpp:156-263)
 //   validate                                              (tree.cpp:138-189)
+//   simulate_data_parallel / simulate_speculative         (warp_sim.cpp:30-274)
 //
 // Errors are caught and returned as the CLI's exit-code taxonomy
 // (main.cpp:703-712): 2 = ArgumentError family, 3 = other spectree::Error.
@@ -25,6 +26,7 @@
 #include <spectree/io.hpp>
 #include <spectree/synthetic.hpp>
 #include <spectree/tree.hpp>
+#include <spectree/warp_sim.hpp>
 
 #include <cstdint>
 #include <cstring>
@@ -190,6 +192,51 @@ int ref_traversal_depths(void* t, void* d, std::uint32_t* out) {
     std::vector<std::uint32_t> r = traversal_depths(static_cast<RefTree*>(t)->tree,
                                                     static_cast<RefData*>(d)->data);
     std::memcpy(out, r.data(), r.size() * 4);
+  });
+}
+
+// --- lockstep warp model (warp_sim.cpp) ------------------------------------
+// out[6] = {divergent_branches, serialized_passes, barriers, node_evals,
+//           reduction_iterations, lane_idle_slots} (warp_sim.hpp:37-44)
+static void put_metrics(const ExecMetrics& m, std::uint64_t* out) {
+  out[0] = m.divergent_branches;
+  out[1] = m.serialized_passes;
+  out[2] = m.barriers;
+  out[3] = m.node_evals;
+  out[4] = m.reduction_iterations;
+  out[5] = m.lane_idle_slots;
+}
+
+int ref_simulate_data_parallel(void* t, void* d, std::uint32_t warp_width, int half_warp,
+                               std::uint32_t workers, std::uint32_t chunk, std::uint64_t* out) {
+  return guarded([&] {
+    WarpConfig w;
+    w.warp_width = warp_width;
+    w.half_warp = half_warp != 0;
+    DataParallelConfig c;
+    c.workers = workers;
+    c.chunk = chunk;
+    put_metrics(simulate_data_parallel(static_cast<RefTree*>(t)->tree, static_cast<RefData*>(d)->data, w, c),
+                out);
+  });
+}
+
+int ref_simulate_speculative(void* t, void* d, std::uint32_t warp_width, int half_warp,
+                             std::uint32_t group_lanes, std::uint32_t groups,
+                             std::uint32_t records_per_group, std::uint32_t reductions, int basic,
+                             std::uint64_t* out) {
+  return guarded([&] {
+    WarpConfig w;
+    w.warp_width = warp_width;
+    w.half_warp = half_warp != 0;
+    SpeculativeConfig c;
+    c.group_lanes = group_lanes;
+    c.groups = groups;
+    c.records_per_group = records_per_group;
+    c.reductions_per_iteration = reductions;
+    put_metrics(simulate_speculative(static_cast<RefTree*>(t)->tree, static_cast<RefData*>(d)->data, w, c,
+                                     basic ? SpeculativeVariant::all_lanes : SpeculativeVariant::mapped_lanes),
+                out);
   });
 }
 

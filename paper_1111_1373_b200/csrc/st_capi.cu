@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -680,11 +681,12 @@ void launch_data_tloc(int tloc, const DataArgs& d, const Staging& stg, const st_
 bool ct_arity(uint32_t a) { return a == 8 || a == 16 || a == 32 || a == 64; }
 
 uint32_t choose_S(uint32_t a, uint32_t want) {
-  // instantiated: a=8 {1,2,4}, a=16 {1,2}, a=32 {1,2}, others {1}
-  const uint32_t maxS = a == 8 ? 4 : (a == 16 || a == 32) ? 2 : 1;
-  // one record per lane; more warps beat more walks per lane (sweeps in
-  // profiles/), except 8-attribute records whose 1 KB tiles are too small
-  if (want == 0) want = a <= 8 ? 2 : 1;
+  // instantiated: a=8 {1,2,4}, a=16 {1,2,4}, a=32 {1,2}, others {1}
+  const uint32_t maxS = (a == 8 || a == 16) ? 4 : a == 32 ? 2 : 1;
+  // predicated walk (k_data data_step): independent chains per lane pay off
+  // where a tile is small -- C3 (a = 8): S = 4 0.63 ms vs S = 2 0.67 ms for 32
+  // frames; C2 (a = 32): S = 2 0.307 vs S = 1 0.321 ms (profiles/r1_sweep_*)
+  if (want == 0) want = a <= 8 ? 4 : a == 32 ? 2 : 1;
   uint32_t S = 1;
   while (S * 2 <= std::min(want, maxS)) S *= 2;
   return S;
@@ -693,7 +695,7 @@ uint32_t choose_S(uint32_t a, uint32_t want) {
 template <int A>
 void launch_data_a(const Staging& stg, int tloc, const DataArgs& d, const st_tree* t, size_t smem,
                    int dev, uint32_t bps, cudaStream_t s) {
-  if constexpr (A == 8) {
+  if constexpr (A == 8 || A == 16) {
     if (stg.S == 4) return launch_data_tloc<A, 4, kTma>(tloc, d, stg, t, smem, dev, bps, s);
   }
   if constexpr (A == 8 || A == 16 || A == 32) {
@@ -1033,10 +1035,10 @@ void launch_forest_t(bool packed, const ForestArgs& fa, const Staging& stg, size
   check_launch();
 }
 
-template <int A, int S>
+template <int A, int S, int U>
 void launch_forest_smem(const Forest2Args& fa, const Staging& stg, size_t smem, int dev,
                         cudaStream_t s) {
-  auto fn = k_forest_smem<A, S>;
+  auto fn = k_forest_smem<A, S, U>;
   const uint64_t n_tiles = (fa.p.m + 32 * S - 1) / (32 * S);
   // warp 0 of each CTA is the tree producer: tiles are spread over warps - 1
   const int blocks = blocks_for((const void*)fn, smem, dev, 0,
@@ -1044,6 +1046,21 @@ void launch_forest_smem(const Forest2Args& fa, const Staging& stg, size_t smem, 
   clear_stale_error();
   fn<<<blocks, stg.warps * 32, smem, s>>>(fa, stg.tmap);
   check_launch();
+}
+
+template <int A, int S>
+void launch_forest_u(uint32_t U, const Forest2Args& fa, const Staging& stg, size_t smem, int dev,
+                     cudaStream_t s) {
+  if constexpr (S == 1 && A > 0 && A <= 64) {  // the transposed-tile walk takes U chains
+    if (U >= 4) return launch_forest_smem<A, S, 4>(fa, stg, smem, dev, s);
+    if (U == 2) return launch_forest_smem<A, S, 2>(fa, stg, smem, dev, s);
+  }
+  return launch_forest_smem<A, S, 1>(fa, stg, smem, dev, s);
+}
+
+uint32_t env_u32(const char* name, uint32_t dflt) {  // development knobs for sweeps
+  const char* v = std::getenv(name);
+  return v && *v ? (uint32_t)std::strtoul(v, nullptr, 10) : dflt;
 }
 
 // Trees streamed through shared memory (packed votes, TMA-staged records).
@@ -1059,24 +1076,29 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   stg.S = S;
   stg.ns = 1;
   stg.stage_bytes = round1024(32ull * S * a * 4);
-  // Tree ring: deep enough that the next trees' loads overlap walking the
-  // current one (a 16 KB tree takes longer to arrive from L2 than 512 records
-  // take to walk it); the rest of shared memory holds resident record tiles.
+  // Geometry: U trees walked per lane at once (U dependent-load chains), a
+  // ring of NT tree slots, and as many consumer warps as the rest of shared
+  // memory holds record tiles for.  The C4 sweep (profiles/r1_forest_sweep.json)
+  // put U = 2 with NT = U + 2 first (8.3 ms vs 10.3 ms for U = 1, NT = 2):
+  // the walk is bound by shared-memory wavefronts of the node loads, so more
+  // chains than that only add ring slots at the expense of record tiles.
+  const bool transposed = S == 1 && a <= 64 && ct_arity(a);
+  const uint32_t U = std::max<uint32_t>(1, std::min<uint32_t>(4, env_u32("ST_FOREST_U", transposed ? 2 : 1)));
+  uint32_t nt = env_u32("ST_FOREST_NT", 0);
+  if (nt == 0) nt = U + 2;
+  if (!transposed && U != 1) return false;
   stg.warps = 0;
-  uint32_t nt = 0;
   size_t fixed = 0;
-  for (uint32_t w : {32u, 25u, 17u, 9u, 5u, 3u, 2u}) {  // 1 producer + w-1 consumer warps
-    for (uint32_t n : {4u, 3u, 2u}) {
-      const size_t region = round1024((uint64_t)n * f->max_tree_bytes);
-      const size_t need = 1024 + region + (size_t)(w - 1) * (stg.stage_bytes + 8u) + 16u * n;
-      if (need <= pr.smem_optin) {
-        stg.warps = w;
-        nt = n;
-        fixed = 1024 + region + 16u * n;
-        break;
-      }
-    }
-    if (stg.warps) break;
+  for (uint32_t n = nt; n >= std::max<uint32_t>(2, U) && !stg.warps; --n) {
+    const size_t region = round1024((uint64_t)n * f->max_tree_bytes);
+    const size_t base = 1024 + region + 16u * n;
+    if (base >= pr.smem_optin) continue;
+    uint32_t w = (uint32_t)std::min<size_t>(32, 1 + (pr.smem_optin - base) / (stg.stage_bytes + 8u));
+    if (const uint32_t ww = env_u32("ST_FOREST_W", 0)) w = std::min(w, ww);
+    if (w < 2) continue;
+    stg.warps = w;
+    nt = n;
+    fixed = base;
   }
   if (!stg.warps) return false;
   make_tmap(stg, x, m, a);
@@ -1096,22 +1118,11 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   fa.tree_bytes = dv.tree_bytes;
   const size_t smem = fixed + (size_t)(stg.warps - 1) * (stg.stage_bytes + 8u);
   switch (a) {
-    case 8:
-      if (S == 4) return launch_forest_smem<8, 4>(fa, stg, smem, dev, s), true;
-      if (S == 2) return launch_forest_smem<8, 2>(fa, stg, smem, dev, s), true;
-      return launch_forest_smem<8, 1>(fa, stg, smem, dev, s), true;
-    case 16:
-      if (S == 4) return launch_forest_smem<16, 4>(fa, stg, smem, dev, s), true;
-      if (S == 2) return launch_forest_smem<16, 2>(fa, stg, smem, dev, s), true;
-      return launch_forest_smem<16, 1>(fa, stg, smem, dev, s), true;
-    case 32:
-      if (S == 2) return launch_forest_smem<32, 2>(fa, stg, smem, dev, s), true;
-      return launch_forest_smem<32, 1>(fa, stg, smem, dev, s), true;
-    case 64:
-      if (S == 2) return launch_forest_smem<64, 2>(fa, stg, smem, dev, s), true;
-      return launch_forest_smem<64, 1>(fa, stg, smem, dev, s), true;
-    default:
-      return launch_forest_smem<0, 1>(fa, stg, smem, dev, s), true;
+    case 8: return launch_forest_u<8, 1>(U, fa, stg, smem, dev, s), true;
+    case 16: return launch_forest_u<16, 1>(U, fa, stg, smem, dev, s), true;
+    case 32: return launch_forest_u<32, 1>(U, fa, stg, smem, dev, s), true;
+    case 64: return launch_forest_u<64, 1>(U, fa, stg, smem, dev, s), true;
+    default: return launch_forest_u<0, 1>(U, fa, stg, smem, dev, s), true;
   }
 }
 

@@ -326,6 +326,33 @@ __device__ __forceinline__ uint32_t align1024(uint32_t a) { return (a + 1023u) &
 // ---------------------------------------------------------------------------
 // K1: data decomposition
 // ---------------------------------------------------------------------------
+// One predicated level step of the data walk over a swizzled record tile
+// whose record sits inside one 128-byte row (A | 32): if the node is internal,
+// node = tb + child + 8*(x[attr] > thr).  bx = row base | in-row XOR mask, so
+// the feature address is one LOP3 ((4*attr) ^ bx); leaves stay put with no
+// branch and no shared-memory traffic.  Ordered compare, no FTZ (tree.hpp:53).
+__device__ __forceinline__ void data_step(uint32_t& thr, uint32_t& meta, uint32_t bx, uint32_t tb,
+                                          uint32_t amask, uint32_t abits) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q;\n\t"
+      ".reg .u32 fa, ch;\n\t"
+      ".reg .f32 v;\n\t"
+      "setp.ge.s32 p, %1, 0;\n\t"
+      "and.b32 fa, %1, %4;\n\t"
+      "xor.b32 fa, fa, %2;\n\t"
+      "@p ld.shared.f32 v, [fa];\n\t"
+      "setp.gt.and.f32 q, v, %0, p;\n\t"
+      "shr.u32 ch, %1, %5;\n\t"
+      "add.u32 ch, ch, %3;\n\t"
+      "@q add.u32 ch, ch, 8;\n\t"
+      "@p ld.shared.v2.u32 {%0, %1}, [ch];\n\t"
+      "}"
+      : "+f"(*reinterpret_cast<float*>(&thr)), "+r"(meta)
+      : "r"(bx), "r"(tb), "r"(amask), "r"(abits)
+      : "memory");
+}
+
 template <int A, int S, int TLOC, int LOADER, int CAP>
 __global__ void __launch_bounds__(kMaxThreads)
     k_data(const DataArgs args, const __grid_constant__ CUtensorMap tmap,
@@ -388,6 +415,35 @@ __global__ void __launch_bounds__(kMaxThreads)
           nd = __ldg(args.wide + c);
         }
         args.labels[r0 + r] = nd.w;
+      }
+    } else if constexpr (TLOC == kShared && LOADER == kTma && Rec<A, LOADER>::kRowLocal) {
+      // S independent predicated chains per lane (no per-level branches)
+      uint32_t thr[S], meta[S], bx[S];
+      const uint2 root = tree.get(0);
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint32_t r = q * 32 + lane;
+        Rec<A, LOADER> rec;
+        rec.init(tile, r, args.p.a, args.p.x, 0, 0, 0);
+        bx[q] = rec.base | rec.xm;
+        thr[q] = root.x;
+        meta[q] = (r0 + r < m) ? root.y : kLeafBit;  // idle slot in the tail tile
+      }
+      while (true) {
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < S; ++q) any |= (int)meta[q] >= 0;
+        if (!any) break;
+#pragma unroll
+        for (int q = 0; q < S; ++q) data_step(thr[q], meta[q], bx[q], tree.s, amask, args.abits);
+      }
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint64_t r = r0 + q * 32 + lane;
+        if (r < m) {
+          const uint32_t c = meta[q] & ~kLeafBit;
+          args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+        }
       }
     } else if constexpr (S == 1) {
       const uint32_t r = lane;
@@ -895,8 +951,38 @@ struct Forest2Args {
 // that every consumer warp arrives on); warps 1..nw-1 are consumers that walk
 // their resident record tile through each tree as soon as its "full" barrier
 // flips -- consumers drift up to NT trees apart instead of meeting at a CTA
-// barrier per tree.
-template <int A, int S>
+// barrier per tree.  Each consumer lane walks U trees at once (U independent
+// dependent-load chains per lane: the walk is shared-memory-latency bound, so
+// chains per SM, not warps, are what hide it; U trees cost tree-ring slots,
+// which are cheaper than record tiles).
+
+// One predicated level step of a forest walk over an attribute-major record
+// tile: if the node is internal, node = tb + child + 8*(x[attr] > thr).
+// Leaves are left untouched (no branch, no shared-memory traffic).
+__device__ __forceinline__ void forest_step(uint32_t& thr, uint32_t& meta, uint32_t tb, uint32_t soa,
+                                            uint32_t amask, uint32_t abits) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q;\n\t"
+      ".reg .u32 fa, ch;\n\t"
+      ".reg .f32 v;\n\t"
+      "setp.ge.s32 p, %1, 0;\n\t"
+      "and.b32 fa, %1, %4;\n\t"
+      "shl.b32 fa, fa, 5;\n\t"
+      "add.u32 fa, fa, %3;\n\t"
+      "@p ld.shared.f32 v, [fa];\n\t"
+      "setp.gt.and.f32 q, v, %0, p;\n\t"
+      "shr.u32 ch, %1, %5;\n\t"
+      "add.u32 ch, ch, %2;\n\t"
+      "@q add.u32 ch, ch, 8;\n\t"
+      "@p ld.shared.v2.u32 {%0, %1}, [ch];\n\t"
+      "}"
+      : "+f"(*reinterpret_cast<float*>(&thr)), "+r"(meta)
+      : "r"(tb), "r"(soa), "r"(amask), "r"(abits)
+      : "memory");
+}
+
+template <int A, int S, int U>
 __global__ void __launch_bounds__(kMaxThreads)
     k_forest_smem(const Forest2Args args, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -942,14 +1028,15 @@ __global__ void __launch_bounds__(kMaxThreads)
 
   if (warp == 0) {  // ---- producer -----------------------------------------
     if (lane == 0) {
+      uint32_t b = 0, ph = 0, tr = 0;
       for (uint64_t gi = 0; gi < total; ++gi) {
-        const uint32_t b = (uint32_t)(gi % NT);
-        if (gi >= NT) mbar_wait(empty0 + 8u * b, (uint32_t)((gi / NT - 1) & 1u));
-        const uint32_t tr = (uint32_t)(gi % T);
+        if (gi >= NT) mbar_wait(empty0 + 8u * b, ph ^ 1u);
         const uint32_t bytes = __ldg(args.tree_bytes + tr);
         mbar_arrive_expect_tx(full0 + 8u * b, bytes);
         bulk_load(tbuf0 + b * args.tree_buf_bytes, args.nodes + __ldg(args.offsets + tr), bytes,
                   full0 + 8u * b);
+        if (++tr == T) tr = 0;
+        if (++b == NT) b = 0, ph ^= 1u;
       }
     }
     return;
@@ -957,7 +1044,7 @@ __global__ void __launch_bounds__(kMaxThreads)
 
   // ---- consumers -----------------------------------------------------------
   const uint32_t amask = (1u << args.abits) - 1u;
-  uint64_t gi = 0;
+  uint32_t b0 = 0, ph0 = 0;  // ring slot / phase of the next tree this warp consumes
   for (uint64_t k = 0; k < my_rounds; ++k) {
     const uint64_t t = first + k * step;
     const bool have = t < n_tiles;
@@ -988,27 +1075,71 @@ __global__ void __launch_bounds__(kMaxThreads)
       }
     }
     const uint32_t soa = tile + 4u * lane;
-    for (uint32_t tr = 0; tr < T; ++tr, ++gi) {
-      const uint32_t b = (uint32_t)(gi % NT);
-      mbar_wait(full0 + 8u * b, (uint32_t)((gi / NT) & 1u));
-      if (have) {
-        const uint32_t tb = tbuf0 + b * args.tree_buf_bytes;
+    for (uint32_t tr = 0; tr < T; tr += U) {
+      const uint32_t nu = min((uint32_t)U, T - tr);  // trees in this step
+      uint32_t tb[U], thr[U], meta[U], slot[U];
 #pragma unroll
-        for (int q = 0; q < S; ++q) {
-          uint2 nd = lds_u2(tb);
-          while (!(nd.y & kLeafBit)) {
-            float v;
-            if constexpr (kTranspose) v = lds_f32(soa + ((nd.y & amask) << 5));
-            else v = rec[q].get(nd.y & amask);
-            nd = lds_u2(tb + (nd.y >> args.abits) + (v > __uint_as_float(nd.x) ? 8u : 0u));
+      for (int u = 0; u < U; ++u) {
+        slot[u] = b0;
+        tb[u] = tbuf0 + b0 * args.tree_buf_bytes;
+        meta[u] = kLeafBit;
+        thr[u] = 0;
+        if ((uint32_t)u < nu) {
+          mbar_wait(full0 + 8u * b0, ph0);
+          if (++b0 == NT) b0 = 0, ph0 ^= 1u;
+        }
+      }
+      if (have) {
+        if constexpr (kTranspose) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if ((uint32_t)u < nu) {
+              const uint2 n = lds_u2(tb[u]);
+              thr[u] = n.x;
+              meta[u] = n.y;
+            }
           }
-          const uint32_t c = nd.y & ~kLeafBit;
-          if (c < 4) h0[q] += 1u << (8 * c);
-          else h1[q] += 1u << (8 * (c - 4));
+          // U predicated chains per lane until every chain sits on a leaf
+          while (true) {
+            bool any = false;
+#pragma unroll
+            for (int u = 0; u < U; ++u) any |= (int)meta[u] >= 0;
+            if (!any) break;
+#pragma unroll
+            for (int u = 0; u < U; ++u) forest_step(thr[u], meta[u], tb[u], soa, amask, args.abits);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if ((uint32_t)u < nu) {
+              const uint32_t c = meta[u] & ~kLeafBit;
+              if (c < 4) h0[0] += 1u << (8 * c);
+              else h1[0] += 1u << (8 * (c - 4));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if ((uint32_t)u >= nu) continue;
+#pragma unroll
+            for (int q = 0; q < S; ++q) {
+              uint2 nd = lds_u2(tb[u]);
+              while (!(nd.y & kLeafBit)) {
+                const float v = rec[q].get(nd.y & amask);
+                nd = lds_u2(tb[u] + (nd.y >> args.abits) + (v > __uint_as_float(nd.x) ? 8u : 0u));
+              }
+              const uint32_t c = nd.y & ~kLeafBit;
+              if (c < 4) h0[q] += 1u << (8 * c);
+              else h1[q] += 1u << (8 * (c - 4));
+            }
+          }
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty0 + 8u * b);  // this warp is done with slot b
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if ((uint32_t)u < nu) mbar_arrive(empty0 + 8u * slot[u]);  // this warp is done with the slot
+      }
     }
     if (have) {
 #pragma unroll

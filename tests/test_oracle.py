@@ -11,6 +11,7 @@
    conditional-descent oracle (eval_serial.cpp:43-75).
 """
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -126,3 +127,27 @@ def test_forest_vote_oracle(co):
     counts = np.stack([(votes == c).sum(0) for c in range(4)])
     want = counts.argmax(0)  # first max = smallest class id on ties
     assert np.array_equal(co.eval_forest(trees, x, 4), want)
+
+
+def test_warp_sim_xcheck_profile(co):
+    """profiles/r1_warp_sim_xcheck.json (ncu per-SASS-line counts of the data
+    and EXACT speculative kernels vs the reference's lockstep warp model,
+    tools/warp_sim_xcheck.py): every check is an exact equality, and the
+    data-kernel predictions restate from the oracle's traversal depths
+    (serialized passes = sum over 32-record warps of the deepest lane)."""
+    import json
+
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                     "r1_warp_sim_xcheck.json")
+    rep = json.load(open(p))
+    assert rep["all_equal"]
+    sys.path.insert(0, os.path.join(os.path.dirname(p), "..", "tools"))
+    import warp_sim_xcheck as xc
+
+    for e in rep["launches"]:
+        if e["algo"] != "data":
+            continue
+        nodes, x = xc.inputs(e["workload"], co.gen_tree, co.gen_dataset)
+        d = co.traversal_depths(nodes, x).astype(np.int64).reshape(-1, 32)
+        assert int(d.max(axis=1).sum()) == e["warp_sim"]["serialized_passes"] == e["ncu"]["warp_instructions"]
+        assert int(d.sum()) == e["warp_sim"]["node_evals"] == e["ncu"]["active_thread_instructions"]

@@ -20,11 +20,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="C2")
 ap.add_argument("--grid", default="data")
 ap.add_argument("--iters", type=int, default=30)
+ap.add_argument("--tile", type=int, default=1, help="repeat the records N times (L2-sized configs)")
 args = ap.parse_args()
 W = bench.WORKLOADS[args.workload]
 m, a = W["m"], W["a"]
 tree = st.generate_synthetic_tree(*W["tree"])
 x = st.generate_synthetic_dataset(m, a, W["seed"])
+if args.tile > 1:
+    import numpy as np
+    x = np.tile(x, (args.tile, 1))
+    m = len(x)
 xd = torch.from_numpy(x).cuda(); out = torch.empty(m, dtype=torch.int32, device="cuda")
 peak, _ = bench.peaks()
 geoms = []
@@ -35,8 +40,11 @@ if "data" in args.grid:
 if "spec" in args.grid:
     for G, pl in itertools.product([2, 4, 8, 16], [1, 2]):
         geoms.append(st.GpuGeom(algo="speculative", group_lanes=G, pipeline=pl))
+if "stages" in args.grid:
+    for S, ns, w in itertools.product([0, 1, 2, 4], [2, 3, 4], [0, 16, 24]):
+        geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, stages=ns, warps_per_cta=w))
 if "warps" in args.grid:
-    for tl, S, w in itertools.product(["shared", "global"], [0, 1, 2], [0, 8, 16, 32]):
+    for tl, S, w in itertools.product(["shared"], [0, 1, 2, 4], [0, 8, 16, 32]):
         geoms.append(st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=S, warps_per_cta=w))
 res = []
 want = None
@@ -44,7 +52,7 @@ for g in geoms:
     try:
         st.eval_device(tree, xd, out, g); torch.cuda.synchronize()
         got = st.fnv1a64(out.cpu().numpy())
-        ok = got == W["labels_fnv"]
+        ok = got == W["labels_fnv"] if args.tile == 1 else None
         ms = timeit(lambda: st.eval_device(tree, xd, out, g), args.iters)
     except Exception as e:
         print("ERR", g, e, flush=True)
@@ -55,4 +63,4 @@ for g in geoms:
 res.sort(key=lambda r: r["ms"])
 print("BEST", json.dumps(res[:5], indent=0))
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-json.dump(res, open(os.path.join(ROOT, "gpurun_out", f"sweep_{args.workload}_{args.grid}.json"), "w"), indent=0)
+json.dump(res, open(os.path.join(ROOT, "gpurun_out", f"sweep_{args.workload}x{args.tile}_{args.grid}.json"), "w"), indent=0)
