@@ -757,6 +757,8 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   }
 }
 
+uint32_t env_u32(const char* name, uint32_t dflt);
+
 // ---- speculative kernel dispatch -----------------------------------------
 template <int A, int LOADER, bool WS, bool EXACT, int STEPS>
 void launch_spec_k(const SpecArgs& sa, const Staging& stg, size_t smem, int dev, uint32_t bps,
@@ -957,7 +959,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // CTA-shared ring (default for the fast path): up to 32 warps on one SM
   // share NS = warps + 12 tile slots; ~12 tiles in flight cover DRAM latency.
   if (stg.loader == kTma && !stats && g.pipeline != 1) {
-    const size_t lb = 16 + 32 * 128;  // ticket + per-warp label rows (up to 32 warps)
+    const size_t lb = 32 + 32 * 128;  // generation padding + ticket + per-warp label rows (<= 32 warps)
     const size_t budget = pr.smem_optin - 1024 - sa.win_bytes - lb;
     const size_t max_slots = budget / (stg.stage_bytes + 16u);
     const uint32_t warps = (uint32_t)std::min<size_t>(32, max_slots > 12 ? max_slots - 12 : 0);
@@ -965,8 +967,10 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       SpecRingArgs ra{};
       ra.s = sa;
       ra.n_slots = (uint32_t)std::min<size_t>(max_slots, warps + 12);
-      const size_t rsmem = 1024 + sa.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 8u) + 16 +
-                           (size_t)warps * 128;
+      // development / stress knob: any ring depth >= 1 must give exact labels
+      if (const uint32_t ns = env_u32("ST_SPEC_RING_SLOTS", 0)) ra.n_slots = std::min<uint32_t>(ra.n_slots, ns);
+      const size_t rsmem = 1024 + sa.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 8u) +
+                           (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128;
       switch (ct_arity(a) ? a : 0) {
         case 8: return launch_spec_ring<8>(win_shared, ra, stg, rsmem, dev, warps, s);
         case 16: return launch_spec_ring<16>(win_shared, ra, stg, rsmem, dev, warps, s);

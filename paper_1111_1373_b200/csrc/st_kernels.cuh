@@ -708,10 +708,11 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t NS = ra.n_slots;
   const uint32_t sbase = align1024(smem_u32(smem));
 
-  // [windows] [NS slots] [full bars] [ticket] [per-warp label rows]
+  // [windows] [NS slots] [full bars] [slot generations] [ticket] [per-warp label rows]
   const uint32_t slots0 = sbase + args.win_bytes;
   const uint32_t full0 = slots0 + NS * args.stage_bytes;
-  const uint32_t ticket = full0 + 8u * NS;
+  const uint32_t gen0 = full0 + 8u * NS;
+  const uint32_t ticket = gen0 + ((4u * NS + 15u) & ~15u);
   const uint32_t lbuf = ticket + 16u + (uint32_t)warp * 128u;
 
   const uint64_t m = args.p.m;
@@ -743,7 +744,10 @@ __global__ void __launch_bounds__(kMaxThreads)
   };
 
   if (threadIdx.x == 0) {
-    for (uint32_t b = 0; b < NS; ++b) mbar_init(full0 + 8u * b, 1);
+    for (uint32_t b = 0; b < NS; ++b) {
+      mbar_init(full0 + 8u * b, 1);
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(0u) : "memory");
+    }
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(ticket), "r"(0u) : "memory");
     fence_barrier_init();
   }
@@ -780,6 +784,19 @@ __global__ void __launch_bounds__(kMaxThreads)
     const uint32_t b = tk % NS;
     const uint32_t tile = slots0 + b * args.stage_bytes;
     const uint32_t rows = (uint32_t)((m - r0) < (uint64_t)R ? (m - r0) : (uint64_t)R);
+    // A parity wait cannot tell generation g of a slot from g + 2: a slow
+    // warp may still hold ticket tk - NS (slot b not yet refilled for tk)
+    // while faster warps have taken every ticket up to tk.  So first wait
+    // until the refill for generation tk / NS has been issued (the warp that
+    // finished tk - NS publishes it), then the parity wait is unambiguous.
+    if (lane == 0) {
+      const uint32_t g = tk / NS;
+      uint32_t have;
+      do {
+        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(have) : "r"(gen0 + 4u * b) : "memory");
+      } while (have < g);
+    }
+    __syncwarp();
     mbar_wait(full0 + 8u * b, (tk / NS) & 1u);
     if (args.root_code & kLeafBit) {  // N == 1
       if (lane < rows)
@@ -822,7 +839,11 @@ __global__ void __launch_bounds__(kMaxThreads)
       } while (__any_sync(0xffffffffu, active));
     }
     __syncwarp();
-    if (tk + NS < my_tiles) fill(tk + NS);  // this warp freed slot b: refill it
+    if (tk + NS < my_tiles) {
+      fill(tk + NS);  // this warp freed slot b: refill it ...
+      if (lane == 0)  // ... and publish that generation tk / NS + 1 is on its way
+        asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(tk / NS + 1u) : "memory");
+    }
     if (lane < rows) {
       uint32_t code;
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(code) : "r"(lbuf + 4u * lane));
@@ -1030,7 +1051,11 @@ __global__ void __launch_bounds__(kMaxThreads)
     if (lane == 0) {
       uint32_t b = 0, ph = 0, tr = 0;
       for (uint64_t gi = 0; gi < total; ++gi) {
-        if (gi >= NT) mbar_wait(empty0 + 8u * b, ph ^ 1u);
+        if (gi >= NT) {
+          mbar_wait(empty0 + 8u * b, ph ^ 1u);
+          // consumers' generic-proxy reads of the slot precede this async write
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
         const uint32_t bytes = __ldg(args.tree_bytes + tr);
         mbar_arrive_expect_tx(full0 + 8u * b, bytes);
         bulk_load(tbuf0 + b * args.tree_buf_bytes, args.nodes + __ldg(args.offsets + tr), bytes,

@@ -108,3 +108,23 @@ def test_cli_verify_bench_classify(cuda, co, cli, tmp_path):
     r = subprocess.run([cli, "verify", "--tree", t, "--data", d, "--strategy", "gpu-bogus"],
                        capture_output=True, text=True)
     assert r.returncode == 2
+
+
+@pytest.mark.parametrize("slots", [1, 3, 7])
+def test_spec_ring_shallow_ring_stress(cuda, co, slots, monkeypatch):
+    """k_spec_ring with a ring shallower than the warp count: tickets run up to
+    several generations ahead of a slow warp on a deep record (skewed depth-24
+    tree), which a parity-only slot wait would mistake for a completed refill.
+    Labels must stay exact for any ring depth."""
+    import torch
+
+    nodes = co.gen_tree(24, 256, 32, 8, 201)
+    x = co.gen_dataset(400_000, 32, 202)
+    want = co.eval_serial(nodes, x)
+    xd = torch.from_numpy(x).cuda()
+    monkeypatch.setenv("ST_SPEC_RING_SLOTS", str(slots))
+    for _ in range(3):
+        out = torch.empty(len(x), dtype=torch.int32, device="cuda")
+        st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative", pipeline=2))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want)

@@ -68,18 +68,22 @@ def main():
     owner = {s: g for g, (lo, hi) in enumerate(own) for s in range(lo, hi)}
     with cf.ThreadPoolExecutor(max_workers=min(len(ring), os.cpu_count() or 1)) as pool:
         pending = {}
+        free = list(ring)  # staging buffers not owned by an in-flight shard
         nxt = 0
         while nxt < S or pending:
-            while nxt < S and len(pending) < len(ring):
-                buf = ring[nxt % len(ring)]
+            while nxt < S and free:
+                buf = free.pop()
                 pending[pool.submit(gen, nxt, buf)] = (nxt, buf)
                 nxt += 1
             done, _ = cf.wait(list(pending), return_when=cf.FIRST_COMPLETED)
             for f in done:
                 s, buf = pending.pop(f)
+                f.result()
                 g = owner[s]
                 lo = own[g][0]
-                xs[g][(s - lo) * SHARD:(s - lo + 1) * SHARD].copy_(buf)  # synchronous: buf is reusable after
+                with torch.cuda.device(g):
+                    xs[g][(s - lo) * SHARD:(s - lo + 1) * SHARD].copy_(buf)  # synchronous
+                free.append(buf)
     t_gen = time.perf_counter() - t_gen
     print(f"generated {S} shards ({S * SHARD * A * 4 / 1e9:.1f} GB) in {t_gen:.1f} s", flush=True)
     labels_host = torch.empty(S * SHARD, dtype=torch.int32, pin_memory=True)

@@ -1,0 +1,58 @@
+"""One small launch of every kernel family (data: shared/global/constant tree,
+S = 1/2/4; speculative: ring, per-warp, EXACT shfl, EXACT CTA; forest), labels
+checked against the C oracle -- the target for compute-sanitizer
+(memcheck / racecheck / synccheck):
+
+    compute-sanitizer --tool racecheck python tools/sanitize_run.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402  (checker only)
+import paper_1111_1373_b200 as st  # noqa: E402
+
+co = oracle.COracle()
+m = int(sys.argv[1]) if len(sys.argv) > 1 else 20_000
+bad = 0
+cases = [((24, 256, 32, 8, 201), 32), ((12, 2048, 8, 8, 301), 8), ((10, 1024, 16, 8, 101), 16),
+         ((11, 16, 19, 7, 1), 19), ((12, 1024, 64, 8, 401), 64)]
+for targs, a in cases:
+    nodes = co.gen_tree(*targs)
+    x = co.gen_dataset(m + 7, a, 5)  # ragged tail tile
+    want = co.eval_serial(nodes, x)
+    xd = torch.from_numpy(x).cuda()
+    geoms = [st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=s)
+             for tl in ("shared", "global", "constant") for s in (1, 2, 4)]
+    geoms += [st.GpuGeom(algo="speculative", pipeline=p, group_lanes=g) for p in (1, 2) for g in (0, 2, 8)]
+    for g in geoms:
+        out = torch.empty(len(x), dtype=torch.int32, device="cuda")
+        st.eval_device(nodes, xd, out, g)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().view(np.uint32)
+        if not np.array_equal(got, want):
+            bad += 1
+            print("MISMATCH", targs, g)
+    it = torch.empty(len(x), dtype=torch.int32, device="cuda")
+    sp = torch.empty(len(x), dtype=torch.int32, device="cuda")
+    out = torch.empty(len(x), dtype=torch.int32, device="cuda")
+    st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative", reductions=2), stats=(it, sp))
+    torch.cuda.synchronize()
+    if not np.array_equal(out.cpu().numpy().view(np.uint32), want):
+        bad += 1
+        print("MISMATCH exact", targs)
+trees = [co.gen_tree(10, 512, 64, 8, 401 + t) for t in range(6)]
+x = co.gen_dataset(m + 5, 64, 9)
+f = st.Forest(trees, 8)
+out = torch.empty(len(x), dtype=torch.int32, device="cuda")
+st.eval_forest_device(f, torch.from_numpy(x).cuda(), out)
+torch.cuda.synchronize()
+if not np.array_equal(out.cpu().numpy().view(np.uint32), co.eval_forest(trees, x, 8)):
+    bad += 1
+    print("MISMATCH forest")
+print("sanitize_run:", "ok" if bad == 0 else f"{bad} mismatches")
+sys.exit(1 if bad else 0)
