@@ -84,7 +84,9 @@ typedef struct st_geom {
   uint32_t warps_per_cta;      /* CTA width in warps, 1-32 (0 = auto) */
   uint32_t pipeline;           /* record staging: 0 = auto, 1 = per-warp TMA ring,
                                   2 = CTA-shared TMA ring with a producer warp (speculative) */
-  uint32_t reserved[2];
+  uint32_t record_regs;         /* data kernel, 8-attribute records: 0 = auto, 1 = walk from
+                                  registers (tile released right after loading), 2 = shared tile */
+  uint32_t reserved[1];
 } st_geom;
 
 /* Optional per-record speculative counters (SpeculativeStats,

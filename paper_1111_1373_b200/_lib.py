@@ -42,7 +42,8 @@ class st_geom(C.Structure):
         ("stages", C.c_uint32),
         ("warps_per_cta", C.c_uint32),
         ("pipeline", C.c_uint32),
-        ("reserved", C.c_uint32 * 2),
+        ("record_regs", C.c_uint32),
+        ("reserved", C.c_uint32 * 1),
     ]
 
 

@@ -105,6 +105,7 @@ int current_device() {
 struct DevProps {
   int sms = 0;
   size_t smem_optin = 0;
+  size_t smem_per_sm = 0;
 };
 DevProps dev_props(int dev) {
   static std::mutex mu;
@@ -118,6 +119,8 @@ DevProps dev_props(int dev) {
   p.sms = v;
   CK(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   p.smem_optin = (size_t)v;
+  CK(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  p.smem_per_sm = (size_t)v;
   cache[dev] = p;
   return p;
 }
@@ -655,6 +658,9 @@ void launch_data_tloc(int tloc, const DataArgs& d, const Staging& stg, const st_
                       size_t smem, int dev, uint32_t bps, cudaStream_t s) {
   switch (tloc) {
     case ST_TREE_SHARED:
+      if constexpr (A == 8 && LOADER == kTma) {
+        if (d.record_regs) return launch_data_t<A, S, kSharedReg, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
+      }
       return launch_data_t<A, S, kShared, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
     case ST_TREE_GLOBAL:
       return launch_data_t<A, S, kGlobal, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
@@ -716,6 +722,7 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.abits = t->abits;
   d.leaf_class = dv.leaf_tbl;
   d.labels = labels;
+  d.record_regs = g.record_regs != 2 ? 1u : 0u;  // 8-attribute records walk from registers
 
   const uint32_t tree_bytes = round1024(t->nodes.size() * sizeof(CNode));
   int tloc = g.tree_loc;
@@ -733,11 +740,22 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // A large shared-memory tree is staged once per CTA: widen the CTA so that
   // one copy serves up to 32 warps instead of capping the SM at one 8-warp CTA.
   stg.warps = pick_warps(g.warps_per_cta, stg, tloc == ST_TREE_SHARED ? tree_bytes : 0, pr);
+  uint32_t want_bps = g.blocks_per_sm;
+  // Small inputs (< 8 tiles per warp at 32 warps/SM, e.g. C1's 1M records)
+  // are ramp-up bound: four 8-warp CTAs per SM stage their tree copies
+  // faster than one 32-warp CTA (C1: 17.0 vs 19.3 us, profiles/r1_sweep_C1x1_small_flush.json).
+  const uint64_t tiles_total = m / (32ull * stg.S);
+  if (!g.warps_per_cta && !g.blocks_per_sm && stg.loader == kTma && tloc == ST_TREE_SHARED &&
+      tiles_total < (uint64_t)pr.sms * 32 * 8 &&
+      4 * (1024 + tree_bytes + (size_t)kWarpsPerCta * stg.ns * (stg.stage_bytes + 8u)) <= pr.smem_per_sm) {
+    stg.warps = kWarpsPerCta;
+    want_bps = 4;
+  }
   d.ns = stg.ns;
   d.stage_bytes = stg.stage_bytes;
   d.tree_bytes = tloc == ST_TREE_SHARED ? tree_bytes : 0;
   const size_t smem = 1024 + d.tree_bytes + stg.tile_smem();
-  const uint32_t bps = default_bps(g.blocks_per_sm, stg, m, pr);
+  const uint32_t bps = default_bps(want_bps, stg, m, pr);
   if (stg.loader == kTma && ct_arity(a)) {
     switch (a) {
       case 8: return launch_data_a<8>(stg, tloc, d, t, smem, dev, bps, s);

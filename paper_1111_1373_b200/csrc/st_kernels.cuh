@@ -57,7 +57,9 @@ struct __align__(16) SEntry {
 };
 
 enum Loader { kTma = 0, kScalar = 1, kSoa = 2, kDirect = 3 };
-enum TreeLoc { kShared = 1, kConst = 2, kGlobal = 3, kWide = 4 };
+// kSharedReg: shared-memory tree, records walked from registers (8-attribute
+// records; the TMA tile is released as soon as it is in registers)
+enum TreeLoc { kShared = 1, kConst = 2, kGlobal = 3, kWide = 4, kSharedReg = 5 };
 
 // ---------------------------------------------------------------------------
 // PTX helpers (32-bit shared addresses)
@@ -300,7 +302,7 @@ struct TreeRef {
       return make_uint2(__float_as_uint(n.thr), n.meta);
     } else if constexpr (TLOC == kGlobal) {
       return __ldg(reinterpret_cast<const uint2*>(g + off));
-    } else {
+    } else {  // kShared, kSharedReg
       return lds_u2(s + off);
     }
   }
@@ -317,6 +319,7 @@ struct DataArgs {
   uint32_t ns;                 // pipeline stages
   uint32_t tree_bytes;         // shared bytes reserved for the node array (kShared)
   uint32_t stage_bytes;        // stride between stages
+  uint32_t record_regs;        // host hint: 8-attribute records walk from registers (kSharedReg)
 };
 
 // Shared-memory carve-out shared by the kernels:
@@ -353,6 +356,36 @@ __device__ __forceinline__ void data_step(uint32_t& thr, uint32_t& meta, uint32_
       : "memory");
 }
 
+// Level step with the feature already selected from registers: if the node
+// is internal, node = tb + child + 8*(v > thr).
+__device__ __forceinline__ void data_step_v(uint32_t& thr, uint32_t& meta, float v, uint32_t tb,
+                                            uint32_t abits) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q;\n\t"
+      ".reg .u32 ch;\n\t"
+      "setp.ge.s32 p, %1, 0;\n\t"
+      "setp.gt.and.f32 q, %2, %0, p;\n\t"
+      "shr.u32 ch, %1, %4;\n\t"
+      "add.u32 ch, ch, %3;\n\t"
+      "@q add.u32 ch, ch, 8;\n\t"
+      "@p ld.shared.v2.u32 {%0, %1}, [ch];\n\t"
+      "}"
+      : "+f"(*reinterpret_cast<float*>(&thr)), "+r"(meta)
+      : "f"(v), "r"(tb), "r"(abits)
+      : "memory");
+}
+
+// x[attr] from 8 registers: a 3-level select tree on the attribute bits of
+// the compact meta (4*attr in the low bits).  Selects move bits: exact.
+__device__ __forceinline__ float pick8(const float (&f)[8], uint32_t meta) {
+  const bool b0 = meta & 4u, b1 = meta & 8u, b2 = meta & 16u;
+  const float a01 = b0 ? f[1] : f[0], a23 = b0 ? f[3] : f[2];
+  const float a45 = b0 ? f[5] : f[4], a67 = b0 ? f[7] : f[6];
+  const float a03 = b1 ? a23 : a01, a47 = b1 ? a67 : a45;
+  return b2 ? a47 : a03;
+}
+
 template <int A, int S, int TLOC, int LOADER, int CAP>
 __global__ void __launch_bounds__(kMaxThreads)
     k_data(const DataArgs args, const __grid_constant__ CUtensorMap tmap,
@@ -385,7 +418,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t amask = (1u << args.abits) - 1u;
 
   // ---- stage the node array once per CTA --------------------------------
-  if constexpr (TLOC == kShared) {
+  if constexpr (TLOC == kShared || TLOC == kSharedReg) {
     const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
     const uint32_t n16 = (args.n_nodes * 8u + 15u) / 16u;
     for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
@@ -416,6 +449,43 @@ __global__ void __launch_bounds__(kMaxThreads)
         }
         args.labels[r0 + r] = nd.w;
       }
+    } else if constexpr (TLOC == kSharedReg && LOADER == kTma && A == 8) {
+      // records -> registers (two conflict-free lds.128 each), tile freed at once
+      float f[S][8];
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint32_t b = (uint32_t)(q * 32 + lane) * 32u;
+        const uint4 lo = lds_u4(tile + swz(b)), hi = lds_u4(tile + swz(b + 16u));
+        f[q][0] = __uint_as_float(lo.x); f[q][1] = __uint_as_float(lo.y);
+        f[q][2] = __uint_as_float(lo.z); f[q][3] = __uint_as_float(lo.w);
+        f[q][4] = __uint_as_float(hi.x); f[q][5] = __uint_as_float(hi.y);
+        f[q][6] = __uint_as_float(hi.z); f[q][7] = __uint_as_float(hi.w);
+      }
+      pipe.release(i, t, step, n_tiles);  // next tile's TMA overlaps this walk
+      uint32_t thr[S], meta[S];
+      const uint2 root = tree.get(0);
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        thr[q] = root.x;
+        meta[q] = (r0 + q * 32 + lane < m) ? root.y : kLeafBit;
+      }
+      while (true) {
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < S; ++q) any |= (int)meta[q] >= 0;
+        if (!any) break;
+#pragma unroll
+        for (int q = 0; q < S; ++q) data_step_v(thr[q], meta[q], pick8(f[q], meta[q]), tree.s, args.abits);
+      }
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint64_t r = r0 + q * 32 + lane;
+        if (r < m) {
+          const uint32_t c = meta[q] & ~kLeafBit;
+          args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+        }
+      }
+      continue;  // stage already released
     } else if constexpr (TLOC == kShared && LOADER == kTma && Rec<A, LOADER>::kRowLocal) {
       // S independent predicated chains per lane (no per-level branches)
       uint32_t thr[S], meta[S], bx[S];

@@ -56,6 +56,7 @@ class GpuGeom:
     stages: int = 0                 # TMA record-pipeline stages per warp
     warps_per_cta: int = 0          # CTA width (warps)
     pipeline: int = 0               # 0 auto, 1 per-warp TMA ring, 2 CTA-shared ring (spec)
+    record_regs: int = 0            # data, 8-attribute records: 0 auto, 1 registers, 2 shared tile
 
     def to_c(self) -> st_geom:
         g = st_geom()
@@ -73,6 +74,7 @@ class GpuGeom:
         g.stages = self.stages
         g.warps_per_cta = self.warps_per_cta
         g.pipeline = self.pipeline
+        g.record_regs = self.record_regs
         return g
 
 

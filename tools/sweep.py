@@ -6,6 +6,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1111_1373_b200 as st
 import bench
+sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 def timeit(fn, iters=30, warm=5):
     for _ in range(warm): fn()
@@ -21,6 +22,8 @@ ap.add_argument("--workload", default="C2")
 ap.add_argument("--grid", default="data")
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--tile", type=int, default=1, help="repeat the records N times (L2-sized configs)")
+ap.add_argument("--flush", action="store_true",
+                help="L2 read-flush before every launch, graph-replay timing (tools/workloads.py)")
 args = ap.parse_args()
 W = bench.WORKLOADS[args.workload]
 m, a = W["m"], W["a"]
@@ -40,6 +43,13 @@ if "data" in args.grid:
 if "spec" in args.grid:
     for G, pl in itertools.product([2, 4, 8, 16], [1, 2]):
         geoms.append(st.GpuGeom(algo="speculative", group_lanes=G, pipeline=pl))
+if "regs" in args.grid:
+    for S, rr, w in itertools.product([0, 1, 2, 4], [1, 2], [0, 16]):
+        geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, record_regs=rr, warps_per_cta=w))
+if "small" in args.grid:
+    for S, ns, w, bps in itertools.product([0, 1, 2, 4], [0, 3], [0, 8, 16], [0, 1, 2, 4]):
+        geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, stages=ns, warps_per_cta=w,
+                                blocks_per_sm=bps))
 if "stages" in args.grid:
     for S, ns, w in itertools.product([0, 1, 2, 4], [2, 3, 4], [0, 16, 24]):
         geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, stages=ns, warps_per_cta=w))
@@ -53,7 +63,13 @@ for g in geoms:
         st.eval_device(tree, xd, out, g); torch.cuda.synchronize()
         got = st.fnv1a64(out.cpu().numpy())
         ok = got == W["labels_fnv"] if args.tile == 1 else None
-        ms = timeit(lambda: st.eval_device(tree, xd, out, g), args.iters)
+        if args.flush:
+            import workloads
+            fl = getattr(workloads, "_sweep_flush", None) or workloads.make_flush()
+            workloads._sweep_flush = fl
+            ms = workloads.graph_time(lambda: st.eval_device(tree, xd, out, g), args.iters, fl)
+        else:
+            ms = timeit(lambda: st.eval_device(tree, xd, out, g), args.iters)
     except Exception as e:
         print("ERR", g, e, flush=True)
         import paper_1111_1373_b200._lib as L
@@ -63,4 +79,4 @@ for g in geoms:
 res.sort(key=lambda r: r["ms"])
 print("BEST", json.dumps(res[:5], indent=0))
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-json.dump(res, open(os.path.join(ROOT, "gpurun_out", f"sweep_{args.workload}x{args.tile}_{args.grid}.json"), "w"), indent=0)
+json.dump(res, open(os.path.join(ROOT, "gpurun_out", f"sweep_{args.workload}x{args.tile}_{args.grid}{'_flush' if args.flush else ''}.json"), "w"), indent=0)
