@@ -805,10 +805,10 @@ void launch_spec_steps(const SpecArgs& sa, const Staging& stg, size_t smem, int 
   }
 }
 
-template <int A, bool WS, int STEPS>
+template <int A, bool WS, int STEPS, int SR>
 void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
                         uint32_t warps, cudaStream_t s) {
-  auto fn = k_spec_ring<A, WS, STEPS>;
+  auto fn = k_spec_ring<A, WS, STEPS, SR>;
   const uint64_t n_tiles = (ra.s.p.m + 31) / 32;
   const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles * warps, warps);
   clear_stale_error();
@@ -816,10 +816,17 @@ void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem,
   check_launch();
 }
 
+template <int A, bool WS, int STEPS>
+void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
+                         uint32_t warps, cudaStream_t s) {
+  if (sr >= 2) return launch_spec_ring_k<A, WS, STEPS, 2>(ra, stg, smem, dev, warps, s);
+  return launch_spec_ring_k<A, WS, STEPS, 1>(ra, stg, smem, dev, warps, s);
+}
+
 template <int A>
-void launch_spec_ring(bool ws, const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
-                      uint32_t warps, cudaStream_t s) {
-#define ST_RING(WSV, ST) return launch_spec_ring_k<A, WSV, ST>(ra, stg, smem, dev, warps, s)
+void launch_spec_ring(bool ws, uint32_t sr, const SpecRingArgs& ra, const Staging& stg, size_t smem,
+                      int dev, uint32_t warps, cudaStream_t s) {
+#define ST_RING(WSV, ST) return launch_spec_ring_sr<A, WSV, ST>(sr, ra, stg, smem, dev, warps, s)
   if (ws) {
     switch (ra.s.smax) {
       case 0: ST_RING(true, 0);
@@ -989,12 +996,16 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       if (const uint32_t ns = env_u32("ST_SPEC_RING_SLOTS", 0)) ra.n_slots = std::min<uint32_t>(ra.n_slots, ns);
       const size_t rsmem = 1024 + sa.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 8u) +
                            (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128;
+      // record streams per group (samples_per_thread): one by default -- two
+      // independent window chains per lane measured slower (C2 G = 4: 0.55 vs
+      // 0.42 ms; profiles/r1_sweep_*_spec2.json)
+      const uint32_t sr = g.samples_per_thread ? g.samples_per_thread : 1;
       switch (ct_arity(a) ? a : 0) {
-        case 8: return launch_spec_ring<8>(win_shared, ra, stg, rsmem, dev, warps, s);
-        case 16: return launch_spec_ring<16>(win_shared, ra, stg, rsmem, dev, warps, s);
-        case 32: return launch_spec_ring<32>(win_shared, ra, stg, rsmem, dev, warps, s);
-        case 64: return launch_spec_ring<64>(win_shared, ra, stg, rsmem, dev, warps, s);
-        default: return launch_spec_ring<0>(win_shared, ra, stg, rsmem, dev, warps, s);
+        case 8: return launch_spec_ring<8>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+        case 16: return launch_spec_ring<16>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+        case 32: return launch_spec_ring<32>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+        case 64: return launch_spec_ring<64>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+        default: return launch_spec_ring<0>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
       }
     }
   }

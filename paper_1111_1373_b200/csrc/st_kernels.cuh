@@ -768,7 +768,7 @@ struct SpecRingArgs {
   uint32_t n_slots;       // NS
 };
 
-template <int A, bool WIN_SHARED, int STEPS>
+template <int A, bool WIN_SHARED, int STEPS, int SR>
 __global__ void __launch_bounds__(kMaxThreads)
     k_spec_ring(const SpecRingArgs ra, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -859,11 +859,15 @@ __global__ void __launch_bounds__(kMaxThreads)
     // while faster warps have taken every ticket up to tk.  So first wait
     // until the refill for generation tk / NS has been issued (the warp that
     // finished tk - NS publishes it), then the parity wait is unambiguous.
+    // The generation word only gates *which* phase to wait for; the tile's
+    // bytes are published by the mbarrier (complete_tx, acquire on the wait),
+    // so plain volatile shared accesses suffice (no fence on the hot path:
+    // an acquire/release pair here cost 18% on C2).
     if (lane == 0) {
       const uint32_t g = tk / NS;
       uint32_t have;
       do {
-        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(have) : "r"(gen0 + 4u * b) : "memory");
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(have) : "r"(gen0 + 4u * b) : "memory");
       } while (have < g);
     }
     __syncwarp();
@@ -872,47 +876,96 @@ __global__ void __launch_bounds__(kMaxThreads)
       if (lane < rows)
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * lane), "r"(args.root_code) : "memory");
     } else {
-      uint32_t r = g;
-      bool active = r < rows;
-      uint32_t woff = 0;
-      Rec<A, kTma> rec;
-      rec.init(tile, active ? r : 0u, args.p.a, args.p.x, 0, 0, 0);
-      do {
-        uint4 e;
-        if constexpr (WIN_SHARED) e = lds_u4(jaddr + woff);
-        else e = __ldg(reinterpret_cast<const uint4*>(wglob + woff));
-        const float v = rec.get(e.y & 0x00FFFFFFu);
-        uint32_t c = (v > __uint_as_float(e.x)) ? e.w : e.z;
+      // SR independent record streams per group: stream s classifies rows
+      // g + s*NG, g + (s + SR)*NG, ...  Two streams double the independent
+      // load chains per lane (the window step is a dependent chain of
+      // shared-memory loads and shuffles).  A group whose stream has run out
+      // of rows issues no loads for it (predicated), but still takes part in
+      // the shuffles, which need every lane of the warp.
+      constexpr bool kRowLocal = Rec<A, kTma>::kRowLocal;
+      const uint32_t a4 = 4u * (A > 0 ? (uint32_t)A : args.p.a);
+      uint32_t r[SR], woff[SR], bx[SR];
+      bool active[SR];
+      Rec<A, kTma> rec[SR];
+#pragma unroll
+      for (int q = 0; q < SR; ++q) {
+        r[q] = g + q * NG;
+        active[q] = r[q] < rows;
+        woff[q] = 0;
+        const uint32_t rr = active[q] ? r[q] : 0u;
+        if constexpr (kRowLocal) {
+          const uint32_t ra4 = rr * a4, rowb = ra4 & ~127u;
+          bx[q] = (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
+        } else {
+          rec[q].init(tile, rr, args.p.a, args.p.x, 0, 0, 0);
+        }
+      }
+      bool any = true;
+      while (any) {
+        uint32_t c[SR];
+#pragma unroll
+        for (int q = 0; q < SR; ++q) {
+          c[q] = kLeafBit;  // an exhausted stream carries a non-lane code
+          if (active[q]) {
+            uint4 e;
+            if constexpr (WIN_SHARED) e = lds_u4(jaddr + woff[q]);
+            else e = __ldg(reinterpret_cast<const uint4*>(wglob + woff[q]));
+            float v;
+            if constexpr (kRowLocal) v = lds_f32((e.y & 0x00FFFFFFu) ^ bx[q]);
+            else v = rec[q].get(e.y & 0x00FFFFFFu);
+            c[q] = (v > __uint_as_float(e.x)) ? e.w : e.z;
+          }
+        }
         if constexpr (STEPS >= 0) {
 #pragma unroll
-          for (int s = 0; s < STEPS; ++s) {
-            const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
-            c = (c < 32u) ? u : c;
+          for (int st = 0; st < STEPS; ++st) {
+#pragma unroll
+            for (int q = 0; q < SR; ++q) {
+              const uint32_t u = __shfl_sync(0xffffffffu, c[q], c[q] & gmask, G);
+              c[q] = (c[q] < 32u) ? u : c[q];
+            }
           }
         } else {
-          for (uint32_t s = 0; s < args.smax; ++s) {
-            const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
-            c = (c < 32u) ? u : c;
+          for (uint32_t st = 0; st < args.smax; ++st) {
+#pragma unroll
+            for (int q = 0; q < SR; ++q) {
+              const uint32_t u = __shfl_sync(0xffffffffu, c[q], c[q] & gmask, G);
+              c[q] = (c[q] < 32u) ? u : c[q];
+            }
           }
         }
-        const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
-        if (root & kLeafBit) {
-          if (active && j == 0)
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(root) : "memory");
-          r += NG;
-          active = r < rows;
-          woff = 0;
-          if (active) rec.advance(r, NG, args.p.a, tile, args.p.x, 0, 0, 0);
-        } else {
-          woff = root & ~kExitBit;
+        any = false;
+#pragma unroll
+        for (int q = 0; q < SR; ++q) {
+          const uint32_t root = __shfl_sync(0xffffffffu, c[q], 0, G);
+          if (active[q]) {
+            if (root & kLeafBit) {
+              if (j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r[q]), "r"(root) : "memory");
+              r[q] += SR * NG;
+              active[q] = r[q] < rows;
+              woff[q] = 0;
+              if (active[q]) {
+                if constexpr (kRowLocal) {
+                  const uint32_t ra4 = r[q] * a4, rowb = ra4 & ~127u;
+                  bx[q] = (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
+                } else {
+                  rec[q].init(tile, r[q], args.p.a, args.p.x, 0, 0, 0);
+                }
+              }
+            } else {
+              woff[q] = root & ~kExitBit;
+            }
+          }
+          any |= active[q];
         }
-      } while (__any_sync(0xffffffffu, active));
+        any = __any_sync(0xffffffffu, any);
+      }
     }
     __syncwarp();
     if (tk + NS < my_tiles) {
       fill(tk + NS);  // this warp freed slot b: refill it ...
       if (lane == 0)  // ... and publish that generation tk / NS + 1 is on its way
-        asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(tk / NS + 1u) : "memory");
+        asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(tk / NS + 1u) : "memory");
     }
     if (lane < rows) {
       uint32_t code;

@@ -40,9 +40,12 @@ if "data" in args.grid:
     for tl, S, ns, bps, w in itertools.product(["shared", "global"], [1, 2, 4], [2, 3], [0, 2], [0, 8, 16, 32]):
         geoms.append(st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=S, stages=ns, blocks_per_sm=bps,
                                 warps_per_cta=w))
-if "spec" in args.grid:
+if "spec" in args.grid and "spec2" not in args.grid:
     for G, pl in itertools.product([2, 4, 8, 16], [1, 2]):
         geoms.append(st.GpuGeom(algo="speculative", group_lanes=G, pipeline=pl))
+if "spec2" in args.grid:
+    for G, sr in itertools.product([2, 4, 8], [1, 2]):
+        geoms.append(st.GpuGeom(algo="speculative", group_lanes=G, samples_per_thread=sr))
 if "regs" in args.grid:
     for S, rr, w in itertools.product([0, 1, 2, 4], [1, 2], [0, 16]):
         geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, record_regs=rr, warps_per_cta=w))
