@@ -172,10 +172,16 @@ def run_ours(args):
     import paper_1111_1373_b200 as st
 
     world, rank, local = dist_env()
+    # one process per GPU; ranks beyond the visible GPUs wrap around (only for
+    # validating the multi-rank path on a smaller box with --backend gloo)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
     W = WORKLOADS[args.workload]
     m, a = W["m"], W["a"]
     tree = st.generate_synthetic_tree(*W["tree"])
@@ -193,7 +199,7 @@ def run_ours(args):
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -446,6 +452,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for barrier / max-over-ranks (timing only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)  # timing rule: >= 3 untimed warm-up steps
     if args.impl == "reference":
