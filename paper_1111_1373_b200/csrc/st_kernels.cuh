@@ -766,6 +766,7 @@ __global__ void __launch_bounds__(kMaxThreads)
 struct SpecRingArgs {
   SpecArgs s;
   uint32_t n_slots;       // NS
+  uint32_t unsafe_no_gen; // benchmark-only: skip the slot-generation handshake
 };
 
 template <int A, bool WIN_SHARED, int STEPS, int SR>
@@ -783,7 +784,8 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t full0 = slots0 + NS * args.stage_bytes;
   const uint32_t gen0 = full0 + 8u * NS;
   const uint32_t ticket = gen0 + ((4u * NS + 15u) & ~15u);
-  const uint32_t lbuf = ticket + 16u + (uint32_t)warp * 128u;
+  uint32_t lbuf;  // opaque copy: keeps the per-warp label row in a register (no S2R remat in the walk)
+  asm("mov.u32 %0, %1;" : "=r"(lbuf) : "r"(ticket + 16u + (uint32_t)warp * 128u));
 
   const uint64_t m = args.p.m;
   const uint64_t n_tiles = (m + R - 1) / R;
@@ -861,20 +863,76 @@ __global__ void __launch_bounds__(kMaxThreads)
     // finished tk - NS publishes it), then the parity wait is unambiguous.
     // The generation word only gates *which* phase to wait for; the tile's
     // bytes are published by the mbarrier (complete_tx, acquire on the wait),
-    // so plain volatile shared accesses suffice (no fence on the hot path:
-    // an acquire/release pair here cost 18% on C2).
-    if (lane == 0) {
+    // so plain volatile shared accesses suffice.  (ra.unsafe_no_gen skips the
+    // handshake: racy, for measuring its cost only.)
+    // Every lane polls the same word (one broadcast wavefront, warp-uniform
+    // exit): no divergent lane-0 section before the walk's shuffles.
+    if (!ra.unsafe_no_gen) {
       const uint32_t g = tk / NS;
       uint32_t have;
       do {
         asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(have) : "r"(gen0 + 4u * b) : "memory");
-      } while (have < g);
+      } while (__any_sync(0xffffffffu, have < g));
     }
-    __syncwarp();
     mbar_wait(full0 + 8u * b, (tk / NS) & 1u);
     if (args.root_code & kLeafBit) {  // N == 1
       if (lane < rows)
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * lane), "r"(args.root_code) : "memory");
+    } else if constexpr (SR == 1) {
+      // One record stream per group: the lean loop.  A group whose rows are
+      // exhausted keeps re-walking its last record (finite, never stored):
+      // its extra loads cost less than predicating every step.
+      constexpr bool kRowLocal = Rec<A, kTma>::kRowLocal;
+      const uint32_t a4 = 4u * (A > 0 ? (uint32_t)A : args.p.a);
+      uint32_t r = g;
+      bool active = r < rows;
+      uint32_t woff = 0, bx = 0;
+      Rec<A, kTma> rec;
+      if constexpr (kRowLocal) {
+        const uint32_t ra4 = (active ? r : 0u) * a4, rowb = ra4 & ~127u;
+        bx = (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
+      } else {
+        rec.init(tile, active ? r : 0u, args.p.a, args.p.x, 0, 0, 0);
+      }
+      do {
+        uint4 e;
+        if constexpr (WIN_SHARED) e = lds_u4(jaddr + woff);
+        else e = __ldg(reinterpret_cast<const uint4*>(wglob + woff));
+        float v;
+        if constexpr (kRowLocal) v = lds_f32((e.y & 0x00FFFFFFu) ^ bx);
+        else v = rec.get(e.y & 0x00FFFFFFu);
+        uint32_t c = (v > __uint_as_float(e.x)) ? e.w : e.z;
+        if constexpr (STEPS >= 0) {
+#pragma unroll
+          for (int st = 0; st < STEPS; ++st) {
+            const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+            c = (c < 32u) ? u : c;
+          }
+        } else {
+          for (uint32_t st = 0; st < args.smax; ++st) {
+            const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+            c = (c < 32u) ? u : c;
+          }
+        }
+        const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
+        if (root & kLeafBit) {
+          if (active && j == 0)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(root) : "memory");
+          r += NG;
+          active = r < rows;
+          woff = 0;
+          if (active) {
+            if constexpr (kRowLocal) {
+              const uint32_t ra4 = r * a4, rowb = ra4 & ~127u;
+              bx = (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
+            } else {
+              rec.init(tile, r, args.p.a, args.p.x, 0, 0, 0);
+            }
+          }
+        } else {
+          woff = root & ~kExitBit;
+        }
+      } while (__any_sync(0xffffffffu, active));
     } else {
       // SR independent record streams per group: stream s classifies rows
       // g + s*NG, g + (s + SR)*NG, ...  Two streams double the independent
