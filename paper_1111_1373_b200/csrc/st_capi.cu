@@ -658,7 +658,7 @@ void launch_data_tloc(int tloc, const DataArgs& d, const Staging& stg, const st_
                       size_t smem, int dev, uint32_t bps, cudaStream_t s) {
   switch (tloc) {
     case ST_TREE_SHARED:
-      if constexpr (A == 8 && LOADER == kTma) {
+      if constexpr ((A == 8 || A == 16) && LOADER == kTma) {
         if (d.record_regs) return launch_data_t<A, S, kSharedReg, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
       }
       return launch_data_t<A, S, kShared, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
@@ -722,7 +722,8 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.abits = t->abits;
   d.leaf_class = dv.leaf_tbl;
   d.labels = labels;
-  d.record_regs = g.record_regs != 2 ? 1u : 0u;  // 8-attribute records walk from registers
+  // records walked from registers: default for 8-attribute records; 16 on request
+  d.record_regs = (g.record_regs == 1 || (g.record_regs == 0 && a == 8)) ? 1u : 0u;
 
   const uint32_t tree_bytes = round1024(t->nodes.size() * sizeof(CNode));
   int tloc = g.tree_loc;
@@ -730,7 +731,12 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   else if (tloc == ST_TREE_AUTO) tloc = tree_bytes <= 96 * 1024 ? ST_TREE_SHARED : ST_TREE_GLOBAL;
   if (tloc == ST_TREE_CONSTANT && t->compact.size() > 4000) tloc = ST_TREE_GLOBAL;
   const uint32_t S0 = ct_arity(a) ? choose_S(a, g.samples_per_thread) : 1;
-  Staging stg = plan_staging(x, m, a, ld, layout, S0, g.stages,
+  // Records walked from registers release their tile before the walk, so one
+  // stage per warp already double-buffers (next TMA in flight during the
+  // walk) and the saved shared memory buys twice the warps (C3 x 32 frames:
+  // 0.566 vs 0.615 ms, profiles/r1_sweep_C3x32_regs1.json).
+  const uint32_t want_ns = g.stages ? g.stages : (d.record_regs && tloc == ST_TREE_SHARED ? 1u : 0u);
+  Staging stg = plan_staging(x, m, a, ld, layout, S0, want_ns,
                              tloc == ST_TREE_SHARED ? tree_bytes : 0, pr);
   if (tloc == ST_TREE_SHARED && tree_bytes + 1024 + stg.tile_smem() > pr.smem_optin) {
     tloc = ST_TREE_GLOBAL;

@@ -376,14 +376,21 @@ __device__ __forceinline__ void data_step_v(uint32_t& thr, uint32_t& meta, float
       : "memory");
 }
 
-// x[attr] from 8 registers: a 3-level select tree on the attribute bits of
-// the compact meta (4*attr in the low bits).  Selects move bits: exact.
-__device__ __forceinline__ float pick8(const float (&f)[8], uint32_t meta) {
-  const bool b0 = meta & 4u, b1 = meta & 8u, b2 = meta & 16u;
-  const float a01 = b0 ? f[1] : f[0], a23 = b0 ? f[3] : f[2];
-  const float a45 = b0 ? f[5] : f[4], a67 = b0 ? f[7] : f[6];
-  const float a03 = b1 ? a23 : a01, a47 = b1 ? a67 : a45;
-  return b2 ? a47 : a03;
+// x[attr] from A registers (A = 8 or 16): a log2(A)-level select tree on the
+// attribute bits of the compact meta (4*attr in the low bits; ptxas turns the
+// bit tests into one R2P).  Selects move bits: exact.
+template <int A>
+__device__ __forceinline__ float pick_reg(const float (&f)[A], uint32_t meta) {
+  float v[A];
+#pragma unroll
+  for (int k = 0; k < A; ++k) v[k] = f[k];
+#pragma unroll
+  for (int w = A / 2, bit = 4; w >= 1; w /= 2, bit <<= 1) {
+    const bool b = meta & (uint32_t)bit;
+#pragma unroll
+    for (int k = 0; k < w; ++k) v[k] = b ? v[2 * k + 1] : v[2 * k];
+  }
+  return v[0];
 }
 
 template <int A, int S, int TLOC, int LOADER, int CAP>
@@ -449,17 +456,20 @@ __global__ void __launch_bounds__(kMaxThreads)
         }
         args.labels[r0 + r] = nd.w;
       }
-    } else if constexpr (TLOC == kSharedReg && LOADER == kTma && A == 8) {
-      // records -> registers (two conflict-free lds.128 each), tile freed at once
-      float f[S][8];
+    } else if constexpr (TLOC == kSharedReg && LOADER == kTma && (A == 8 || A == 16)) {
+      // records -> registers (A/4 conflict-free lds.128 each), tile freed at once
+      float f[S][A];
 #pragma unroll
       for (int q = 0; q < S; ++q) {
-        const uint32_t b = (uint32_t)(q * 32 + lane) * 32u;
-        const uint4 lo = lds_u4(tile + swz(b)), hi = lds_u4(tile + swz(b + 16u));
-        f[q][0] = __uint_as_float(lo.x); f[q][1] = __uint_as_float(lo.y);
-        f[q][2] = __uint_as_float(lo.z); f[q][3] = __uint_as_float(lo.w);
-        f[q][4] = __uint_as_float(hi.x); f[q][5] = __uint_as_float(hi.y);
-        f[q][6] = __uint_as_float(hi.z); f[q][7] = __uint_as_float(hi.w);
+        const uint32_t b = (uint32_t)(q * 32 + lane) * (4u * A);
+#pragma unroll
+        for (int c = 0; c < A / 4; ++c) {
+          const uint4 v = lds_u4(tile + swz(b + 16u * c));
+          f[q][4 * c + 0] = __uint_as_float(v.x);
+          f[q][4 * c + 1] = __uint_as_float(v.y);
+          f[q][4 * c + 2] = __uint_as_float(v.z);
+          f[q][4 * c + 3] = __uint_as_float(v.w);
+        }
       }
       pipe.release(i, t, step, n_tiles);  // next tile's TMA overlaps this walk
       uint32_t thr[S], meta[S];
@@ -475,7 +485,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         for (int q = 0; q < S; ++q) any |= (int)meta[q] >= 0;
         if (!any) break;
 #pragma unroll
-        for (int q = 0; q < S; ++q) data_step_v(thr[q], meta[q], pick8(f[q], meta[q]), tree.s, args.abits);
+        for (int q = 0; q < S; ++q) data_step_v(thr[q], meta[q], pick_reg<A>(f[q], meta[q]), tree.s, args.abits);
       }
 #pragma unroll
       for (int q = 0; q < S; ++q) {

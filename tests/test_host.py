@@ -272,3 +272,40 @@ def test_product_generators_fuzz_and_gaussian(co):
         st.generate_synthetic_tree(3, 9, 2, 2, 1)
     with pytest.raises(st.ArgumentError, match="need at least depth \\+ 1 leaves"):
         st.generate_synthetic_tree(5, 3, 2, 2, 1)
+
+
+def test_cli_cpu_strategies_and_exit_codes(tmp_path):
+    """tools/spectree_b200_cli (the reference CLI's verify/bench with GPU names,
+    built against the reference sources into oracle/_ref): CPU strategies run
+    here; a GPU strategy without a device exits 3 (Error, no CPU fallback);
+    an unknown strategy exits 2 (ArgumentError) -- main.cpp:37-40, 703-712."""
+    import subprocess
+
+    cli = os.path.join(ROOT, "oracle", "_ref", "spectree_b200_cli")
+    if not os.path.exists(cli):
+        pytest.skip("oracle/_ref/spectree_b200_cli not built (needs /root/reference)")
+    t, d = str(tmp_path / "t.json"), str(tmp_path / "d.strec")
+    r = subprocess.run([cli, "gen", "--records", "2000", "--out-tree", t, "--out-data", d],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([cli, "verify", "--tree", t, "--data", d, "--strategy", "serial", "--strategy", "data",
+                        "--strategy", "spec", "--strategy", "spec-basic"], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.count(": OK (2000 records)") == 4, r.stdout + r.stderr
+    r = subprocess.run([cli, "bench", "--tree", t, "--data", d, "--strategy", "serial", "--strategy", "data",
+                        "--iterations", "3", "--warmup", "1", "--format", "json"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    import json as _json
+    rep = _json.loads(r.stdout)
+    assert rep["version"] == 1 and [s["name"] for s in rep["strategies"]] == ["serial", "data"]
+    assert rep["strategies"][1]["inner_us"]["iterations"] == 3
+    import torch
+
+    if not torch.cuda.is_available():
+        r = subprocess.run([cli, "verify", "--tree", t, "--data", d, "--strategy", "gpu-data"],
+                           capture_output=True, text=True)
+        assert r.returncode == 3 and "no CUDA device" in r.stderr
+    r = subprocess.run([cli, "verify", "--tree", t, "--data", d, "--strategy", "nope"],
+                       capture_output=True, text=True)
+    assert r.returncode == 2
+    r = subprocess.run([cli, "verify", "--tree", t], capture_output=True, text=True)
+    assert r.returncode == 2 and "--data is required" in r.stderr

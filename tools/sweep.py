@@ -46,7 +46,13 @@ if "spec" in args.grid and "spec2" not in args.grid:
 if "spec2" in args.grid:
     for G, sr in itertools.product([2, 4, 8], [1, 2]):
         geoms.append(st.GpuGeom(algo="speculative", group_lanes=G, samples_per_thread=sr))
-if "regs" in args.grid:
+if "regs1" in args.grid:
+    for S, ns, w in itertools.product([1, 2, 4], [1, 2], [0, 32]):
+        geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, record_regs=1, stages=ns, warps_per_cta=w))
+if "regs0" in args.grid:
+    for S in [0, 1, 2]:
+        geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, record_regs=2))
+if "regs" in args.grid and "regs1" not in args.grid and "regs0" not in args.grid:
     for S, rr, w in itertools.product([0, 1, 2, 4], [1, 2], [0, 16]):
         geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, record_regs=rr, warps_per_cta=w))
 if "small" in args.grid:
