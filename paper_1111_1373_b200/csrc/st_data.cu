@@ -1,0 +1,150 @@
+// Data-decomposition kernel dispatch (K1 k_data, st_kernels.cuh).
+#include "st_internal.cuh"
+
+namespace sti {
+
+// ---- data kernel dispatch ------------------------------------------------
+template <int A, int S, int TLOC, int LOADER, int CAP>
+void launch_data_t(const DataArgs& d, const Staging& stg, const ConstTree<CAP>* ct, size_t smem,
+                   int dev, uint32_t bps, cudaStream_t s) {
+  auto fn = k_data<A, S, TLOC, LOADER, CAP>;
+  const uint64_t n_tiles = (d.p.m + 32 * S - 1) / (32 * S);
+  const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles, stg.warps);
+  static const ConstTree<1> dummy{};
+  clear_stale_error();
+  if constexpr (CAP == 1) {
+    fn<<<blocks, stg.warps * 32, smem, s>>>(d, stg.tmap, ct ? *ct : dummy);
+  } else {
+    fn<<<blocks, stg.warps * 32, smem, s>>>(d, stg.tmap, *ct);
+  }
+  check_launch();
+}
+
+template <int A, int S, int LOADER>
+void launch_data_tloc(int tloc, const DataArgs& d, const Staging& stg, const st_tree* t,
+                      size_t smem, int dev, uint32_t bps, cudaStream_t s) {
+  switch (tloc) {
+    case ST_TREE_SHARED:
+      if constexpr ((A == 8 || A == 16) && LOADER == kTma) {
+        if (d.record_regs) return launch_data_t<A, S, kSharedReg, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
+      }
+      return launch_data_t<A, S, kShared, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
+    case ST_TREE_GLOBAL:
+      return launch_data_t<A, S, kGlobal, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
+    case ST_TREE_CONSTANT: {
+      if constexpr (LOADER == kTma) {
+        if (t->compact.size() <= 512) {
+          ConstTree<512> ct{};
+          std::copy(t->compact.begin(), t->compact.end(), ct.n);
+          return launch_data_t<A, S, kConst, LOADER, 512>(d, stg, &ct, smem, dev, bps, s);
+        }
+        auto ct = std::make_unique<ConstTree<4000>>();
+        std::copy(t->compact.begin(), t->compact.end(), ct->n);
+        return launch_data_t<A, S, kConst, LOADER, 4000>(d, stg, ct.get(), smem, dev, bps, s);
+      }
+      break;
+    }
+    default:
+      break;
+  }
+  return launch_data_t<A, S, kWide, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
+}
+
+
+uint32_t choose_S(uint32_t a, uint32_t want) {
+  // instantiated: a=8 {1,2,4}, a=16 {1,2,4}, a=32 {1,2}, others {1}
+  const uint32_t maxS = (a == 8 || a == 16) ? 4 : a == 32 ? 2 : 1;
+  // predicated walk (k_data data_step): independent chains per lane pay off
+  // where a tile is small -- C3 (a = 8): S = 4 0.63 ms vs S = 2 0.67 ms for 32
+  // frames; C2 (a = 32): S = 2 0.307 vs S = 1 0.321 ms (profiles/r1_sweep_*)
+  if (want == 0) want = a <= 8 ? 4 : a == 32 ? 2 : 1;
+  uint32_t S = 1;
+  while (S * 2 <= std::min(want, maxS)) S *= 2;
+  return S;
+}
+
+template <int A>
+void launch_data_a(const Staging& stg, int tloc, const DataArgs& d, const st_tree* t, size_t smem,
+                   int dev, uint32_t bps, cudaStream_t s) {
+  if constexpr (A == 8 || A == 16) {
+    if (stg.S == 4) return launch_data_tloc<A, 4, kTma>(tloc, d, stg, t, smem, dev, bps, s);
+  }
+  if constexpr (A == 8 || A == 16 || A == 32) {
+    if (stg.S == 2) return launch_data_tloc<A, 2, kTma>(tloc, d, stg, t, smem, dev, bps, s);
+  }
+  return launch_data_tloc<A, 1, kTma>(tloc, d, stg, t, smem, dev, bps, s);
+}
+
+void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+                      const st_geom& g, uint32_t* labels, cudaStream_t s, int dev) {
+  st_tree::Dev& dv = t->device(dev);
+  const DevProps pr = dev_props(dev);
+  DataArgs d{};
+  d.p = pipe_args(x, m, a, ld, layout);
+  d.nodes = dv.compact;
+  d.wide = dv.wide;
+  d.n_nodes = (uint32_t)t->nodes.size();
+  d.abits = t->abits;
+  d.leaf_class = dv.leaf_tbl;
+  d.labels = labels;
+  // records walked from registers: default for 8-attribute records; 16 on request
+  d.record_regs = (g.record_regs == 1 || (g.record_regs == 0 && a == 8)) ? 1u : 0u;
+
+  const uint32_t tree_bytes = round1024(t->nodes.size() * sizeof(CNode));
+  int tloc = g.tree_loc;
+  if (!t->compact_ok) tloc = kWide;
+  else if (tloc == ST_TREE_AUTO) tloc = tree_bytes <= 96 * 1024 ? ST_TREE_SHARED : ST_TREE_GLOBAL;
+  if (tloc == ST_TREE_CONSTANT && t->compact.size() > 4000) tloc = ST_TREE_GLOBAL;
+  const uint32_t S0 = ct_arity(a) ? choose_S(a, g.samples_per_thread) : 1;
+  // Records walked from registers release their tile before the walk, so one
+  // stage per warp already double-buffers (next TMA in flight during the
+  // walk) and the saved shared memory buys twice the warps (C3 x 32 frames:
+  // 0.566 vs 0.615 ms, profiles/r1_sweep_C3x32_regs1.json).
+  const uint32_t want_ns = g.stages ? g.stages : (d.record_regs && tloc == ST_TREE_SHARED ? 1u : 0u);
+  Staging stg = plan_staging(x, m, a, ld, layout, S0, want_ns,
+                             tloc == ST_TREE_SHARED ? tree_bytes : 0, pr);
+  if (tloc == ST_TREE_SHARED && tree_bytes + 1024 + stg.tile_smem() > pr.smem_optin) {
+    tloc = ST_TREE_GLOBAL;
+    stg = plan_staging(x, m, a, ld, layout, S0, g.stages, 0, pr);
+  }
+  if (tloc == ST_TREE_CONSTANT && stg.loader != kTma) tloc = ST_TREE_GLOBAL;
+  // A large shared-memory tree is staged once per CTA: widen the CTA so that
+  // one copy serves up to 32 warps instead of capping the SM at one 8-warp CTA.
+  stg.warps = pick_warps(g.warps_per_cta, stg, tloc == ST_TREE_SHARED ? tree_bytes : 0, pr);
+  uint32_t want_bps = g.blocks_per_sm;
+  // Small inputs (< 8 tiles per warp at 32 warps/SM, e.g. C1's 1M records)
+  // are ramp-up bound: four 8-warp CTAs per SM stage their tree copies
+  // faster than one 32-warp CTA (C1: 17.0 vs 19.3 us, profiles/r1_sweep_C1x1_small_flush.json).
+  const uint64_t tiles_total = m / (32ull * stg.S);
+  if (!g.warps_per_cta && !g.blocks_per_sm && stg.loader == kTma && tloc == ST_TREE_SHARED &&
+      tiles_total < (uint64_t)pr.sms * 32 * 8 &&
+      4 * (1024 + tree_bytes + (size_t)kWarpsPerCta * stg.ns * (stg.stage_bytes + 8u)) <= pr.smem_per_sm) {
+    stg.warps = kWarpsPerCta;
+    want_bps = 4;
+  }
+  d.ns = stg.ns;
+  d.stage_bytes = stg.stage_bytes;
+  d.tree_bytes = tloc == ST_TREE_SHARED ? tree_bytes : 0;
+  const size_t smem = 1024 + d.tree_bytes + stg.tile_smem();
+  const uint32_t bps = default_bps(want_bps, stg, m, pr);
+  if (stg.loader == kTma && ct_arity(a)) {
+    switch (a) {
+      case 8: return launch_data_a<8>(stg, tloc, d, t, smem, dev, bps, s);
+      case 16: return launch_data_a<16>(stg, tloc, d, t, smem, dev, bps, s);
+      case 32: return launch_data_a<32>(stg, tloc, d, t, smem, dev, bps, s);
+      case 64: return launch_data_a<64>(stg, tloc, d, t, smem, dev, bps, s);
+    }
+  }
+  switch (stg.loader) {
+    case kTma: return launch_data_tloc<0, 1, kTma>(tloc, d, stg, t, smem, dev, bps, s);
+    case kDirect:
+      return launch_data_tloc<0, 1, kDirect>(tloc == ST_TREE_CONSTANT ? ST_TREE_GLOBAL : tloc, d,
+                                             stg, t, smem, dev, bps, s);
+    default:
+      return launch_data_tloc<0, 1, kScalar>(tloc == ST_TREE_CONSTANT ? ST_TREE_GLOBAL : tloc, d,
+                                             stg, t, smem, dev, bps, s);
+  }
+}
+
+
+}  // namespace sti

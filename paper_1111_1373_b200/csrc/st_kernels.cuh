@@ -1397,6 +1397,7 @@ struct SpecExactArgs {
   uint32_t* steps;
 };
 
+template <int = 0>  // a template so every translation unit may include this header
 __global__ void __launch_bounds__(kMaxThreads) k_spec_exact_cta(const SpecExactArgs args) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint32_t* buf_a = reinterpret_cast<uint32_t*>(smem);

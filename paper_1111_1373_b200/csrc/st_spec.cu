@@ -1,0 +1,255 @@
+// Speculative-decomposition kernel dispatch (K2 k_spec_ring / k_spec / k_spec_exact_cta).
+#include "st_internal.cuh"
+
+namespace sti {
+
+// ---- speculative kernel dispatch -----------------------------------------
+template <int A, int LOADER, bool WS, bool EXACT, int STEPS>
+void launch_spec_k(const SpecArgs& sa, const Staging& stg, size_t smem, int dev, uint32_t bps,
+                   cudaStream_t s) {
+  auto fn = k_spec<A, LOADER, WS, EXACT, STEPS>;
+  const uint64_t n_tiles = (sa.p.m + 31) / 32;
+  const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles, stg.warps);
+  clear_stale_error();
+  fn<<<blocks, stg.warps * 32, smem, s>>>(sa, stg.tmap);
+  check_launch();
+}
+
+// Fast path: the doubling count is a compile-time constant for the usual
+// window heights (steps 0..3); EXACT (reference counters) and taller windows
+// use a runtime count.
+template <int A, int LOADER, bool WS>
+void launch_spec_steps(const SpecArgs& sa, const Staging& stg, size_t smem, int dev, uint32_t bps,
+                       cudaStream_t s) {
+  if (sa.iters) return launch_spec_k<A, LOADER, WS, true, -1>(sa, stg, smem, dev, bps, s);
+  switch (sa.smax) {
+    case 0: return launch_spec_k<A, LOADER, WS, false, 0>(sa, stg, smem, dev, bps, s);
+    case 1: return launch_spec_k<A, LOADER, WS, false, 1>(sa, stg, smem, dev, bps, s);
+    case 2: return launch_spec_k<A, LOADER, WS, false, 2>(sa, stg, smem, dev, bps, s);
+    case 3: return launch_spec_k<A, LOADER, WS, false, 3>(sa, stg, smem, dev, bps, s);
+    default: return launch_spec_k<A, LOADER, WS, false, -1>(sa, stg, smem, dev, bps, s);
+  }
+}
+
+template <int A, bool WS, int STEPS, int SR>
+void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
+                        uint32_t warps, cudaStream_t s) {
+  auto fn = k_spec_ring<A, WS, STEPS, SR>;
+  const uint64_t n_tiles = (ra.s.p.m + 31) / 32;
+  const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles * warps, warps);
+  clear_stale_error();
+  fn<<<blocks, warps * 32, smem, s>>>(ra, stg.tmap);
+  check_launch();
+}
+
+template <int A, bool WS, int STEPS>
+void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
+                         uint32_t warps, cudaStream_t s) {
+  if (sr >= 2) return launch_spec_ring_k<A, WS, STEPS, 2>(ra, stg, smem, dev, warps, s);
+  return launch_spec_ring_k<A, WS, STEPS, 1>(ra, stg, smem, dev, warps, s);
+}
+
+template <int A>
+void launch_spec_ring(bool ws, uint32_t sr, const SpecRingArgs& ra, const Staging& stg, size_t smem,
+                      int dev, uint32_t warps, cudaStream_t s) {
+#define ST_RING(WSV, ST) return launch_spec_ring_sr<A, WSV, ST>(sr, ra, stg, smem, dev, warps, s)
+  if (ws) {
+    switch (ra.s.smax) {
+      case 0: ST_RING(true, 0);
+      case 1: ST_RING(true, 1);
+      case 2: ST_RING(true, 2);
+      case 3: ST_RING(true, 3);
+      default: ST_RING(true, -1);
+    }
+  }
+  switch (ra.s.smax) {
+    case 0: ST_RING(false, 0);
+    case 1: ST_RING(false, 1);
+    case 2: ST_RING(false, 2);
+    case 3: ST_RING(false, 3);
+    default: ST_RING(false, -1);
+  }
+#undef ST_RING
+}
+
+template <int A, int LOADER>
+void launch_spec_t(bool win_shared, const SpecArgs& sa, const Staging& stg, size_t smem, int dev,
+                   uint32_t bps, cudaStream_t s) {
+  if (win_shared) return launch_spec_steps<A, LOADER, true>(sa, stg, smem, dev, bps, s);
+  return launch_spec_steps<A, LOADER, false>(sa, stg, smem, dev, bps, s);
+}
+
+void spec_geometry(const st_tree* t, const st_geom& g, uint32_t& G, uint32_t& H) {
+  G = g.group_lanes;
+  if (G == 0) {
+    const uint32_t I = std::max<uint32_t>(1, t->info.internal);
+    if (I <= 32) {
+      // whole tree in one record group: the paper's Proc. 5 geometry
+      // (15 internal nodes -> its half-warp of 16 lanes)
+      G = 1;
+      while (G < I) G *= 2;
+    } else {
+      // larger trees: 3-node windows in 4-lane groups (two levels per window,
+      // one shfl doubling) measured fastest on C2 among genuine speculation
+      G = 4;
+    }
+  }
+  if (G > 32 || (G & (G - 1)) != 0)
+    fail(ST_ERR_ARGUMENT, "group_lanes must be a power of two <= 32 on the GPU, got " +
+                              std::to_string(g.group_lanes));
+  H = g.window_levels;
+  if (H == 0) {
+    if (t->info.internal <= G) {
+      // whole tree in one window: the paper's Proc. 5 geometry (mapped lanes)
+      H = std::max<uint32_t>(1, t->info.depth);
+    } else {
+      // complete-level windows: largest H with 2^H - 1 <= G
+      H = 1;
+      while ((2u << H) - 1 <= G) ++H;
+    }
+  }
+}
+
+// Reference counters for trees with more than 32 internal nodes: CTA-scope
+// whole-tree speculation (k_spec_exact_cta).
+void eval_spec_exact_cta(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                         int layout, uint32_t k, uint32_t* labels, st_stats* stats, cudaStream_t s,
+                         int dev) {
+  st_tree::Dev& dv = t->device(dev);
+  const DevProps pr = dev_props(dev);
+  SpecExactArgs ea{};
+  ea.p = pipe_args(x, m, a, ld, layout);
+  ea.nodes = dv.wide;
+  ea.map = dv.internal_map;
+  ea.n = (uint32_t)t->nodes.size();
+  ea.I = t->info.internal;
+  ea.k = k ? k : 1;
+  ea.labels = labels;
+  ea.iters = stats->iterations;
+  ea.steps = stats->doubling_steps;
+  const size_t smem = 8ull * t->nodes.size() + 16;
+  if (smem > pr.smem_optin) fail(ST_ERR_ARGUMENT, "tree too large for exact speculative counters");
+  const uint32_t threads = std::min<uint32_t>(1024, std::max<uint32_t>(32, (ea.I + 31) / 32 * 32));
+  auto fn = k_spec_exact_cta<0>;
+  static std::mutex mu;
+  static std::map<int, bool> attr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!attr.count(dev)) {
+      CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)pr.smem_optin));
+      attr[dev] = true;
+    }
+  }
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)threads, smem));
+  const uint64_t blocks = std::min<uint64_t>(m, (uint64_t)pr.sms * std::max(occ, 1));
+  clear_stale_error();
+  fn<<<(unsigned)blocks, threads, smem, s>>>(ea);
+  check_launch();
+}
+
+void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+                      const st_geom& g, uint32_t* labels, st_stats* stats, cudaStream_t s, int dev) {
+  if (stats && t->info.internal > 32) {
+    // counters are defined by whole-tree speculation (the reference law)
+    return eval_spec_exact_cta(t, x, m, a, ld, layout, g.reductions, labels, stats, s, dev);
+  }
+  st_geom gg = g;
+  if (stats) {
+    // whole tree in one record group so the counters follow the reference law
+    uint32_t G = 1;
+    while (G < std::max<uint32_t>(1, t->info.internal)) G *= 2;
+    gg.group_lanes = G;
+    gg.window_levels = std::max<uint32_t>(1, t->info.depth);
+  }
+  uint32_t G, H;
+  spec_geometry(t, gg, G, H);
+  if (4ull * t->info.max_attribute >= (1u << 24))
+    fail(ST_ERR_ARGUMENT, "speculative kernel requires attribute indices < 2^22");
+  auto wt = t->windows(G, H);
+  SEntry* wdev = t->device_windows(dev, G, H, *wt);
+  st_tree::Dev& dv = t->device(dev);
+  const DevProps pr = dev_props(dev);
+  SpecArgs sa{};
+  sa.p = pipe_args(x, m, a, ld, layout);
+  sa.win = wdev;
+  sa.n_entries = (uint32_t)wt->entries.size();
+  sa.root_code = wt->root_code;
+  sa.G = G;
+  sa.smax = wt->max_steps;
+  sa.k = g.reductions;
+  sa.leaf_class = dv.leaf_tbl;
+  sa.labels = labels;
+  if (stats) {
+    sa.iters = stats->iterations;
+    sa.steps = stats->doubling_steps;
+    if (!sa.iters || !sa.steps) fail(ST_ERR_ARGUMENT, "st_stats requires both arrays");
+    if (sa.k == 0) sa.k = 1;  // counters follow the reference loop (k per root check)
+  } else if (sa.k != 0) {
+    // k without counters: same labels; the fixed-step path is used
+    sa.k = 0;
+  }
+  const uint32_t win_bytes = round1024(wt->entries.size() * sizeof(SEntry));
+  bool win_shared = win_bytes <= 96 * 1024;
+  Staging stg = plan_staging(x, m, a, ld, layout, 1, g.stages, win_shared ? win_bytes : 0, pr);
+  if (win_shared && win_bytes + 1024 + stg.tile_smem() > pr.smem_optin) {
+    win_shared = false;
+    stg = plan_staging(x, m, a, ld, layout, 1, g.stages, 0, pr);
+  }
+  sa.win_bytes = win_shared ? win_bytes : 0;
+  if (stg.loader == kDirect) stg.ns = 1, stg.stage_bytes = 0;
+  // speculative is issue/latency-bound: several 8-warp CTAs per SM (the
+  // occupancy maximum) beat one wide CTA (C2: 0.52 vs 0.68 ms)
+  stg.warps = g.warps_per_cta ? pick_warps(g.warps_per_cta, stg, sa.win_bytes, pr) : kWarpsPerCta;
+  sa.ns = stg.ns;
+  sa.stage_bytes = stg.stage_bytes;
+  const size_t smem = 1024 + sa.win_bytes + (size_t)stg.warps * stg.ns * (stg.stage_bytes + 8u) +
+                      (size_t)stg.warps * 3 * 128;  // + per-warp label/counter rows
+  const uint32_t bps = g.blocks_per_sm;  // speculative is latency-bound: keep every resident CTA
+  // CTA-shared ring (default for the fast path): up to 32 warps on one SM
+  // share NS = warps + 12 tile slots; ~12 tiles in flight cover DRAM latency.
+  if (stg.loader == kTma && !stats && g.pipeline != 1) {
+    const size_t lb = 32 + 32 * 128;  // generation padding + ticket + per-warp label rows (<= 32 warps)
+    const size_t budget = pr.smem_optin - 1024 - sa.win_bytes - lb;
+    const size_t max_slots = budget / (stg.stage_bytes + 16u);
+    const uint32_t warps = (uint32_t)std::min<size_t>(32, max_slots > 12 ? max_slots - 12 : 0);
+    if (warps >= 4) {
+      SpecRingArgs ra{};
+      ra.s = sa;
+      ra.n_slots = (uint32_t)std::min<size_t>(max_slots, warps + 12);
+      // development / stress knob: any ring depth >= 1 must give exact labels
+      if (const uint32_t ns = env_u32("ST_SPEC_RING_SLOTS", 0)) ra.n_slots = std::min<uint32_t>(ra.n_slots, ns);
+      ra.unsafe_no_gen = env_u32("ST_SPEC_RING_UNSAFE_NO_GEN", 0);  // measurement of the handshake only
+      const size_t rsmem = 1024 + sa.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 8u) +
+                           (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128;
+      // record streams per group (samples_per_thread): one by default -- two
+      // independent window chains per lane measured slower (C2 G = 4: 0.55 vs
+      // 0.42 ms; profiles/r1_sweep_*_spec2.json)
+      const uint32_t sr = g.samples_per_thread ? g.samples_per_thread : 1;
+      switch (ct_arity(a) ? a : 0) {
+        case 8: return launch_spec_ring<8>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+        case 16: return launch_spec_ring<16>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+        case 32: return launch_spec_ring<32>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+        case 64: return launch_spec_ring<64>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+        default: return launch_spec_ring<0>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+      }
+    }
+  }
+  if (stg.loader == kTma && ct_arity(a)) {
+    switch (a) {
+      case 8: return launch_spec_t<8, kTma>(win_shared, sa, stg, smem, dev, bps, s);
+      case 16: return launch_spec_t<16, kTma>(win_shared, sa, stg, smem, dev, bps, s);
+      case 32: return launch_spec_t<32, kTma>(win_shared, sa, stg, smem, dev, bps, s);
+      case 64: return launch_spec_t<64, kTma>(win_shared, sa, stg, smem, dev, bps, s);
+    }
+  }
+  switch (stg.loader) {
+    case kTma: return launch_spec_t<0, kTma>(win_shared, sa, stg, smem, dev, bps, s);
+    case kDirect: return launch_spec_t<0, kDirect>(win_shared, sa, stg, smem, dev, bps, s);
+    default: return launch_spec_t<0, kScalar>(win_shared, sa, stg, smem, dev, bps, s);
+  }
+}
+
+
+}  // namespace sti
