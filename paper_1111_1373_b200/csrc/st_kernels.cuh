@@ -943,6 +943,57 @@ __global__ void __launch_bounds__(kMaxThreads)
           woff = root & ~kExitBit;
         }
       } while (__any_sync(0xffffffffu, active));
+    } else if constexpr (SR == 2 && WIN_SHARED && Rec<A, kTma>::kRowLocal) {
+      // Two record streams per group in the lean style (no predication; an
+      // exhausted stream re-walks its last record): two independent window
+      // chains per lane to overlap the entry -> feature -> shuffle latencies.
+      const uint32_t a4 = 4u * (uint32_t)A;
+      auto base_of = [&](uint32_t rr) {
+        const uint32_t ra4 = rr * a4, rowb = ra4 & ~127u;
+        return (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
+      };
+      uint32_t rA = g, rB = g + NG;
+      bool aA = rA < rows, aB = rB < rows;
+      uint32_t wA = 0, wB = 0;
+      uint32_t bA = base_of(aA ? rA : 0u), bB = base_of(aB ? rB : 0u);
+      do {
+        const uint4 eA = lds_u4(jaddr + wA), eB = lds_u4(jaddr + wB);
+        const float vA = lds_f32((eA.y & 0x00FFFFFFu) ^ bA), vB = lds_f32((eB.y & 0x00FFFFFFu) ^ bB);
+        uint32_t cA = (vA > __uint_as_float(eA.x)) ? eA.w : eA.z;
+        uint32_t cB = (vB > __uint_as_float(eB.x)) ? eB.w : eB.z;
+        auto jump = [&]() {
+          const uint32_t uA = __shfl_sync(0xffffffffu, cA, cA & gmask, G);
+          const uint32_t uB = __shfl_sync(0xffffffffu, cB, cB & gmask, G);
+          cA = (cA < 32u) ? uA : cA;
+          cB = (cB < 32u) ? uB : cB;
+        };
+        if constexpr (STEPS >= 0) {
+#pragma unroll
+          for (int st = 0; st < STEPS; ++st) jump();
+        } else {
+          for (uint32_t st = 0; st < args.smax; ++st) jump();
+        }
+        const uint32_t rtA = __shfl_sync(0xffffffffu, cA, 0, G);
+        const uint32_t rtB = __shfl_sync(0xffffffffu, cB, 0, G);
+        if (rtA & kLeafBit) {
+          if (aA && j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rA), "r"(rtA) : "memory");
+          rA += 2 * NG;
+          aA = rA < rows;
+          wA = 0;
+          if (aA) bA = base_of(rA);
+        } else {
+          wA = rtA & ~kExitBit;
+        }
+        if (rtB & kLeafBit) {
+          if (aB && j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rB), "r"(rtB) : "memory");
+          rB += 2 * NG;
+          aB = rB < rows;
+          wB = 0;
+          if (aB) bB = base_of(rB);
+        } else {
+          wB = rtB & ~kExitBit;
+        }
+      } while (__any_sync(0xffffffffu, aA || aB));
     } else {
       // SR independent record streams per group: stream s classifies rows
       // g + s*NG, g + (s + SR)*NG, ...  Two streams double the independent
