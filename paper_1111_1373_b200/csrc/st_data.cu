@@ -95,6 +95,9 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   if (!t->compact_ok) tloc = kWide;
   else if (tloc == ST_TREE_AUTO) tloc = tree_bytes <= 96 * 1024 ? ST_TREE_SHARED : ST_TREE_GLOBAL;
   if (tloc == ST_TREE_CONSTANT && t->compact.size() > 4000) tloc = ST_TREE_GLOBAL;
+  // shared trees are rebased to absolute shared addresses inside the compact
+  // child field: the largest address must fit below the leaf bit
+  if (tloc == ST_TREE_SHARED && ((uint64_t)pr.smem_optin << t->abits) >= (1ull << 31)) tloc = ST_TREE_GLOBAL;
   const uint32_t S0 = ct_arity(a) ? choose_S(a, g.samples_per_thread) : 1;
   // Records walked from registers release their tile before the walk, so one
   // stage per warp already double-buffers (next TMA in flight during the

@@ -291,19 +291,27 @@ struct ConstTree {
   CNode n[CAP];
 };
 
+// Shared-memory trees are rebased when staged: an internal node's child field
+// then holds the child's absolute shared-memory byte address, so the walk's
+// next-node address is (meta >> abits) + 8*(x > thr) with no base add.
+// Constant / global trees keep offsets relative to node 0.
+template <int TLOC>
+constexpr bool kAbsTree = (TLOC == kShared || TLOC == kSharedReg);
+
 template <int TLOC, int CAP>
 struct TreeRef {
   uint32_t s;                   // shared address of node 0
   const char* g;                // global node array
   const ConstTree<CAP>* c;      // constant-bank copy
+  __device__ __forceinline__ uint32_t root() const { return kAbsTree<TLOC> ? s : 0u; }
   __device__ __forceinline__ uint2 get(uint32_t off) const {
     if constexpr (TLOC == kConst) {
       const CNode n = *reinterpret_cast<const CNode*>(reinterpret_cast<const char*>(c->n) + off);
       return make_uint2(__float_as_uint(n.thr), n.meta);
     } else if constexpr (TLOC == kGlobal) {
       return __ldg(reinterpret_cast<const uint2*>(g + off));
-    } else {  // kShared, kSharedReg
-      return lds_u2(s + off);
+    } else {  // kShared, kSharedReg: absolute shared addresses
+      return lds_u2(off);
     }
   }
 };
@@ -334,45 +342,42 @@ __device__ __forceinline__ uint32_t align1024(uint32_t a) { return (a + 1023u) &
 // node = tb + child + 8*(x[attr] > thr).  bx = row base | in-row XOR mask, so
 // the feature address is one LOP3 ((4*attr) ^ bx); leaves stay put with no
 // branch and no shared-memory traffic.  Ordered compare, no FTZ (tree.hpp:53).
-__device__ __forceinline__ void data_step(uint32_t& thr, uint32_t& meta, uint32_t bx, uint32_t tb,
-                                          uint32_t amask, uint32_t abits) {
+__device__ __forceinline__ void data_step(uint32_t& thr, uint32_t& meta, uint32_t bx, uint32_t amask,
+                                          uint32_t abits) {
   asm volatile(
       "{\n\t"
       ".reg .pred p, q;\n\t"
       ".reg .u32 fa, ch;\n\t"
       ".reg .f32 v;\n\t"
       "setp.ge.s32 p, %1, 0;\n\t"
-      "and.b32 fa, %1, %4;\n\t"
+      "and.b32 fa, %1, %3;\n\t"
       "xor.b32 fa, fa, %2;\n\t"
       "@p ld.shared.f32 v, [fa];\n\t"
       "setp.gt.and.f32 q, v, %0, p;\n\t"
-      "shr.u32 ch, %1, %5;\n\t"
-      "add.u32 ch, ch, %3;\n\t"
+      "shr.u32 ch, %1, %4;\n\t"
       "@q add.u32 ch, ch, 8;\n\t"
       "@p ld.shared.v2.u32 {%0, %1}, [ch];\n\t"
       "}"
       : "+f"(*reinterpret_cast<float*>(&thr)), "+r"(meta)
-      : "r"(bx), "r"(tb), "r"(amask), "r"(abits)
+      : "r"(bx), "r"(amask), "r"(abits)
       : "memory");
 }
 
 // Level step with the feature already selected from registers: if the node
 // is internal, node = tb + child + 8*(v > thr).
-__device__ __forceinline__ void data_step_v(uint32_t& thr, uint32_t& meta, float v, uint32_t tb,
-                                            uint32_t abits) {
+__device__ __forceinline__ void data_step_v(uint32_t& thr, uint32_t& meta, float v, uint32_t abits) {
   asm volatile(
       "{\n\t"
       ".reg .pred p, q;\n\t"
       ".reg .u32 ch;\n\t"
       "setp.ge.s32 p, %1, 0;\n\t"
       "setp.gt.and.f32 q, %2, %0, p;\n\t"
-      "shr.u32 ch, %1, %4;\n\t"
-      "add.u32 ch, ch, %3;\n\t"
+      "shr.u32 ch, %1, %3;\n\t"
       "@q add.u32 ch, ch, 8;\n\t"
       "@p ld.shared.v2.u32 {%0, %1}, [ch];\n\t"
       "}"
       : "+f"(*reinterpret_cast<float*>(&thr)), "+r"(meta)
-      : "f"(v), "r"(tb), "r"(abits)
+      : "f"(v), "r"(abits)
       : "memory");
 }
 
@@ -428,8 +433,11 @@ __global__ void __launch_bounds__(kMaxThreads)
   if constexpr (TLOC == kShared || TLOC == kSharedReg) {
     const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
     const uint32_t n16 = (args.n_nodes * 8u + 15u) / 16u;
+    const uint32_t rebase = sbase << args.abits;  // child offset -> absolute address
     for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
-      const uint4 v = __ldg(src + i);
+      uint4 v = __ldg(src + i);
+      if (!(v.y & kLeafBit)) v.y += rebase;
+      if (!(v.w & kLeafBit)) v.w += rebase;
       asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
                    "r"(v.y), "r"(v.z), "r"(v.w)
                    : "memory");
@@ -473,7 +481,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       }
       pipe.release(i, t, step, n_tiles);  // next tile's TMA overlaps this walk
       uint32_t thr[S], meta[S];
-      const uint2 root = tree.get(0);
+      const uint2 root = tree.get(tree.root());
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         thr[q] = root.x;
@@ -485,7 +493,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         for (int q = 0; q < S; ++q) any |= (int)meta[q] >= 0;
         if (!any) break;
 #pragma unroll
-        for (int q = 0; q < S; ++q) data_step_v(thr[q], meta[q], pick_reg<A>(f[q], meta[q]), tree.s, args.abits);
+        for (int q = 0; q < S; ++q) data_step_v(thr[q], meta[q], pick_reg<A>(f[q], meta[q]), args.abits);
       }
 #pragma unroll
       for (int q = 0; q < S; ++q) {
@@ -499,7 +507,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     } else if constexpr (TLOC == kShared && LOADER == kTma && Rec<A, LOADER>::kRowLocal) {
       // S independent predicated chains per lane (no per-level branches)
       uint32_t thr[S], meta[S], bx[S];
-      const uint2 root = tree.get(0);
+      const uint2 root = tree.get(tree.root());
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         const uint32_t r = q * 32 + lane;
@@ -515,7 +523,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         for (int q = 0; q < S; ++q) any |= (int)meta[q] >= 0;
         if (!any) break;
 #pragma unroll
-        for (int q = 0; q < S; ++q) data_step(thr[q], meta[q], bx[q], tree.s, amask, args.abits);
+        for (int q = 0; q < S; ++q) data_step(thr[q], meta[q], bx[q], amask, args.abits);
       }
 #pragma unroll
       for (int q = 0; q < S; ++q) {
@@ -530,7 +538,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       const bool valid = r0 + r < m;
       Rec<A, LOADER> rec;
       rec.init(tile, r, args.p.a, args.p.x, r0 + (valid ? r : 0), args.p.ld, args.p.layout_soa);
-      uint2 nd = tree.get(0);
+      uint2 nd = tree.get(tree.root());
       uint32_t meta = valid ? nd.y : kLeafBit;
       float thr = __uint_as_float(nd.x);
       // Branch-free successor per level: child + (x > thr), as byte offsets.
@@ -548,7 +556,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       Rec<A, LOADER> rec[S];
       float thr[S];
       uint32_t meta[S];
-      const uint2 root = tree.get(0);
+      const uint2 root = tree.get(tree.root());
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         const uint32_t r = q * 32 + lane;
@@ -995,90 +1003,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         }
       } while (__any_sync(0xffffffffu, aA || aB));
     } else {
-      // SR independent record streams per group: stream s classifies rows
-      // g + s*NG, g + (s + SR)*NG, ...  Two streams double the independent
-      // load chains per lane (the window step is a dependent chain of
-      // shared-memory loads and shuffles).  A group whose stream has run out
-      // of rows issues no loads for it (predicated), but still takes part in
-      // the shuffles, which need every lane of the warp.
-      constexpr bool kRowLocal = Rec<A, kTma>::kRowLocal;
-      const uint32_t a4 = 4u * (A > 0 ? (uint32_t)A : args.p.a);
-      uint32_t r[SR], woff[SR], bx[SR];
-      bool active[SR];
-      Rec<A, kTma> rec[SR];
-#pragma unroll
-      for (int q = 0; q < SR; ++q) {
-        r[q] = g + q * NG;
-        active[q] = r[q] < rows;
-        woff[q] = 0;
-        const uint32_t rr = active[q] ? r[q] : 0u;
-        if constexpr (kRowLocal) {
-          const uint32_t ra4 = rr * a4, rowb = ra4 & ~127u;
-          bx[q] = (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
-        } else {
-          rec[q].init(tile, rr, args.p.a, args.p.x, 0, 0, 0);
-        }
-      }
-      bool any = true;
-      while (any) {
-        uint32_t c[SR];
-#pragma unroll
-        for (int q = 0; q < SR; ++q) {
-          c[q] = kLeafBit;  // an exhausted stream carries a non-lane code
-          if (active[q]) {
-            uint4 e;
-            if constexpr (WIN_SHARED) e = lds_u4(jaddr + woff[q]);
-            else e = __ldg(reinterpret_cast<const uint4*>(wglob + woff[q]));
-            float v;
-            if constexpr (kRowLocal) v = lds_f32((e.y & 0x00FFFFFFu) ^ bx[q]);
-            else v = rec[q].get(e.y & 0x00FFFFFFu);
-            c[q] = (v > __uint_as_float(e.x)) ? e.w : e.z;
-          }
-        }
-        if constexpr (STEPS >= 0) {
-#pragma unroll
-          for (int st = 0; st < STEPS; ++st) {
-#pragma unroll
-            for (int q = 0; q < SR; ++q) {
-              const uint32_t u = __shfl_sync(0xffffffffu, c[q], c[q] & gmask, G);
-              c[q] = (c[q] < 32u) ? u : c[q];
-            }
-          }
-        } else {
-          for (uint32_t st = 0; st < args.smax; ++st) {
-#pragma unroll
-            for (int q = 0; q < SR; ++q) {
-              const uint32_t u = __shfl_sync(0xffffffffu, c[q], c[q] & gmask, G);
-              c[q] = (c[q] < 32u) ? u : c[q];
-            }
-          }
-        }
-        any = false;
-#pragma unroll
-        for (int q = 0; q < SR; ++q) {
-          const uint32_t root = __shfl_sync(0xffffffffu, c[q], 0, G);
-          if (active[q]) {
-            if (root & kLeafBit) {
-              if (j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r[q]), "r"(root) : "memory");
-              r[q] += SR * NG;
-              active[q] = r[q] < rows;
-              woff[q] = 0;
-              if (active[q]) {
-                if constexpr (kRowLocal) {
-                  const uint32_t ra4 = r[q] * a4, rowb = ra4 & ~127u;
-                  bx[q] = (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
-                } else {
-                  rec[q].init(tile, r[q], args.p.a, args.p.x, 0, 0, 0);
-                }
-              }
-            } else {
-              woff[q] = root & ~kExitBit;
-            }
-          }
-          any |= active[q];
-        }
-        any = __any_sync(0xffffffffu, any);
-      }
+      static_assert(SR == 1 || SR == 2, "one or two record streams per group");
     }
     __syncwarp();
     if (tk + NS < my_tiles) {

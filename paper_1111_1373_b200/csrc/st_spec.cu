@@ -45,7 +45,10 @@ void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem,
 template <int A, bool WS, int STEPS>
 void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
                          uint32_t warps, cudaStream_t s) {
-  if (sr >= 2) return launch_spec_ring_k<A, WS, STEPS, 2>(ra, stg, smem, dev, warps, s);
+  // two record streams: shared window table and records inside one 128-byte row
+  if constexpr (WS && (A == 8 || A == 16 || A == 32)) {
+    if (sr >= 2) return launch_spec_ring_k<A, WS, STEPS, 2>(ra, stg, smem, dev, warps, s);
+  }
   return launch_spec_ring_k<A, WS, STEPS, 1>(ra, stg, smem, dev, warps, s);
 }
 
