@@ -18,13 +18,17 @@ GOLD = os.path.join(os.path.dirname(__file__), "golden")
 DATA_GEOMS = [st.GpuGeom(algo="data"),
               st.GpuGeom(algo="data", samples_per_thread=1),
               st.GpuGeom(algo="data", tree_loc="global"),
-              st.GpuGeom(algo="data", tree_loc="constant")]
+              st.GpuGeom(algo="data", tree_loc="constant"),
+              st.GpuGeom(algo="data", record_regs=1, samples_per_thread=2),   # 8/16 attrs from registers
+              st.GpuGeom(algo="data", record_regs=2, stages=3)]
 SPEC_GEOMS = [st.GpuGeom(algo="speculative"),
               st.GpuGeom(algo="speculative", group_lanes=4),
               st.GpuGeom(algo="speculative", group_lanes=8),
               st.GpuGeom(algo="speculative", group_lanes=32),
               st.GpuGeom(algo="speculative", group_lanes=16, window_levels=8),
-              st.GpuGeom(algo="speculative", reductions=2)]
+              st.GpuGeom(algo="speculative", reductions=2),
+              st.GpuGeom(algo="speculative", samples_per_thread=2),           # two record streams
+              st.GpuGeom(algo="speculative", group_lanes=8, samples_per_thread=2)]
 ALL_GEOMS = DATA_GEOMS + SPEC_GEOMS
 
 

@@ -123,8 +123,8 @@ def test_spec_ring_shallow_ring_stress(cuda, co, slots, monkeypatch):
     want = co.eval_serial(nodes, x)
     xd = torch.from_numpy(x).cuda()
     monkeypatch.setenv("ST_SPEC_RING_SLOTS", str(slots))
-    for _ in range(3):
+    for sr in (1, 2, 1):
         out = torch.empty(len(x), dtype=torch.int32, device="cuda")
-        st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative", pipeline=2))
+        st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative", pipeline=2, samples_per_thread=sr))
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want)

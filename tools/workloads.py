@@ -128,6 +128,7 @@ def main():
     ap.add_argument("--only", default="C1,C2,C3,C4,C5")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--flush", choices=("read", "write"), default="read")
+    ap.add_argument("--e2e", action="store_true", help="also time C1 / C3 / C4 end to end from pinned host memory")
     args = ap.parse_args()
     global FLUSH_MODE
     FLUSH_MODE = args.flush
@@ -184,6 +185,38 @@ def main():
                      "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 4), "labels_ok": bool(ok),
                      "trees": 128, "node_visits_per_s_est": len(x) * 128 * 9.09 / (ms * 1e-3)}
         print("C4", json.dumps(out["C4"]), flush=True)
+    if "E2E" in only or args.e2e:
+        # end to end through the host-buffer API (pinned host records -> H2D ->
+        # kernel -> D2H labels, chunked over 3 streams): PCIe-bound
+        e2e = {}
+        for name in ("C1", "C3"):
+            w = W[name]
+            tree = st.generate_synthetic_tree(*w["tree"])
+            xh = torch.empty((w["m"], w["a"]), dtype=torch.float32, pin_memory=True)
+            st.generate_synthetic_dataset(w["m"], w["a"], w["seed"], out=xh.numpy())
+            lab = torch.empty(w["m"], dtype=torch.int32, pin_memory=True)
+            st.eval_gpu(tree, xh.numpy(), out=lab.numpy().view(np.uint32))
+            t0 = time.perf_counter()
+            reps = 10
+            for _ in range(reps):
+                st.eval_gpu(tree, xh.numpy(), out=lab.numpy().view(np.uint32))
+            dt = (time.perf_counter() - t0) / reps
+            e2e[name] = {"s_per_call": dt, "samples_per_s": w["m"] / dt,
+                         "h2d_GBs": 4 * w["a"] * w["m"] / dt / 1e9,
+                         "frames_per_s" if name == "C3" else "calls_per_s": 1.0 / dt}
+            print("E2E", name, json.dumps(e2e[name]), flush=True)
+        trees = [st.generate_synthetic_tree(12, 1024, 64, 8, 401 + t) for t in range(128)]
+        f = st.Forest(trees, 8)
+        xh = torch.empty((8_000_000, 64), dtype=torch.float32, pin_memory=True)
+        st.generate_synthetic_dataset(8_000_000, 64, 499, out=xh.numpy())
+        st.eval_forest(f, xh.numpy())
+        t0 = time.perf_counter()
+        lab = st.eval_forest(f, xh.numpy())
+        dt = time.perf_counter() - t0
+        e2e["C4"] = {"s_per_call": dt, "samples_per_s": 8_000_000 / dt,
+                     "labels_ok": st.fnv1a64(lab) == 0x1b2543c41e436ce0}
+        print("E2E C4", json.dumps(e2e["C4"]), flush=True)
+        out["e2e"] = e2e
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", f"workloads_{FLUSH_MODE}.json"), "w") as fh:
         json.dump(out, fh, indent=1)
