@@ -90,7 +90,12 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // records walked from registers: default for 8-attribute records; 16 on request
   d.record_regs = (g.record_regs == 1 || (g.record_regs == 0 && a == 8)) ? 1u : 0u;
 
-  const uint32_t tree_bytes = round1024(t->nodes.size() * sizeof(CNode));
+  // the folded tree (leaf pairs inside terminals) serves the shared-tree TMA
+  // walks over 8/16/32-attribute records; every other path reads `compact`
+  const bool fold = t->fold_ok && (a == 8 || a == 16 || a == 32) &&
+                    (g.tree_loc == ST_TREE_AUTO || g.tree_loc == ST_TREE_SHARED) &&
+                    tma_ok(x, m, a, ld, layout, ct_arity(a) ? choose_S(a, g.samples_per_thread) : 1);
+  uint32_t tree_bytes = round1024((fold ? t->folded.size() : t->nodes.size()) * sizeof(CNode));
   int tloc = g.tree_loc;
   if (!t->compact_ok) tloc = kWide;
   else if (tloc == ST_TREE_AUTO) tloc = tree_bytes <= 96 * 1024 ? ST_TREE_SHARED : ST_TREE_GLOBAL;
@@ -127,6 +132,11 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   }
   d.ns = stg.ns;
   d.stage_bytes = stg.stage_bytes;
+  if (fold && tloc == ST_TREE_SHARED) {
+    if (stg.loader != kTma) fail(ST_ERR_CUDA, "internal: folded tree without the TMA walk");
+    d.nodes = dv.folded;
+    d.n_nodes = (uint32_t)t->folded.size();
+  }
   d.tree_bytes = tloc == ST_TREE_SHARED ? tree_bytes : 0;
   const size_t smem = 1024 + d.tree_bytes + stg.tile_smem();
   const uint32_t bps = default_bps(want_bps, stg, m, pr);

@@ -141,11 +141,14 @@ struct st_tree {
   std::vector<uint32_t> leaf_classes;  // ordinal -> class
   std::vector<uint32_t> leaf_code;     // node -> code payload (class or ordinal)
   std::vector<CNode> compact;
+  std::vector<CNode> folded;  // leaf pairs folded into terminals (data walk, shared tree)
+  bool fold_ok = false;
 
   std::mutex mu;
   std::map<std::pair<uint32_t, uint32_t>, std::shared_ptr<WinTable>> wins;  // (G, H)
   struct Dev {
     CNode* compact = nullptr;
+    CNode* folded = nullptr;
     uint4* wide = nullptr;
     uint32_t* leaf_tbl = nullptr;
     uint32_t* internal_map = nullptr;  // processor_node_map (tree.cpp:204-209)
@@ -159,6 +162,7 @@ struct st_tree {
     for (auto& kv : dev) {
       if (cudaSetDevice(kv.first) != cudaSuccess) continue;
       cudaFree(kv.second.compact);
+      cudaFree(kv.second.folded);
       cudaFree(kv.second.wide);
       cudaFree(kv.second.leaf_tbl);
       cudaFree(kv.second.internal_map);
@@ -288,6 +292,12 @@ struct st_tree {
       CK(cudaMemcpy(dv.compact, compact.data(), compact.size() * sizeof(CNode),
                     cudaMemcpyHostToDevice));
     }
+    if (fold_ok) {
+      const size_t bytes = ((folded.size() * sizeof(CNode) + 15) & ~size_t(15)) + 16;
+      CK(cudaMalloc(&dv.folded, bytes));
+      CK(cudaMemset(dv.folded, 0, bytes));
+      CK(cudaMemcpy(dv.folded, folded.data(), folded.size() * sizeof(CNode), cudaMemcpyHostToDevice));
+    }
     {
       std::vector<uint32_t> map;
       for (uint32_t i = 0; i < nodes.size(); ++i)
@@ -385,7 +395,9 @@ inline uint32_t bits_for(uint64_t v) {  // bits to hold values 0..v
 
 // Compact meta for an internal node: (8*child) << abits | 4*attr.
 inline bool compact_fits(uint32_t n, uint32_t max_attribute, uint32_t* abits) {
-  *abits = bits_for(4ull * max_attribute);
+  // at least 6 bits: the register walk selects x[attr] from the meta's bits
+  // 2..5 (16 attributes) without masking, so they must be attribute bits
+  *abits = std::max<uint32_t>(6, bits_for(4ull * max_attribute));
   return *abits < 31 && ((8ull * n) << *abits) < (1ull << 31);
 }
 
@@ -432,6 +444,31 @@ inline std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
     }
   }
   in.compact = t->compact_ok ? 1 : 0;
+  // Folded layout for the shared-tree data walk: BFS, children adjacent, every
+  // internal node whose two children are leaves becomes a terminal carrying
+  // both classes (kPairBit); its leaves are dropped.  Needs classes < 1024,
+  // 4*attr < 1024 and a compact encoding.
+  if (t->compact_ok && !t->leaf_table && in.max_class < 1024 && 4ull * in.max_attribute < 1024 && n > 1) {
+    auto is_leaf = [&](uint32_t i) { return nodes[i].class_id != ST_NO_CLASS; };
+    std::vector<uint32_t> order{0};  // original index per folded slot
+    std::vector<CNode>& f = t->folded;
+    f.clear();
+    for (size_t k = 0; k < order.size() && order.size() <= 2ull * n; ++k) {  // DAG inputs may not shrink
+      const st_node& nd = nodes[order[k]];
+      if (is_leaf(order[k])) {
+        f.push_back(CNode{nd.threshold, kLeafBit | nd.class_id});
+      } else if (is_leaf(nd.child) && is_leaf(nd.child + 1)) {
+        f.push_back(CNode{nd.threshold, kLeafBit | kPairBit | (nodes[nd.child + 1].class_id << 20) |
+                                            (nodes[nd.child].class_id << 10) | (4u * nd.attribute)});
+      } else {
+        const uint32_t fc = (uint32_t)order.size();  // children take the next two slots
+        f.push_back(CNode{nd.threshold, ((8u * fc) << t->abits) | (4u * nd.attribute)});
+        order.push_back(nd.child);
+        order.push_back(nd.child + 1);
+      }
+    }
+    t->fold_ok = f.size() == order.size() && f.size() <= n && ((8ull * f.size()) << t->abits) < (1ull << 31);
+  }
   return t;
 }
 

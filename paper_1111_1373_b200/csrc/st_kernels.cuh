@@ -32,6 +32,10 @@ namespace stk {
 
 constexpr uint32_t kLeafBit = 0x80000000u;  // compact-node meta: leaf marker
 constexpr uint32_t kExitBit = 0x40000000u;  // speculative code: exit to window
+// Folded data-walk trees: a node whose two children are both leaves becomes a
+// terminal  {thr, kLeafBit | kPairBit | classR << 20 | classL << 10 | 4*attr}
+// (classes < 1024, 4*attr < 1024); its leaf pair is dropped from the array.
+constexpr uint32_t kPairBit = 0x40000000u;
 constexpr uint32_t kNoClass = 0xFFFFFFFFu;
 constexpr int kWarpsPerCta = 8;    // default CTA width (warps); launches may use up to 32
 constexpr int kMaxThreads = 1024;
@@ -496,6 +500,14 @@ __global__ void __launch_bounds__(kMaxThreads)
         for (int q = 0; q < S; ++q) data_step_v(thr[q], meta[q], pick_reg<A>(f[q], meta[q]), args.abits);
       }
 #pragma unroll
+      for (int q = 0; q < S; ++q) {  // folded terminal: last predicate picks the leaf of the pair
+        if (meta[q] & kPairBit) {
+          const float v = pick_reg<A>(f[q], meta[q]);
+          const uint32_t c = (v > __uint_as_float(thr[q])) ? (meta[q] >> 20) : (meta[q] >> 10);
+          meta[q] = kLeafBit | (c & 0x3FFu);
+        }
+      }
+#pragma unroll
       for (int q = 0; q < S; ++q) {
         const uint64_t r = r0 + q * 32 + lane;
         if (r < m) {
@@ -524,6 +536,14 @@ __global__ void __launch_bounds__(kMaxThreads)
         if (!any) break;
 #pragma unroll
         for (int q = 0; q < S; ++q) data_step(thr[q], meta[q], bx[q], amask, args.abits);
+      }
+#pragma unroll
+      for (int q = 0; q < S; ++q) {  // folded terminal: last predicate picks the leaf of the pair
+        if (meta[q] & kPairBit) {
+          const float v = lds_f32((meta[q] & 0x3FFu) ^ bx[q]);
+          const uint32_t c = (v > __uint_as_float(thr[q])) ? (meta[q] >> 20) : (meta[q] >> 10);
+          meta[q] = kLeafBit | (c & 0x3FFu);
+        }
       }
 #pragma unroll
       for (int q = 0; q < S; ++q) {

@@ -357,3 +357,35 @@ def test_reference_acceptance_through_cpp_dropin(cuda):
     print(p.stdout)
     assert p.returncode == 0, p.stdout + p.stderr
     assert p.stdout.count("PASS") >= 5
+
+
+def test_folded_tree_walks(cuda, co):
+    """Folded shared trees (leaf pairs inside terminal nodes) for 8/16/32-
+    attribute records: all 626 exhaustive shapes (terminal roots, mixed
+    pairs, ties on grid records) and 300 synthetic trees, through the
+    register walk and the shared-tile walk, against the oracles."""
+    geoms = [st.GpuGeom(algo="data"), st.GpuGeom(algo="data", record_regs=2),
+             st.GpuGeom(algo="data", record_regs=1, samples_per_thread=1)]
+    for leaves in range(1, 9):
+        for shape in support.all_shapes(leaves):
+            internal = support.assign_labels(shape)
+            x = support.grid_records(internal)
+            tree = encode_breadth_first(shape)
+            want = support.recursive_oracle(shape, x)
+            for a in (8, 16):
+                if x.shape[1] > a:
+                    continue
+                xa = np.zeros((len(x), a), np.float32)
+                xa[:, : x.shape[1]] = x
+                reps = -(-512 // len(xa))  # several full TMA tiles
+                xa = np.tile(xa, (reps, 1))
+                for g in geoms:
+                    assert np.array_equal(st.eval_gpu(tree, xa, g), np.tile(want, reps)), (leaves, a, g)
+    for seed in range(1, 301):
+        depth, leaves, _, classes = support.fuzz_shape(seed)
+        a = (8, 16, 32)[seed % 3]
+        nodes = co.gen_tree(depth, leaves, a, classes, seed)
+        x = co.gen_dataset(2000, a, seed + 7000, gaussian=(seed % 2 == 0))
+        want = co.eval_serial(nodes, x)
+        for g in geoms:
+            assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, g)
