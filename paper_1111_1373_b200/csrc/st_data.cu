@@ -91,8 +91,12 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.record_regs = (g.record_regs == 1 || (g.record_regs == 0 && a == 8)) ? 1u : 0u;
 
   // the folded tree (leaf pairs inside terminals) serves the shared-tree TMA
-  // walks over 8/16/32-attribute records; every other path reads `compact`
-  const bool fold = t->fold_ok && (a == 8 || a == 16 || a == 32) &&
+  // walks over 8/16/32-attribute records of large trees; every other path
+  // reads `compact`.  Same-box A/B (profiles/r1_fold_ab.txt): C5 d12 -6 %,
+  // C1 -5 %, C5 d16 / d20 -3 / -2 %; on small trees the post-loop terminal
+  // step only lengthens each tile (C2 +4 %, C5 d8 +3 %), hence >= 2047 nodes.
+  const bool fold = t->fold_ok && t->nodes.size() >= 2047 && (a == 8 || a == 16 || a == 32) &&
+                    !env_u32("ST_DATA_NO_FOLD", 0) &&
                     (g.tree_loc == ST_TREE_AUTO || g.tree_loc == ST_TREE_SHARED) &&
                     tma_ok(x, m, a, ld, layout, ct_arity(a) ? choose_S(a, g.samples_per_thread) : 1);
   uint32_t tree_bytes = round1024((fold ? t->folded.size() : t->nodes.size()) * sizeof(CNode));
