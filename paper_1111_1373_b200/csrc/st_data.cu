@@ -95,7 +95,8 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // reads `compact`.  Same-box A/B (profiles/r1_fold_ab.txt): C5 d12 -6 %,
   // C1 -5 %, C5 d16 / d20 -3 / -2 %; on small trees the post-loop terminal
   // step only lengthens each tile (C2 +4 %, C5 d8 +3 %), hence >= 2047 nodes.
-  const bool fold = t->fold_ok && t->nodes.size() >= 2047 && (a == 8 || a == 16 || a == 32) &&
+  const bool fold = t->fold_ok && t->nodes.size() >= env_u32("ST_DATA_FOLD_MIN", 2047) &&
+                    (a == 8 || a == 16 || a == 32) &&
                     !env_u32("ST_DATA_NO_FOLD", 0) &&
                     (g.tree_loc == ST_TREE_AUTO || g.tree_loc == ST_TREE_SHARED) &&
                     tma_ok(x, m, a, ld, layout, ct_arity(a) ? choose_S(a, g.samples_per_thread) : 1);

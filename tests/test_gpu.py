@@ -359,11 +359,14 @@ def test_reference_acceptance_through_cpp_dropin(cuda):
     assert p.stdout.count("PASS") >= 5
 
 
-def test_folded_tree_walks(cuda, co):
+@pytest.mark.parametrize("fold_min", ["1", "1000000"])
+def test_folded_tree_walks(cuda, co, fold_min, monkeypatch):
     """Folded shared trees (leaf pairs inside terminal nodes) for 8/16/32-
     attribute records: all 626 exhaustive shapes (terminal roots, mixed
     pairs, ties on grid records) and 300 synthetic trees, through the
-    register walk and the shared-tile walk, against the oracles."""
+    register walk and the shared-tile walk, against the oracles -- with the
+    fold forced on for every tree size (ST_DATA_FOLD_MIN=1) and off."""
+    monkeypatch.setenv("ST_DATA_FOLD_MIN", fold_min)
     geoms = [st.GpuGeom(algo="data"), st.GpuGeom(algo="data", record_regs=2),
              st.GpuGeom(algo="data", record_regs=1, samples_per_thread=1)]
     for leaves in range(1, 9):
