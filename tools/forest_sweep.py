@@ -21,8 +21,11 @@ x = torch.from_numpy(st.generate_synthetic_dataset(m, 64, 499)).cuda()
 f = st.Forest(trees, 8)
 lab = torch.empty(m, dtype=torch.int32, device="cuda")
 res = []
-for u, nt, w in [(0, 0, 0)] + list(itertools.product([1, 2, 4], [0, 1, 2, 3], [0, 17, 25])):
-    env = {"ST_FOREST_U": u, "ST_FOREST_NT": (u + nt if nt else 0) if u else 0, "ST_FOREST_W": w}
+grid = [(0, 0, 0)] + [(u, u + k, w) for u, k, w in itertools.product([1, 2, 4], [1, 2, 3], [0, 17, 25])]
+if len(sys.argv) > 2 and sys.argv[2] == "deep":  # deeper rings at fewer consumer warps
+    grid = [(0, 0, 0)] + [(u, nt, 0) for u in (1, 2, 3, 4) for nt in range(u + 1, 11)]
+for u, nt, w in grid:
+    env = {"ST_FOREST_U": u, "ST_FOREST_NT": nt, "ST_FOREST_W": w}
     for k, v in env.items():
         os.environ[k] = str(v)
     try:
