@@ -37,7 +37,7 @@ _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 
 def build() -> None:
     """Build both oracle libraries (the reference one only if its sources exist)."""
-    subprocess.run(["make", "-s", "-C", HERE], check=True)
+    subprocess.run(["make", "-s", "-j4", "-C", HERE], check=True)
 
 
 class OracleError(RuntimeError):
