@@ -40,6 +40,7 @@ void launch_forest_u(uint32_t U, const Forest2Args& fa, const Staging& stg, size
                      cudaStream_t s) {
   if constexpr (S == 1 && A > 0 && A <= 64) {  // the transposed-tile walk takes U chains
     if (U >= 4) return launch_forest_smem<A, S, 4>(fa, stg, smem, dev, s);
+    if (U == 3) return launch_forest_smem<A, S, 3>(fa, stg, smem, dev, s);
     if (U == 2) return launch_forest_smem<A, S, 2>(fa, stg, smem, dev, s);
   }
   return launch_forest_smem<A, S, 1>(fa, stg, smem, dev, s);
@@ -61,14 +62,15 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   stg.stage_bytes = round1024(32ull * S * a * 4);
   // Geometry: U trees walked per lane at once (U dependent-load chains), a
   // ring of NT tree slots, and as many consumer warps as the rest of shared
-  // memory holds record tiles for.  The C4 sweep (profiles/r1_forest_sweep.json)
-  // put U = 2 with NT = U + 2 first (8.3 ms vs 10.3 ms for U = 1, NT = 2):
-  // the walk is bound by shared-memory wavefronts of the node loads, so more
-  // chains than that only add ring slots at the expense of record tiles.
+  // memory holds record tiles for.  With folded trees (~10 KB for C4) the
+  // sweep (profiles/r1_forest_sweep_fold.json) puts U = 3, NT = 6 first
+  // (7.76 ms; U = 2, NT = 4: 7.95 ms; unfolded U = 2, NT = 4: 8.33 ms): the
+  // walk is bound by shared-memory wavefronts of the node loads, so more
+  // chains only add ring slots at the expense of record tiles.
   const bool transposed = S == 1 && a <= 64 && ct_arity(a);
-  const uint32_t U = std::max<uint32_t>(1, std::min<uint32_t>(4, env_u32("ST_FOREST_U", transposed ? 2 : 1)));
+  const uint32_t U = std::max<uint32_t>(1, std::min<uint32_t>(4, env_u32("ST_FOREST_U", transposed ? 3 : 1)));
   uint32_t nt = env_u32("ST_FOREST_NT", 0);
-  if (nt == 0) nt = U + 2;
+  if (nt == 0) nt = U + 3;
   if (!transposed && U != 1) return false;
   stg.warps = 0;
   size_t fixed = 0;

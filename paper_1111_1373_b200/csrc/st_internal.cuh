@@ -401,6 +401,32 @@ inline bool compact_fits(uint32_t n, uint32_t max_attribute, uint32_t* abits) {
   return *abits < 31 && ((8ull * n) << *abits) < (1ull << 31);
 }
 
+// Folded compact layout: BFS, children adjacent, every internal node whose two
+// children are leaves becomes a terminal {thr, kLeafBit | kPairBit | classR <<
+// 20 | classL << 10 | 4*attr} and its leaf pair is dropped (classes < 1024,
+// 4*attr < 1024 are the caller's preconditions).  False when the folded array
+// would not shrink (DAG-shaped inputs) or not fit the compact child field.
+inline bool fold_tree(const st_node* nodes, uint32_t n, uint32_t abits, std::vector<CNode>& f) {
+  auto is_leaf = [&](uint32_t i) { return nodes[i].class_id != ST_NO_CLASS; };
+  std::vector<uint32_t> order{0};  // original index per folded slot
+  f.clear();
+  for (size_t k = 0; k < order.size() && order.size() <= 2ull * n; ++k) {
+    const st_node& nd = nodes[order[k]];
+    if (is_leaf(order[k])) {
+      f.push_back(CNode{nd.threshold, kLeafBit | nd.class_id});
+    } else if (is_leaf(nd.child) && is_leaf(nd.child + 1)) {
+      f.push_back(CNode{nd.threshold, kLeafBit | kPairBit | (nodes[nd.child + 1].class_id << 20) |
+                                          (nodes[nd.child].class_id << 10) | (4u * nd.attribute)});
+    } else {
+      const uint32_t fc = (uint32_t)order.size();  // children take the next two slots
+      f.push_back(CNode{nd.threshold, ((8u * fc) << abits) | (4u * nd.attribute)});
+      order.push_back(nd.child);
+      order.push_back(nd.child + 1);
+    }
+  }
+  return f.size() == order.size() && f.size() <= n && ((8ull * f.size()) << abits) < (1ull << 31);
+}
+
 inline std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
   validate_links(nodes, n, "tree");
   auto t = std::make_unique<st_tree>();
@@ -444,31 +470,9 @@ inline std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
     }
   }
   in.compact = t->compact_ok ? 1 : 0;
-  // Folded layout for the shared-tree data walk: BFS, children adjacent, every
-  // internal node whose two children are leaves becomes a terminal carrying
-  // both classes (kPairBit); its leaves are dropped.  Needs classes < 1024,
-  // 4*attr < 1024 and a compact encoding.
-  if (t->compact_ok && !t->leaf_table && in.max_class < 1024 && 4ull * in.max_attribute < 1024 && n > 1) {
-    auto is_leaf = [&](uint32_t i) { return nodes[i].class_id != ST_NO_CLASS; };
-    std::vector<uint32_t> order{0};  // original index per folded slot
-    std::vector<CNode>& f = t->folded;
-    f.clear();
-    for (size_t k = 0; k < order.size() && order.size() <= 2ull * n; ++k) {  // DAG inputs may not shrink
-      const st_node& nd = nodes[order[k]];
-      if (is_leaf(order[k])) {
-        f.push_back(CNode{nd.threshold, kLeafBit | nd.class_id});
-      } else if (is_leaf(nd.child) && is_leaf(nd.child + 1)) {
-        f.push_back(CNode{nd.threshold, kLeafBit | kPairBit | (nodes[nd.child + 1].class_id << 20) |
-                                            (nodes[nd.child].class_id << 10) | (4u * nd.attribute)});
-      } else {
-        const uint32_t fc = (uint32_t)order.size();  // children take the next two slots
-        f.push_back(CNode{nd.threshold, ((8u * fc) << t->abits) | (4u * nd.attribute)});
-        order.push_back(nd.child);
-        order.push_back(nd.child + 1);
-      }
-    }
-    t->fold_ok = f.size() == order.size() && f.size() <= n && ((8ull * f.size()) << t->abits) < (1ull << 31);
-  }
+  // Folded layout for the shared-tree data walk (fold_tree)
+  if (t->compact_ok && !t->leaf_table && in.max_class < 1024 && 4ull * in.max_attribute < 1024 && n > 1)
+    t->fold_ok = fold_tree(nodes, n, t->abits, t->folded);
   return t;
 }
 

@@ -1103,7 +1103,9 @@ __global__ void __launch_bounds__(kMaxThreads)
         nd = __ldg(reinterpret_cast<const uint2*>(
             tn + (nd.y >> args.abits) + (v > __uint_as_float(nd.x) ? 8u : 0u)));
       }
-      const uint32_t c = nd.y & ~kLeafBit;
+      uint32_t c = nd.y & ~kLeafBit;
+      if (nd.y & kPairBit)  // folded terminal
+        c = ((rec.get(nd.y & 0x3FFu) > __uint_as_float(nd.x)) ? (nd.y >> 20) : (nd.y >> 10)) & 0x3FFu;
       if constexpr (PACKED) {
         if (c < 4) h0 += 1u << (8 * c);
         else h1 += 1u << (8 * (c - 4));
@@ -1321,6 +1323,14 @@ __global__ void __launch_bounds__(kMaxThreads)
             for (int u = 0; u < U; ++u) forest_step(thr[u], meta[u], tb[u], soa, amask, args.abits);
           }
 #pragma unroll
+          for (int u = 0; u < U; ++u) {  // folded terminal: the last predicate picks the pair's leaf
+            if (meta[u] & kPairBit) {
+              const float v = lds_f32(soa + ((meta[u] & 0x3FFu) << 5));
+              const uint32_t c = (v > __uint_as_float(thr[u])) ? (meta[u] >> 20) : (meta[u] >> 10);
+              meta[u] = kLeafBit | (c & 0x3FFu);
+            }
+          }
+#pragma unroll
           for (int u = 0; u < U; ++u) {
             if ((uint32_t)u < nu) {
               const uint32_t c = meta[u] & ~kLeafBit;
@@ -1339,7 +1349,9 @@ __global__ void __launch_bounds__(kMaxThreads)
                 const float v = rec[q].get(nd.y & amask);
                 nd = lds_u2(tb[u] + (nd.y >> args.abits) + (v > __uint_as_float(nd.x) ? 8u : 0u));
               }
-              const uint32_t c = nd.y & ~kLeafBit;
+              uint32_t c = nd.y & ~kLeafBit;
+              if (nd.y & kPairBit)
+                c = ((rec[q].get(nd.y & 0x3FFu) > __uint_as_float(nd.x)) ? (nd.y >> 20) : (nd.y >> 10)) & 0x3FFu;
               if (c < 4) h0[q] += 1u << (8 * c);
               else h1[q] += 1u << (8 * (c - 4));
             }

@@ -286,12 +286,27 @@ def test_dag_shaped_input(cuda, co):
         assert np.array_equal(st.eval_gpu(nodes, x, g), want)
 
 
-def test_forest_variants(cuda, co):
+@pytest.mark.parametrize("no_fold", ["0", "1"])
+def test_forest_variants(cuda, co, no_fold, monkeypatch):
+    """Shared-memory ring (<= 8 classes, <= 255 trees) and the L1 fallback,
+    aligned (TMA) and unaligned / SoA-less record views, trees folded (leaf
+    pairs in terminal nodes) or not, against the oracle vote."""
+    monkeypatch.setenv("ST_FOREST_NO_FOLD", no_fold)
     x = co.gen_dataset(7001, 12, 9)
     for t_count, classes in ((1, 3), (7, 8), (300, 5), (9, 40)):
         trees = [co.gen_tree(7, 40, 12, classes, 50 + t) for t in range(t_count)]
         want = co.eval_forest(trees, x, classes)
-        assert np.array_equal(st.eval_forest(st.Forest(trees, classes), x), want), (t_count, classes)
+        f = st.Forest(trees, classes)
+        assert np.array_equal(st.eval_forest(f, x), want), (t_count, classes)
+        xd = torch.from_numpy(x[1:]).cuda()  # odd base address: no TMA, warp-stored tiles
+        out = torch.empty(len(x) - 1, dtype=torch.int32, device="cuda")
+        st.eval_forest_device(f, xd, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), want[1:]), (t_count, classes)
+    for a in (8, 16, 64):  # compile-time arities of the transposed-tile walk
+        trees = [co.gen_tree(9, 100, a, 8, 900 + t) for t in range(11)]
+        xa = co.gen_dataset(3001, a, 77)
+        assert np.array_equal(st.eval_forest(st.Forest(trees, 8), xa), co.eval_forest(trees, xa, 8)), a
     with pytest.raises(st.ArgumentError):
         st.Forest([co.gen_tree(7, 40, 12, 9, 1)], 4)  # class >= n_classes
 

@@ -49,12 +49,14 @@ def main():
     ap.add_argument("--depths", default="8,10,12,14,16,18,20")
     args = ap.parse_args()
     G, S = args.gpus, args.shards
+    ndev = torch.cuda.device_count()
+    dv = lambda g: g % ndev  # noqa: E731  (more shard owners than GPUs: validation runs only)
     peak, _ = bench.peaks()
     own = [(g * S // G, (g + 1) * S // G) for g in range(G)]
     xs, labs, streams = [], [], []
     t_gen = time.perf_counter()
     for g, (lo, hi) in enumerate(own):
-        dev = torch.device("cuda", g)
+        dev = torch.device("cuda", dv(g))
         xs.append(torch.empty(((hi - lo) * SHARD, A), dtype=torch.float32, device=dev))
         labs.append(torch.empty((hi - lo) * SHARD, dtype=torch.int32, device=dev))
         streams.append(torch.cuda.Stream(device=dev))
@@ -81,14 +83,14 @@ def main():
                 f.result()
                 g = owner[s]
                 lo = own[g][0]
-                with torch.cuda.device(g):
+                with torch.cuda.device(dv(g)):
                     xs[g][(s - lo) * SHARD:(s - lo + 1) * SHARD].copy_(buf)  # synchronous
                 free.append(buf)
     t_gen = time.perf_counter() - t_gen
     print(f"generated {S} shards ({S * SHARD * A * 4 / 1e9:.1f} GB) in {t_gen:.1f} s", flush=True)
     labels_host = torch.empty(S * SHARD, dtype=torch.int32, pin_memory=True)
 
-    out = {"gpus": G, "shards": S, "records": S * SHARD, "arity": A, "peak_GBs": peak,
+    out = {"gpus": G, "devices_used": min(G, ndev), "shards": S, "records": S * SHARD, "arity": A, "peak_GBs": peak,
            "device": torch.cuda.get_device_name(0), "generation_s": t_gen, "depths": {}}
     for D in [int(d) for d in args.depths.split(",")]:
         tree = st.generate_synthetic_tree(D, min(2 ** D, 4096), A, 8, 500 + D)
@@ -99,7 +101,7 @@ def main():
             def launch_all():
                 evs = []
                 for g in range(G):
-                    with torch.cuda.device(g):
+                    with torch.cuda.device(dv(g)):
                         e0 = torch.cuda.Event(enable_timing=True)
                         e1 = torch.cuda.Event(enable_timing=True)
                         e0.record(streams[g])
@@ -107,7 +109,7 @@ def main():
                         e1.record(streams[g])
                         evs.append((e0, e1))
                 for g in range(G):
-                    torch.cuda.synchronize(g)
+                    torch.cuda.synchronize(dv(g))
                 return max(a.elapsed_time(b) for a, b in evs) / 1e3
 
             launch_all()  # warm (device tree / window tables)
@@ -127,7 +129,7 @@ def main():
             labels_host[off:off + n].copy_(labs[g], non_blocking=True)
             off += n
         for g in range(G):
-            torch.cuda.synchronize(g)
+            torch.cuda.synchronize(dv(g))
         row["label_gather_s"] = time.perf_counter() - g0
         row["spec_over_data_time"] = row["speculative"]["s"] / row["data"]["s"]
         out["depths"][f"d{D}"] = row
