@@ -138,7 +138,9 @@ def main():
     spec_g2 = ("speculative-G2", st.GpuGeom(algo="speculative", group_lanes=2))
     spec_g8 = ("speculative-G8", st.GpuGeom(algo="speculative", group_lanes=8))
     spec_g16 = ("speculative-G16", st.GpuGeom(algo="speculative", group_lanes=16))
-    geoms = [data_g, spec_g, spec_g2, spec_g8, spec_g16]
+    data_const = ("data-constant-tree", st.GpuGeom(algo="data", tree_loc="constant"))
+    data_glob = ("data-global-tree", st.GpuGeom(algo="data", tree_loc="global"))
+    geoms = [data_g, data_const, data_glob, spec_g, spec_g2, spec_g8, spec_g16]
     out = {"peak_GBs": PEAK, "device": torch.cuda.get_device_name(0), "flush": FLUSH_MODE}
     W = bench.WORKLOADS
     for name in ("C1", "C2", "C3"):
