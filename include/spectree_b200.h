@@ -73,19 +73,21 @@ enum st_tree_loc {
 typedef struct st_geom {
   uint32_t algo;               /* st_algo */
   uint32_t tree_loc;           /* st_tree_loc (data kernel) */
-  uint32_t samples_per_thread; /* data kernel: independent walks per lane (0 = auto) */
+  uint32_t samples_per_thread; /* data kernel: independent walks per lane (0 = auto);
+                                  speculative ring: record streams per group, 1 or 2 (0 = auto) */
   uint32_t group_lanes;        /* speculative: lanes per record group, power of two <= 32 (0 = auto) */
   uint32_t window_levels;      /* speculative: max window height in tree levels (0 = auto) */
   uint32_t reductions;         /* speculative: 0 = fixed per-window doubling count;
                                   k >= 1 = check the root after every k doublings
                                   (reference ReductionMode::barrier_separated, k = reductions_per_iteration) */
   uint32_t blocks_per_sm;      /* 0 = occupancy-derived persistent grid */
-  uint32_t stages;             /* TMA record-pipeline stages per warp (0 = auto, 2-4) */
+  uint32_t stages;             /* TMA record-pipeline stages per warp (0 = auto, 1-8) */
   uint32_t warps_per_cta;      /* CTA width in warps, 1-32 (0 = auto) */
-  uint32_t pipeline;           /* record staging: 0 = auto, 1 = per-warp TMA ring,
-                                  2 = CTA-shared TMA ring with a producer warp (speculative) */
-  uint32_t record_regs;         /* data kernel, 8-attribute records: 0 = auto, 1 = walk from
-                                  registers (tile released right after loading), 2 = shared tile */
+  uint32_t pipeline;           /* speculative record staging: 0 = auto (CTA-shared ticketed TMA
+                                  ring), 1 = per-warp TMA ring */
+  uint32_t record_regs;        /* data kernel, 8/16-attribute records: 0 = auto (registers for 8),
+                                  1 = walk from registers (tile released right after loading),
+                                  2 = walk from the shared tile */
   uint32_t reserved[1];
 } st_geom;
 
