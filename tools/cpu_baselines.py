@@ -2,8 +2,9 @@
 host cores of the box it runs on: the reference's own eval_serial on ONE
 pinned core and eval_data_parallel on ALL cores (workers = os_threads = nproc,
 chunk = ceil(M / nproc)), over bounded samples of the same records
-(oracle/_ref = the reference compiled from its unmodified sources).  The
-rates extrapolate linearly to the full configuration (records are
+(oracle/_ref = the reference compiled from its unmodified sources); 2
+warm-up runs, then the mean and best of >= 5 timed runs.  The rates
+extrapolate linearly to the full configuration (records are
 independent).  C4 times all 128 trees' eval_serial on the sample (the vote is
 ours and negligible).  Writes gpurun_out/cpu_baselines.json.
 
@@ -26,14 +27,16 @@ import oracle  # noqa: E402
 
 
 def rate(fn, n, seconds):
-    fn()  # warm
-    done, t0 = 0, time.perf_counter()
-    while True:
+    """SURVEY 8d: 2 warm-up runs, then >= 5 timed runs (more until `seconds`);
+    returns (mean rate, best rate) in records/s."""
+    for _ in range(2):
         fn()
-        done += n
-        if time.perf_counter() - t0 >= seconds:
-            break
-    return done / (time.perf_counter() - t0)
+    ts, t_all = [], time.perf_counter()
+    while len(ts) < 5 or time.perf_counter() - t_all < seconds:
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return n * len(ts) / sum(ts), n / min(ts)
 
 
 def pin_one():
@@ -49,10 +52,11 @@ def measure(ref, trees, x, seconds, cores):
         handles = [ref.tree(t) for t in trees]
         try:
             allc = pin_one()
-            out["serial_1core"] = rate(lambda: [h.eval_serial(d) for h in handles], m, seconds)
+            out["serial_1core"], out["serial_1core_best"] = rate(
+                lambda: [h.eval_serial(d) for h in handles], m, seconds)
             os.sched_setaffinity(0, set(allc))
             chunk = -(-m // cores)
-            out["data_parallel_all_cores"] = rate(
+            out["data_parallel_all_cores"], out["data_parallel_all_cores_best"] = rate(
                 lambda: [h.eval_data_parallel(d, cores, chunk, os_threads=cores) for h in handles], m, seconds)
         finally:
             for h in handles:
