@@ -228,9 +228,10 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
                            (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128;
       // record streams per group (samples_per_thread): two independent
       // window chains per lane pay off on large trees, where a record walks
-      // many windows (C5 d16: 0.61 vs 0.68 ms), and cost a little on small
-      // ones (C2: 0.399 vs 0.390 ms; profiles/r1_sweep_*_spec2d.json)
-      const uint32_t sr = g.samples_per_thread ? g.samples_per_thread : (t->info.internal > 1024 ? 2u : 1u);
+      // many windows (C5 d16: 0.61 vs 0.68 ms; C1, 1023 internal nodes: 0.038
+      // vs 0.040 ms), and cost a little on small ones (C2, 255: 0.399 vs
+      // 0.390 ms; profiles/r1_sweep_*_spec2d.json, *_spec2e.json)
+      const uint32_t sr = g.samples_per_thread ? g.samples_per_thread : (t->info.internal > 511 ? 2u : 1u);
       switch (ct_arity(a) ? a : 0) {
         case 8: return launch_spec_ring<8>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
         case 16: return launch_spec_ring<16>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
