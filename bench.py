@@ -437,13 +437,167 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+FOREST = dict(desc="random forest of 128 depth-12 trees, 64 float32 attributes, 8M samples per GPU, "
+                   "majority-vote labels", trees=[(12, 1024, 64, 8, 401 + t) for t in range(128)],
+              m=8_000_000, a=64, seed=499, classes=8, labels_fnv=0x1b2543c41e436ce0)
+
+
+def run_forest(args):
+    """--workload C4 (BASELINE configs[3]): one step = the 128-tree forest vote
+    over the rank's 8M records; same timing rules as run_ours.  The forest is
+    shared-memory bound, so `roofline` reports the HBM fraction for the record
+    bytes (4*A per sample) beside node visits/s."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1111_1373_b200 as st
+
+    world, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.backend)
+    F = FOREST
+    m, a = F["m"], F["a"]
+    forest = st.Forest([st.generate_synthetic_tree(*t) for t in F["trees"]], F["classes"])
+    x_host = torch.empty((m, a), dtype=torch.float32, pin_memory=True)
+    st.generate_synthetic_dataset(m, a, F["seed"] + 1000 * rank, out=x_host.numpy())
+    x_dev = x_host.to(dev)
+    labels = torch.empty(m, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    st.eval_forest_device(forest, x_dev, labels, stream=stream)
+    torch.cuda.synchronize()
+    labels_ok = (st.fnv1a64(labels.cpu().numpy()) == F["labels_fnv"]) if rank == 0 else None
+    steps = max(1, min(args.steps, 50))
+    for _ in range(args.warmup):
+        st.eval_forest_device(forest, x_dev, labels, stream=stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    c0 = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(steps):
+        st.eval_forest_device(forest, x_dev, labels, stream=stream)
+        launches += st.last_launch_count()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    c1 = time.perf_counter()
+    barrier()
+    torch.cuda.synchronize()
+    t_local = ev0.elapsed_time(ev1) / 1e3
+    t_max = t_local
+    if world > 1:
+        t = torch.tensor([t_local], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max = float(t.item())
+    sampler.stop_ev.set()
+    clocks = sampler.summary(c0, c1)
+    # end to end: pinned host records -> H2D -> forest -> D2H votes (st_forest_eval)
+    e_steps = max(1, args.e2e_steps)
+    xnp = x_host.numpy()
+    st.eval_forest(forest, xnp)
+    barrier()
+    e0 = time.perf_counter()
+    for _ in range(e_steps):
+        st.eval_forest(forest, xnp)
+    e_local = time.perf_counter() - e0
+    e_max = e_local
+    if world > 1:
+        t = torch.tensor([e_local], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_max = float(t.item())
+    peak, peak_src = peaks()
+    kernel_s = t_local / steps
+    achieved = 4.0 * a * m / kernel_s / 1e9
+    line = {
+        "metric": METRIC, "value": world * m * steps / t_max, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": t_max / steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: reference generators (128 trees + records), canonical seeds",
+        "config": {"workload": f"C4: {F['desc']}", "trees": "generate_synthetic_tree(12, 1024, 64, 8, 401+t), t<128",
+                   "records_per_gpu": m, "arity": a, "layout": "AoS float32", "algo": "forest vote (k_forest_smem)",
+                   "parallelism": f"sample-sharded x{world} (weak), forest replicated, no collective",
+                   "l2": f"inputs {4 * a * m / 1e9:.2f} GB/GPU > L2 126 MB: no flush needed"},
+        "labels_match_reference_hash": {"forest_vote": labels_ok} if rank == 0 else None,
+        "roofline": {"bound": "smem (node loads); hbm fraction reported", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": 4.0 * a * m, "kernel_ms": kernel_s * 1e3},
+        "e2e": {"value": world * m * e_steps / e_max, "unit": UNIT, "h2d_bytes_per_step": 4 * a * m,
+                "d2h_bytes_per_step": 4 * m, "steps": e_steps, "api": "st_forest_eval (host pinned buffers)"},
+        "clocks": clocks, "gpu_launches": launches,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference_forest(args):
+    """Reference arm for C4: the reference has no forest, so one
+    step is its own eval_data_parallel (all host cores) for each of the 128
+    trees over a bounded sample, plus the vote (numpy bincount argmax)."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    F = FOREST
+    impl, kind = _ref_or_port()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    sample = min(F["m"], max(1000, args.ref_sample // 20))
+    x = impl.gen_dataset(sample, F["a"], F["seed"])
+    trees = [impl.gen_tree(*t) for t in F["trees"]]
+    chunk = -(-sample // cores)
+
+    if kind != "reference":
+        raise SystemExit("C4 reference arm needs oracle/_ref")
+    handles = [impl.tree(nodes) for nodes in trees]  # tree construction outside the timed steps
+    data = impl.data(x)
+    rows = np.arange(sample)
+
+    def step():
+        votes = np.zeros((sample, F["classes"]), np.uint32)
+        for t in handles:
+            votes[rows, t.eval_data_parallel(data, cores, chunk, os_threads=cores)] += 1
+        return votes.argmax(axis=1)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    value = sample * args.steps / el
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: reference generators, canonical seeds",
+        "config": {"workload": f"C4: {F['desc']}", "records_per_step": sample, "arity": F["a"],
+                   "algo": "128 x spectree::eval_data_parallel (CPU threads) + vote"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"first {sample} records of C4 per step, 128 trees", "cpu": _cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["C4"], default="C2")
     ap.add_argument("--algo", choices=["auto", "data", "speculative"], default="auto")
     ap.add_argument("--alt-steps", type=int, default=200,
                     help="timed steps for the non-headline algorithm in by_algorithm")
@@ -457,7 +611,12 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)  # timing rule: >= 3 untimed warm-up steps
     if args.impl == "reference":
+        if args.workload == "C4":
+            run_reference_forest(args)
+            return
         run_reference(args)
+    elif args.workload == "C4":
+        run_forest(args)
     else:
         run_ours(args)
 

@@ -13,12 +13,19 @@ import paper_1111_1373_b200 as st  # noqa: E402
 
 var, vals = sys.argv[1], sys.argv[2].split(",")
 tile = 1
+flush = False
 names = []
 for a in sys.argv[3:]:
     if a.startswith("--tile="):
         tile = int(a.split("=")[1])
+    elif a == "--flush":
+        flush = True
     else:
         names.append(a)
+if flush:
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import workloads  # noqa: E402
+    fl = workloads.make_flush()
 for name in names:
     w = bench.WORKLOADS[name]
     tree = st.generate_synthetic_tree(*w["tree"])
@@ -32,6 +39,9 @@ for name in names:
     for rep in range(3):
         for v in vals:
             os.environ[var] = v
+            if flush:  # L2 read-flushed graph replay (tools/workloads.py)
+                res[v].append(round(workloads.graph_time(lambda: st.eval_device(tree, xd, out, g), 20, fl), 5))
+                continue
             for _ in range(3):
                 st.eval_device(tree, xd, out, g)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
