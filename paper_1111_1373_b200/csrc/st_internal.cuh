@@ -127,6 +127,12 @@ struct WinTable {
   uint32_t root_code = 0;
   uint32_t windows = 0;
   uint32_t max_steps = 0;
+  // One-window trees: entries[pm_off + j] = path mask of leaf j
+  // {thr = 0, attr_steps = leaf code, left = care, right = want}: bits of the
+  // window lanes on the root-to-leaf path and their right-turn directions.
+  // Unused lanes carry code 0.  pm_off 0 = none (more windows, more leaves
+  // than lanes, or a DAG-shaped input).
+  uint32_t pm_off = 0;
 };
 
 }  // namespace sti
@@ -275,7 +281,39 @@ struct st_tree {
     }
     wt.root_code = kExitBit | 0u;
     wt.windows = nw;
+    if (nw == 1) add_path_masks(wt, members[0], G);
     return wt;
+  }
+
+  // Path masks of a one-window tree (ballot reduction, k_spec_ring SR == 0):
+  // leaf l is reached iff ((preds ^ want_l) & care_l) == 0, preds = the
+  // window lanes' predicate bits (1 = right, the reference's x > thr).
+  void add_path_masks(WinTable& wt, const std::vector<uint32_t>& mem, uint32_t G) const {
+    if (mem.size() > 32) return;
+    std::vector<int32_t> lane_of(nodes.size(), -1);
+    for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = (int32_t)j;
+    std::vector<uint8_t> seen(nodes.size(), 0);
+    std::vector<SEntry> pm;
+    struct Item { uint32_t node, care, want; };
+    std::vector<Item> stack{{0u, 0u, 0u}};
+    while (!stack.empty()) {
+      const Item it = stack.back();
+      stack.pop_back();
+      if (seen[it.node]++) return;  // reached twice: DAG-shaped input
+      if (is_leaf(it.node)) {
+        pm.push_back(SEntry{0.0f, kLeafBit | leaf_code[it.node], it.care, it.want});
+        continue;
+      }
+      const int32_t j = lane_of[it.node];
+      if (j < 0) return;
+      const uint32_t bit = 1u << j;
+      stack.push_back({nodes[it.node].child, it.care | bit, it.want});
+      stack.push_back({nodes[it.node].child + 1, it.care | bit, it.want | bit});
+    }
+    if (pm.size() > G) return;
+    wt.pm_off = (uint32_t)wt.entries.size();
+    pm.resize(32, SEntry{0.0f, 0u, 0u, 0u});  // unused lanes: code 0, never stored
+    wt.entries.insert(wt.entries.end(), pm.begin(), pm.end());
   }
 
   Dev& device(int d) {

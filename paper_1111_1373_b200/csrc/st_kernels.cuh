@@ -629,6 +629,7 @@ struct SpecArgs {
   uint32_t* iters;       // EXACT path: per-record counters
   uint32_t* steps;
   uint32_t ns, win_bytes, stage_bytes;
+  uint32_t pm_off;       // k_spec_ring SR == 0: path-mask entries (0 = pointer jumping)
 };
 
 // Window codes: lane index (< 32), kExitBit | byte offset of the next
@@ -883,6 +884,14 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + 16u * j;
   const char* wglob = reinterpret_cast<const char*>(args.win) + 16u * j;
   if constexpr (WIN_SHARED) __syncthreads();  // window table staged
+  // SR == 0: the whole tree is one window (the paper's Proc. 5 geometry):
+  // each lane's entry is the same for every record -- load it once.
+  uint4 e1 = make_uint4(0u, 0u, 0u, 0u), pm1 = make_uint4(0u, 0u, 0u, 0u);
+  if constexpr (SR == 0) {
+    static_assert(SR != 0 || WIN_SHARED, "one-window path stages its table in shared memory");
+    e1 = lds_u4(jaddr);
+    if (args.pm_off) pm1 = lds_u4(sbase + 16u * (args.pm_off + j));
+  }
 
   while (true) {
     uint32_t tk = 0;
@@ -916,6 +925,57 @@ __global__ void __launch_bounds__(kMaxThreads)
     if (args.root_code & kLeafBit) {  // N == 1
       if (lane < rows)
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * lane), "r"(args.root_code) : "memory");
+    } else if constexpr (SR == 0) {
+      // One window: every record resolves in one pass, so the passes over
+      // the tile's records are independent chains (feature load -> compare
+      // -> doubling shuffles -> root) the compiler interleaves.  Rows past a
+      // partial tile's end re-read the last row and are never stored.
+      const uint32_t thr = e1.x, attr4 = e1.y & 0x00FFFFFFu;
+      auto feature = [&](uint32_t r) {
+        const uint32_t rr = r < rows ? r : rows - 1u;
+        if constexpr (Rec<A, kTma>::kRowLocal) {
+          const uint32_t ra4 = rr * (4u * (uint32_t)A), rowb = ra4 & ~127u;
+          return lds_f32(attr4 ^ ((tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u))));
+        } else {
+          Rec<A, kTma> rec;
+          rec.init(tile, rr, args.p.a, args.p.x, 0, 0, 0);
+          return rec.get(attr4);
+        }
+      };
+      if (args.pm_off) {
+        // Ballot reduction: one vote gathers every lane's predicate (the
+        // same speculation), and the lane whose leaf path mask matches --
+        // exactly one per group in a tree -- stores its class.  No shuffles.
+        const uint32_t gsh = g * G;
+#pragma unroll 4
+        for (uint32_t r = g; r < 32u; r += NG) {
+          const float v = feature(r);
+          const uint32_t preds = __ballot_sync(0xffffffffu, v > __uint_as_float(thr)) >> gsh;
+          if (pm1.y != 0u && ((preds ^ pm1.w) & pm1.z) == 0u && r < rows)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(pm1.y) : "memory");
+        }
+      } else {
+#pragma unroll 4
+        for (uint32_t r = g; r < 32u; r += NG) {
+          const float v = feature(r);
+          uint32_t c = (v > __uint_as_float(thr)) ? e1.w : e1.z;
+          if constexpr (STEPS >= 0) {
+#pragma unroll
+            for (int st = 0; st < STEPS; ++st) {
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              c = (c < 32u) ? u : c;
+            }
+          } else {
+            for (uint32_t st = 0; st < args.smax; ++st) {
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              c = (c < 32u) ? u : c;
+            }
+          }
+          const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
+          if (j == 0 && r < rows)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(root) : "memory");
+        }
+      }
     } else if constexpr (SR == 1) {
       // One record stream per group: the lean loop.  A group whose rows are
       // exhausted keeps re-walking its last record (finite, never stored):
@@ -1023,7 +1083,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         }
       } while (__any_sync(0xffffffffu, aA || aB));
     } else {
-      static_assert(SR == 1 || SR == 2, "one or two record streams per group");
+      static_assert(SR >= 0 && SR <= 2, "one window, or one or two record streams per group");
     }
     __syncwarp();
     if (tk + NS < my_tiles) {

@@ -55,6 +55,20 @@ void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg
 template <int A>
 void launch_spec_ring(bool ws, uint32_t sr, const SpecRingArgs& ra, const Staging& stg, size_t smem,
                       int dev, uint32_t warps, cudaStream_t s) {
+  // the whole tree in one window (sr == 0): hoisted entry, independent
+  // passes, the doubling count (<= 5 for <= 32 lanes) always compile-time so
+  // the passes interleave
+  if (sr == 0 && ws && ra.s.smax <= 5) {
+    switch (ra.s.smax) {
+      case 0: return launch_spec_ring_k<A, true, 0, 0>(ra, stg, smem, dev, warps, s);
+      case 1: return launch_spec_ring_k<A, true, 1, 0>(ra, stg, smem, dev, warps, s);
+      case 2: return launch_spec_ring_k<A, true, 2, 0>(ra, stg, smem, dev, warps, s);
+      case 3: return launch_spec_ring_k<A, true, 3, 0>(ra, stg, smem, dev, warps, s);
+      case 4: return launch_spec_ring_k<A, true, 4, 0>(ra, stg, smem, dev, warps, s);
+      default: return launch_spec_ring_k<A, true, 5, 0>(ra, stg, smem, dev, warps, s);
+    }
+  }
+  if (sr == 0) sr = 1;
 #define ST_RING(WSV, ST) return launch_spec_ring_sr<A, WSV, ST>(sr, ra, stg, smem, dev, warps, s)
   if (ws) {
     switch (ra.s.smax) {
@@ -231,7 +245,12 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       // many windows (C5 d16: 0.61 vs 0.68 ms; C1, 1023 internal nodes: 0.038
       // vs 0.040 ms), and cost a little on small ones (C2, 255: 0.399 vs
       // 0.390 ms; profiles/r1_sweep_*_spec2d.json, *_spec2e.json)
-      const uint32_t sr = g.samples_per_thread ? g.samples_per_thread : (t->info.internal > 511 ? 2u : 1u);
+      uint32_t sr = g.samples_per_thread ? g.samples_per_thread : (t->info.internal > 511 ? 2u : 1u);
+      if (wt->windows == 1 && win_shared && !env_u32("ST_SPEC_NO_ONEWIN", 0)) {
+        sr = 0;  // whole tree in one window
+        // ballot + leaf path masks unless pointer jumping is asked for
+        ra.s.pm_off = env_u32("ST_SPEC_ONEWIN_JUMP", 0) ? 0u : wt->pm_off;
+      }
       switch (ct_arity(a) ? a : 0) {
         case 8: return launch_spec_ring<8>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
         case 16: return launch_spec_ring<16>(win_shared, sr, ra, stg, rsmem, dev, warps, s);

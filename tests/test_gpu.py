@@ -407,3 +407,38 @@ def test_folded_tree_walks(cuda, co, fold_min, monkeypatch):
         want = co.eval_serial(nodes, x)
         for g in geoms:
             assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, g)
+
+
+@pytest.mark.parametrize("mode", ["ballot", "jump", "general"])
+def test_single_window_speculation(cuda, co, mode, monkeypatch):
+    """Trees with <= 32 internal nodes speculate as one window (the paper's
+    Proc. 5 geometry): the one-window ring path with the ballot + leaf
+    path-mask reduction (default), with pointer jumping
+    (ST_SPEC_ONEWIN_JUMP=1), and the general window loop
+    (ST_SPEC_NO_ONEWIN=1), against the oracles -- all exhaustive shapes up to
+    8 leaves, and random small trees over row-local, odd and wide arities
+    with ragged record counts."""
+    monkeypatch.setenv("ST_SPEC_NO_ONEWIN", "1" if mode == "general" else "0")
+    monkeypatch.setenv("ST_SPEC_ONEWIN_JUMP", "1" if mode == "jump" else "0")
+    geoms = [st.GpuGeom(algo="speculative"), st.GpuGeom(algo="speculative", group_lanes=32),
+             st.GpuGeom(algo="speculative", group_lanes=16)]
+    for leaves in range(1, 9):
+        for shape in support.all_shapes(leaves):
+            internal = support.assign_labels(shape)
+            x = support.grid_records(internal)
+            tree = encode_breadth_first(shape)
+            want = support.recursive_oracle(shape, x)
+            reps = -(-300 // len(x))
+            xt = np.tile(x, (reps, 1))
+            for g in geoms:
+                assert np.array_equal(st.eval_gpu(tree, xt, g), np.tile(want, reps)), (leaves, g)
+    for seed in range(1, 121):
+        a = (8, 16, 32, 19, 64, 3)[seed % 6]
+        depth = 2 + seed % 9
+        leaves = min(max(depth + 1, 2 + seed % 32), 2 ** depth, 33)
+        nodes = co.gen_tree(depth, leaves, a, 2 + seed % 7, seed)
+        m = (1, 31, 33, 1000, 4097, 20011)[seed % 6]
+        x = co.gen_dataset(m, a, seed + 9000, gaussian=(seed % 2 == 0))
+        want = co.eval_serial(nodes, x)
+        for g in geoms:
+            assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, m, g)

@@ -151,6 +151,18 @@ def main():
         x = st.generate_synthetic_dataset(w["m"], w["a"], w["seed"])
         div, unit = (w["m"], "frames/s") if name == "C3" else (1.0, "samples/s")
         out[name] = run_tree(name, tree, x, w["labels_fnv"], geoms, args.iters, div, unit)
+    if "PAPER" in only or "C1" in only:
+        # the paper's own workload (main.cpp:233-246): tree(11,16,19,7,1) with
+        # 15 internal nodes -> one speculative window on 16 lanes (Proc. 5)
+        tree = st.generate_synthetic_tree(11, 16, 19, 7, 1)
+        x = np.tile(st.generate_synthetic_dataset(16384, 19, 2), (4, 1))
+        out["paper"] = run_tree("paper", tree, x, 0xc90f17638d0c1525,
+                                [data_g, spec_g, ("speculative-G32", st.GpuGeom(algo="speculative", group_lanes=32))],
+                                args.iters)
+        x = np.tile(x, (256, 1))  # 16.8M records: out of L2, HBM-scale
+        out["paper_x256"] = run_tree("paper_x256", tree, x, None,
+                                     [data_g, spec_g, ("speculative-G4-windows", st.GpuGeom(algo="speculative", group_lanes=4)),
+                                      ("speculative-G2-windows", st.GpuGeom(algo="speculative", group_lanes=2))], args.iters)
     if "C3" in only:
         # video stream: 32 frames (2.1 GB) per launch -> frames/s at HBM scale
         w = W["C3"]
