@@ -1,5 +1,6 @@
 """One small launch of every kernel family (data: shared/global/constant tree,
-S = 1/2/4; speculative: ring, per-warp, EXACT shfl, EXACT CTA; forest), labels
+S = 1/2/4; speculative: ring, one-window ballot / jump, per-warp, EXACT shfl, EXACT CTA;
+forest), labels
 checked against the C oracle -- the target for compute-sanitizer
 (memcheck / racecheck / synccheck):
 
@@ -39,6 +40,15 @@ for targs, a in cases:
         if not np.array_equal(got, want):
             bad += 1
             print("MISMATCH", targs, g)
+    # one-window trees: the pointer-jumping variant of the one-window path too
+    os.environ["ST_SPEC_ONEWIN_JUMP"] = "1"
+    out = torch.empty(len(x), dtype=torch.int32, device="cuda")
+    st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative"))
+    torch.cuda.synchronize()
+    del os.environ["ST_SPEC_ONEWIN_JUMP"]
+    if not np.array_equal(out.cpu().numpy().view(np.uint32), want):
+        bad += 1
+        print("MISMATCH one-window jump", targs)
     it = torch.empty(len(x), dtype=torch.int32, device="cuda")
     sp = torch.empty(len(x), dtype=torch.int32, device="cuda")
     out = torch.empty(len(x), dtype=torch.int32, device="cuda")
