@@ -59,9 +59,116 @@ bool is_pinned_or_device(const void* p) {
          at.type == cudaMemoryTypeManaged;
 }
 
+// Host worker threads for packing pageable records into pinned staging: the
+// driver's own pageable H2D stages through one thread (~11 GB/s on the B200
+// boxes); several threads copying into pinned buffers keep PCIe busy.  Jobs
+// from concurrent callers share the workers; the caller runs part 0 itself.
+class HostCopyPool {
+ public:
+  static HostCopyPool& get() {
+    static HostCopyPool* p = new HostCopyPool();  // intentionally leaked (detached workers)
+    return *p;
+  }
+  int width() const { return (int)workers_ + 1; }
+  // fn(i) for i in [0, n); returns when all parts are done.  Parts are
+  // claimed from a shared counter by the caller and up to n - 1 woken
+  // workers, so a descheduled worker delays at most the part it holds.
+  void run(int n, const std::function<void(int)>& fn) {
+    if (n <= 1 || workers_ == 0) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    struct Job {
+      std::atomic<int> next{0}, done{0};
+      int n = 0;
+      std::mutex mu;
+      std::condition_variable cv;
+    };
+    auto job = std::make_shared<Job>();
+    job->n = n;
+    const std::function<void(int)>* f = &fn;  // valid while any part is unclaimed
+    auto work = [job, f] {
+      for (int i; (i = job->next.fetch_add(1)) < job->n;) {
+        (*f)(i);
+        if (job->done.fetch_add(1) + 1 == job->n) {
+          std::lock_guard<std::mutex> lk(job->mu);
+          job->cv.notify_all();
+        }
+      }
+    };
+    const int helpers = std::min<int>((int)workers_, n - 1);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (int h = 0; h < helpers; ++h) q_.emplace_back(work);
+    }
+    if (helpers == 1) cv_.notify_one();
+    else cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(job->mu);
+    job->cv.wait(lk, [&] { return job->done.load() == job->n; });
+  }
+
+ private:
+  HostCopyPool() {
+    const uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
+    workers_ = env_u32("ST_HOST_COPY_THREADS", std::min(16u, hw)) - 1u;
+    if (workers_ > 63) workers_ = 0;  // ST_HOST_COPY_THREADS=0 -> single-threaded
+    for (uint32_t i = 0; i < workers_; ++i)
+      std::thread([this] {
+        for (;;) {
+          std::function<void()> task;
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return !q_.empty(); });
+            task = std::move(q_.front());
+            q_.pop_front();
+          }
+          task();
+        }
+      }).detach();
+  }
+  uint32_t workers_ = 0;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::function<void()>> q_;
+};
+
+// Pack records [r0, r0 + rows) of host x into dst as the dense device layout
+// the kernels get from the host path (AoS: rows x a; SoA: a columns of rows),
+// split over the copy pool (byte ranges of a contiguous block, else row ranges).
+void pack_records(void* dst, const float* x, uint64_t r0, uint64_t rows, uint32_t a, uint64_t ld,
+                  int layout) {
+  HostCopyPool& pool = HostCopyPool::get();
+  const uint64_t row_bytes = (uint64_t)a * 4;
+  const uint64_t bytes = rows * row_bytes;
+  // ~512 KB parts, claimed dynamically by the pool's threads
+  const int parts = (int)std::max<uint64_t>(1, std::min<uint64_t>(4096, bytes >> 19));
+  char* d = static_cast<char*>(dst);
+  if (layout == ST_LAYOUT_AOS && ld == a) {
+    const char* src = reinterpret_cast<const char*>(x + r0 * a);
+    const uint64_t piece = ((bytes + parts - 1) / parts + 4095) & ~uint64_t(4095);
+    pool.run(parts, [&](int i) {
+      const uint64_t b0 = std::min(bytes, (uint64_t)i * piece), b1 = std::min(bytes, b0 + piece);
+      if (b1 > b0) std::memcpy(d + b0, src + b0, b1 - b0);
+    });
+    return;
+  }
+  const uint64_t per = (rows + parts - 1) / parts;
+  pool.run(parts, [&](int i) {
+    const uint64_t q0 = std::min(rows, (uint64_t)i * per), q1 = std::min(rows, q0 + per);
+    if (layout == ST_LAYOUT_AOS) {
+      for (uint64_t r = q0; r < q1; ++r) std::memcpy(d + r * row_bytes, x + (r0 + r) * ld, row_bytes);
+    } else {
+      for (uint32_t k = 0; k < a; ++k)
+        std::memcpy(d + ((uint64_t)k * rows + q0) * 4, x + (uint64_t)k * ld + r0 + q0, (q1 - q0) * 4);
+    }
+  });
+}
+
 // Per-device staging slots reused across host-path calls (a slot = stream +
-// device record/label buffers + pinned label staging), so the H2D/kernel/D2H
-// pipeline does not pay cudaMalloc/cudaFree per call.
+// device record/label buffers + pinned label staging + pinned record staging
+// for pageable inputs), so the H2D/kernel/D2H pipeline does not pay
+// cudaMalloc/cudaFree or page pinning per call.
 struct Slot {
   cudaStream_t stream = nullptr;
   float* x = nullptr;
@@ -69,12 +176,15 @@ struct Slot {
   uint32_t* out[3] = {nullptr, nullptr, nullptr};  // labels + up to 2 counters
   uint32_t* pinned[3] = {nullptr, nullptr, nullptr};
   size_t out_cap = 0;
+  void* pin_x = nullptr;  // pinned record staging (pageable inputs)
+  size_t pin_cap = 0;
+  cudaEvent_t x_free = nullptr;  // recorded after the last copy out of pin_x / into pinned[0]
   bool busy = false;
 };
 
 class SlotPool {
  public:
-  std::vector<Slot*> acquire(int dev, int n, size_t x_bytes, size_t rows) {
+  std::vector<Slot*> acquire(int dev, int n, size_t x_bytes, size_t rows, size_t pin_bytes = 0) {
     std::lock_guard<std::mutex> lk(mu_);
     auto& v = pools_[dev];
     std::vector<Slot*> got;
@@ -109,6 +219,14 @@ class SlotPool {
           }
           sl->out_cap = rows;
         }
+        if (sl->pin_cap < pin_bytes) {
+          cudaFreeHost(sl->pin_x);
+          sl->pin_x = nullptr;
+          sl->pin_cap = 0;
+          CK(cudaMallocHost(&sl->pin_x, pin_bytes));
+          sl->pin_cap = pin_bytes;
+        }
+        if (!sl->x_free) CK(cudaEventCreateWithFlags(&sl->x_free, cudaEventDisableTiming));
       } catch (...) {
         for (Slot* q : got) q->busy = false;
         throw;
@@ -131,6 +249,27 @@ SlotPool& slot_pool() {
   return *p;
 }
 
+// Stream-ordered device memory for st_eval_timed's per-call buffers: one pool
+// per device that keeps freed memory (release threshold = max), so a call's
+// allocation after the first is a pool hit rather than cudaMalloc/cudaFree.
+cudaMemPool_t timed_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool;
+  CK(cudaMemPoolCreate(&pool, &props));
+  uint64_t keep = UINT64_MAX;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  pools[dev] = pool;
+  return pool;
+}
+
 // Runs `kernel(x_dev, rows, ld_dev, labels_dev, extra_dev, stream)` over
 // chunks of the host records with H2D / kernel / D2H overlapped across
 // several streams.  Labels (and counters) come back through pinned staging
@@ -147,7 +286,10 @@ void host_pipeline(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layo
   const uint64_t n_chunks = (m + chunk - 1) / chunk;
   const int ns = (int)std::min<uint64_t>(kStreams, n_chunks);
   const int dev = current_device();
-  std::vector<Slot*> slots = slot_pool().acquire(dev, ns, chunk * row_bytes, chunk);
+  // pageable records go through pinned staging packed by the host copy pool
+  const bool staged = !is_pinned_or_device(x);
+  std::vector<Slot*> slots =
+      slot_pool().acquire(dev, ns, chunk * row_bytes, chunk, staged ? chunk * row_bytes : 0);
   struct Release {
     std::vector<Slot*>& s;
     ~Release() {
@@ -164,7 +306,8 @@ void host_pipeline(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layo
     if (pinned_labels || pending[i].second == 0) return;
     CK(cudaStreamSynchronize(slots[i]->stream));
     for (size_t k = 0; k < outs.size(); ++k)
-      std::memcpy(outs[k] + pending[i].first, slots[i]->pinned[k], pending[i].second * 4);
+      pack_records(outs[k] + pending[i].first, reinterpret_cast<const float*>(slots[i]->pinned[k]), 0,
+                   pending[i].second, 1, 1, ST_LAYOUT_AOS);
     pending[i] = {0, 0};
   };
   for (uint64_t c = 0; c < n_chunks; ++c) {
@@ -173,7 +316,14 @@ void host_pipeline(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layo
     drain(i);
     const uint64_t r0 = c * chunk;
     const uint64_t rows = std::min(chunk, m - r0);
-    if (layout == ST_LAYOUT_AOS) {
+    if (staged) {
+      // the previous H2D out of this slot's pinned buffer must be done; the
+      // other slots' copies and kernels run while this chunk is packed
+      CK(cudaEventSynchronize(sl->x_free));
+      pack_records(sl->pin_x, x, r0, rows, a, ld, layout);
+      CK(cudaMemcpyAsync(sl->x, sl->pin_x, rows * row_bytes, cudaMemcpyHostToDevice, sl->stream));
+      CK(cudaEventRecord(sl->x_free, sl->stream));
+    } else if (layout == ST_LAYOUT_AOS) {
       if (ld == a)
         CK(cudaMemcpyAsync(sl->x, x + r0 * a, rows * row_bytes, cudaMemcpyDefault, sl->stream));
       else
@@ -387,23 +537,57 @@ int st_eval_timed(const st_tree* tree, const float* x, uint64_t m, uint32_t a, u
     } ev;
     CK(cudaStreamCreateWithFlags(&ev.s, cudaStreamNonBlocking));
     for (auto& e : ev.e) CK(cudaEventCreate(&e));
+    const int dev = current_device();
     const uint64_t row_bytes = (uint64_t)a * 4;
+    // pageable records: chunks (total / 8, 2..64 MB) packed into two pinned
+    // staging buffers by the host copy pool while the previous chunk is on
+    // the wire
+    const bool staged = !is_pinned_or_device(x);
+    const uint64_t cbytes = std::min<uint64_t>(64ull << 20, std::max<uint64_t>(2ull << 20, m * row_bytes / 8));
+    const uint64_t chunk = std::min<uint64_t>(m, std::max<uint64_t>(256, cbytes / row_bytes));
+    const bool staged_out = !is_pinned_or_device(labels);
+    std::vector<Slot*> stage;
+    if (staged || staged_out)
+      stage = slot_pool().acquire(dev, 2, 0, staged_out ? chunk : 0, staged ? chunk * row_bytes : 0);
+    struct Release {
+      std::vector<Slot*>& s;
+      ~Release() {
+        for (Slot* sl : s) cudaEventSynchronize(sl->x_free);
+        if (!s.empty()) slot_pool().release(s);
+      }
+    } release{stage};
+    cudaMemPool_t pool = timed_pool(dev);
     const auto o0 = Clock::now();
     float* xd = nullptr;
     uint32_t* ld_out = nullptr;
-    CK(cudaMalloc(&xd, m * row_bytes));
+    CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&xd), m * row_bytes, pool, ev.s));
     struct Free {
       void* p[2];
+      cudaStream_t s;
       ~Free() {
         for (void* q : p)
-          if (q) cudaFree(q);
+          if (q) cudaFreeAsync(q, s);
+        cudaStreamSynchronize(s);
       }
-    } guard{{xd, nullptr}};
-    CK(cudaMalloc(&ld_out, m * 4));
+    } guard{{xd, nullptr}, ev.s};
+    CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&ld_out), m * 4, pool, ev.s));
     guard.p[1] = ld_out;
     const auto a1 = Clock::now();
     CK(cudaEventRecord(ev.e[0], ev.s));
-    if (layout == ST_LAYOUT_AOS) {
+    if (staged) {
+      for (uint64_t r0 = 0, c = 0; r0 < m; r0 += chunk, ++c) {
+        Slot* sl = stage[c & 1];
+        const uint64_t rows = std::min(chunk, m - r0);
+        CK(cudaEventSynchronize(sl->x_free));
+        pack_records(sl->pin_x, x, r0, rows, a, ld2, layout);
+        if (layout == ST_LAYOUT_AOS)
+          CK(cudaMemcpyAsync(xd + r0 * a, sl->pin_x, rows * row_bytes, cudaMemcpyHostToDevice, ev.s));
+        else
+          CK(cudaMemcpy2DAsync(xd + r0, m * 4, sl->pin_x, rows * 4, rows * 4, a, cudaMemcpyHostToDevice,
+                               ev.s));
+        CK(cudaEventRecord(sl->x_free, ev.s));
+      }
+    } else if (layout == ST_LAYOUT_AOS) {
       if (ld2 == a)
         CK(cudaMemcpyAsync(xd, x, m * row_bytes, cudaMemcpyDefault, ev.s));
       else
@@ -415,13 +599,36 @@ int st_eval_timed(const st_tree* tree, const float* x, uint64_t m, uint32_t a, u
     eval_device_impl(t, xd, m, a, layout == ST_LAYOUT_AOS ? (uint64_t)a : m, layout, &g, ld_out,
                      nullptr, ev.s);
     CK(cudaEventRecord(ev.e[2], ev.s));
-    CK(cudaMemcpyAsync(labels, ld_out, m * 4, cudaMemcpyDefault, ev.s));
-    CK(cudaEventRecord(ev.e[3], ev.s));
+    if (staged_out) {
+      // pageable labels: chunks land in the two pinned label buffers; chunk
+      // c - 1 is copied out by the host pool while chunk c is on the wire
+      uint64_t prev0 = 0, prev_rows = 0;
+      int prev_k = 0;
+      auto copy_out = [&](int k, uint64_t r0, uint64_t rows) {
+        CK(cudaEventSynchronize(stage[k]->x_free));
+        pack_records(labels + r0, reinterpret_cast<const float*>(stage[k]->pinned[0]), 0, rows, 1, 1,
+                     ST_LAYOUT_AOS);
+      };
+      for (uint64_t r0 = 0, c = 0; r0 < m; r0 += chunk, ++c) {
+        const int k = (int)(c & 1);
+        const uint64_t rows = std::min(chunk, m - r0);
+        CK(cudaMemcpyAsync(stage[k]->pinned[0], ld_out + r0, rows * 4, cudaMemcpyDeviceToHost, ev.s));
+        CK(cudaEventRecord(stage[k]->x_free, ev.s));
+        if (prev_rows) copy_out(prev_k, prev0, prev_rows);
+        prev0 = r0, prev_rows = rows, prev_k = k;
+      }
+      CK(cudaEventRecord(ev.e[3], ev.s));
+      copy_out(prev_k, prev0, prev_rows);
+    } else {
+      CK(cudaMemcpyAsync(labels, ld_out, m * 4, cudaMemcpyDefault, ev.s));
+      CK(cudaEventRecord(ev.e[3], ev.s));
+    }
     CK(cudaStreamSynchronize(ev.s));
     const auto f0 = Clock::now();
     guard.p[0] = guard.p[1] = nullptr;
-    CK(cudaFree(xd));
-    CK(cudaFree(ld_out));
+    CK(cudaFreeAsync(xd, ev.s));
+    CK(cudaFreeAsync(ld_out, ev.s));
+    CK(cudaStreamSynchronize(ev.s));
     const auto o1 = Clock::now();
     float ms[3];
     for (int k = 0; k < 3; ++k) CK(cudaEventElapsedTime(&ms[k], ev.e[k], ev.e[k + 1]));

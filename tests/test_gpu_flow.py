@@ -128,3 +128,66 @@ def test_spec_ring_shallow_ring_stress(cuda, co, slots, monkeypatch):
         st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative", pipeline=2, samples_per_thread=sr))
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
+
+
+def _c_eval(tree, buf, m, a, ld, layout, timed=False):
+    """st_eval / st_eval_timed straight through the C ABI on a host buffer."""
+    import ctypes as C
+    from paper_1111_1373_b200 import _lib
+    L = _lib.load()
+    out = np.empty(m, np.uint32)
+    g = st.GpuGeom().to_c()
+    h = tree.handle()
+    ptr = C.c_void_p(buf.ctypes.data)
+    lay = _lib.ST_LAYOUT_SOA if layout == "soa" else _lib.ST_LAYOUT_AOS
+    if timed:
+        t = _lib.st_timing()
+        rc = L.st_eval_timed(h.h, ptr, m, a, ld, lay, C.byref(g), out.ctypes.data_as(C.c_void_p), C.byref(t))
+    else:
+        rc = L.st_eval(h.h, ptr, m, a, ld, lay, C.byref(g), out.ctypes.data_as(C.c_void_p), None)
+    assert rc == 0, _lib.last_error()
+    return out
+
+
+def _host_layout_cases(co, timed):
+    """Pageable host records packed into pinned staging by the host copy pool
+    (several 64 MB chunks, ragged tail): dense / strided AoS, SoA with a
+    leading dimension, unaligned base, and the same from pinned memory."""
+    import torch
+    nodes = co.gen_tree(10, 1000, 64, 8, 77)
+    tree = st.EncodedTree(nodes)
+    m, a = 600_001, 64  # 154 MB: 3 chunks of 262,144 records
+    x = co.gen_dataset(m, a, 78)
+    want = co.eval_serial(nodes, x)
+    assert np.array_equal(_c_eval(tree, x, m, a, a, "aos", timed), want)
+    wide = np.zeros((m, a + 5), np.float32)
+    wide[:, :a] = x
+    assert np.array_equal(_c_eval(tree, wide, m, a, a + 5, "aos", timed), want)
+    del wide
+    soa = np.zeros((a, m + 7), np.float32)
+    soa[:, :m] = x.T
+    assert np.array_equal(_c_eval(tree, soa, m, a, m + 7, "soa", timed), want)
+    del soa
+    raw = np.zeros(m * a + 1, np.float32)
+    raw[1:] = x.reshape(-1)
+    assert np.array_equal(_c_eval(tree, raw[1:], m, a, a, "aos", timed), want)
+    del raw
+    pinned = torch.from_numpy(x).pin_memory().numpy()
+    assert np.array_equal(_c_eval(tree, pinned, m, a, a, "aos", timed), want)
+
+
+@pytest.mark.parametrize("timed", [False, True])
+def test_pageable_staging_layouts(cuda, co, timed):
+    _host_layout_cases(co, timed)
+
+
+def test_pageable_staging_thread_counts(cuda, tmp_path):
+    """The copy pool's split is exact for any worker count (the pool size is
+    fixed per process: run in subprocesses)."""
+    code = ("import sys; sys.path.insert(0, 'tests'); import oracle, test_gpu_flow as t; "
+            "co = oracle.COracle(); t._host_layout_cases(co, False); t._host_layout_cases(co, True)")
+    for n in ("1", "3"):
+        env = dict(os.environ, ST_HOST_COPY_THREADS=n)
+        r = subprocess.run(["python", "-c", code], cwd=ROOT, env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, (n, r.stdout[-2000:], r.stderr[-2000:])
