@@ -24,6 +24,8 @@ res = []
 grid = [(0, 0, 0)] + [(u, u + k, w) for u, k, w in itertools.product([1, 2, 4], [1, 2, 3], [0, 17, 25])]
 if len(sys.argv) > 2 and sys.argv[2] == "deep":  # deeper rings at fewer consumer warps
     grid = [(0, 0, 0)] + [(u, nt, 0) for u in (1, 2, 3, 4) for nt in range(u + 1, 11)]
+if len(sys.argv) > 2 and sys.argv[2] == "fine":  # around the folded-tree optimum
+    grid = [(0, 0, 0)] + [(u, nt, w) for u in (2, 3, 4) for nt in range(u + 2, u + 5) for w in (0, 24, 20, 16)]
 for u, nt, w in grid:
     env = {"ST_FOREST_U": u, "ST_FOREST_NT": nt, "ST_FOREST_W": w}
     for k, v in env.items():
