@@ -135,6 +135,10 @@ struct WinTable {
   // Unused lanes carry code 0.  pm_off 0 = none (more windows, more leaves
   // than lanes, or a DAG-shaped input).
   uint32_t pm_off = 0;
+  // 8-byte windows (k_spec_ring CW), appended as SEntry units at cw_off
+  // (cw_units of them; 0 = none): entry (w, j) at 8 * (G * w + j) bytes,
+  // word = attr4 | left << cw_abits | right << (cw_abits + cw_cbits).
+  uint32_t cw_off = 0, cw_units = 0, cw_abits = 0, cw_cbits = 0;
 };
 
 }  // namespace sti
@@ -255,6 +259,20 @@ struct st_tree {
     }
     if (16 * (total + 32) >= (1u << 30)) fail(ST_ERR_ARGUMENT, "tree too large for speculative windows");
     wt.entries.resize(total + 32, SEntry{0.0f, 0u, 0u, 0u});
+    // 8-byte windows if every field fits: attr4 in abits, codes in cbits =
+    // (32 - abits) / 2 with (cbits - 2)-bit window indices and classes
+    uint32_t max_a4 = 0, max_code = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      if (is_leaf(i)) max_code = std::max(max_code, leaf_code[i]);
+      else max_a4 = std::max(max_a4, 4u * nodes[i].attribute);
+    }
+    uint32_t abits = 2;
+    while ((max_a4 >> abits) != 0) ++abits;
+    const uint32_t cbits = (32 - abits) / 2;
+    const bool cw = G <= 32 && cbits >= 8 && nw < (1u << (cbits - 2)) && max_code < (1u << (cbits - 2)) &&
+                    (uint64_t)nw * G < (1u << 24);
+    std::vector<uint2> cwt;
+    if (cw) cwt.assign((size_t)nw * G + 64, make_uint2(0u, 0u));
     std::vector<int32_t> lane_of(n, -1);
     for (uint32_t w = 0; w < nw; ++w) {
       const auto& mem = members[w];
@@ -270,6 +288,11 @@ struct st_tree {
         if (lane_of[c] >= 0) return (uint32_t)lane_of[c];
         return kExitBit | (16u * base[win_of_root[c]]);  // byte offset of the window
       };
+      auto ccode = [&](uint32_t c) -> uint32_t {
+        if (is_leaf(c)) return (1u << (cbits - 1)) | leaf_code[c];
+        if (lane_of[c] >= 0) return (uint32_t)lane_of[c];
+        return (1u << (cbits - 2)) | (uint32_t)win_of_root[c];
+      };
       for (uint32_t j = 0; j < mem.size(); ++j) {
         const st_node& nd = nodes[mem[j]];
         SEntry e;
@@ -278,11 +301,27 @@ struct st_tree {
         e.left = code(nd.child);
         e.right = code(nd.child + 1);
         wt.entries[base[w] + j] = e;
+        if (cw) {
+          uint32_t tb;
+          std::memcpy(&tb, &nd.threshold, 4);
+          cwt[(size_t)w * G + j] = make_uint2(
+              tb, (4u * nd.attribute) | (ccode(nd.child) << abits) | (ccode(nd.child + 1) << (abits + cbits)));
+        }
       }
       for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = -1;
     }
     wt.root_code = kExitBit | 0u;
     wt.windows = nw;
+    if (cw) {
+      if (cwt.size() & 1) cwt.push_back(make_uint2(0u, 0u));
+      wt.cw_off = (uint32_t)wt.entries.size();
+      wt.cw_units = (uint32_t)(cwt.size() / 2);
+      wt.cw_abits = abits;
+      wt.cw_cbits = cbits;
+      const size_t base_units = wt.entries.size();
+      wt.entries.resize(base_units + wt.cw_units, SEntry{0.0f, 0u, 0u, 0u});
+      std::memcpy(wt.entries.data() + base_units, cwt.data(), cwt.size() * sizeof(uint2));
+    }
     if (nw == 1) add_path_masks(wt, members[0], G);
     return wt;
   }

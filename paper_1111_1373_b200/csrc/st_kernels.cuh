@@ -630,6 +630,10 @@ struct SpecArgs {
   uint32_t* steps;
   uint32_t ns, win_bytes, stage_bytes;
   uint32_t pm_off;       // k_spec_ring SR == 0: path-mask entries (0 = pointer jumping)
+  // k_spec_ring CW (8-byte entries), precomputed on the host so the loop
+  // reads them straight from the constant bank: attr4 mask, left / right
+  // code shifts, code mask, leaf bit, exit payload mask, window stride (8 G)
+  uint32_t cw_amask, cw_lsh, cw_rsh, cw_cmask, cw_leaf, cw_emask, cw_wstride;
 };
 
 // Window codes: lane index (< 32), kExitBit | byte offset of the next
@@ -808,9 +812,10 @@ struct SpecRingArgs {
   uint32_t unsafe_no_gen; // benchmark-only: skip the slot-generation handshake
 };
 
-template <int A, bool WIN_SHARED, int STEPS, int SR>
+template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false>
 __global__ void __launch_bounds__(kMaxThreads)
     k_spec_ring(const SpecRingArgs ra, const __grid_constant__ CUtensorMap tmap) {
+  static_assert(!CW || (WIN_SHARED && SR >= 1), "8-byte windows: shared table, window-loop paths");
   extern __shared__ __align__(1024) unsigned char smem[];
   const SpecArgs& args = ra.s;
   constexpr int R = 32;
@@ -881,9 +886,39 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t g = lane / G;
   const uint32_t j = lane & (G - 1);
   const uint32_t gmask = G - 1;
-  const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + 16u * j;
+  const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + (CW ? 8u : 16u) * j;
   const char* wglob = reinterpret_cast<const char*>(args.win) + 16u * j;
   if constexpr (WIN_SHARED) __syncthreads();  // window table staged
+  // Window entry formats.  16-byte SEntry, or (CW) 8-byte {thr, attr4 |
+  // left << cw_abits | right << (cw_abits + cw_cbits)} with cw_cbits-bit
+  // codes: lane (< 32), exit (bit cbits-2 | window index; windows are G
+  // entries apart), leaf (bit cbits-1 | class): half the shared-memory
+  // wavefronts of the entry loads.
+  struct Ent { uint32_t thr, w, l, r; };
+  const uint32_t leafbit = CW ? args.cw_leaf : kLeafBit;
+  auto load_ent = [&](uint32_t woff) -> Ent {
+    if constexpr (CW) {
+      const uint2 t = lds_u2(jaddr + woff);
+      return {t.x, t.y, 0u, 0u};
+    } else {
+      uint4 t;
+      if constexpr (WIN_SHARED) t = lds_u4(jaddr + woff);
+      else t = __ldg(reinterpret_cast<const uint4*>(wglob + woff));
+      return {t.x, t.y, t.z, t.w};
+    }
+  };
+  auto ent_attr4 = [&](const Ent& e) -> uint32_t {
+    if constexpr (CW) return e.w & args.cw_amask;
+    else return e.w & 0x00FFFFFFu;
+  };
+  auto ent_next = [&](const Ent& e, bool right) -> uint32_t {
+    if constexpr (CW) return right ? (e.w >> args.cw_rsh) : ((e.w >> args.cw_lsh) & args.cw_cmask);
+    else return right ? e.r : e.l;
+  };
+  auto exit_off = [&](uint32_t root) -> uint32_t {
+    if constexpr (CW) return (root & args.cw_emask) * args.cw_wstride;
+    else return root & ~kExitBit;
+  };
   // SR == 0: the whole tree is one window (the paper's Proc. 5 geometry):
   // each lane's entry is the same for every record -- load it once.
   uint4 e1 = make_uint4(0u, 0u, 0u, 0u), pm1 = make_uint4(0u, 0u, 0u, 0u);
@@ -993,13 +1028,11 @@ __global__ void __launch_bounds__(kMaxThreads)
         rec.init(tile, active ? r : 0u, args.p.a, args.p.x, 0, 0, 0);
       }
       do {
-        uint4 e;
-        if constexpr (WIN_SHARED) e = lds_u4(jaddr + woff);
-        else e = __ldg(reinterpret_cast<const uint4*>(wglob + woff));
+        const Ent e = load_ent(woff);
         float v;
-        if constexpr (kRowLocal) v = lds_f32((e.y & 0x00FFFFFFu) ^ bx);
-        else v = rec.get(e.y & 0x00FFFFFFu);
-        uint32_t c = (v > __uint_as_float(e.x)) ? e.w : e.z;
+        if constexpr (kRowLocal) v = lds_f32(ent_attr4(e) ^ bx);
+        else v = rec.get(ent_attr4(e));
+        uint32_t c = ent_next(e, v > __uint_as_float(e.thr));
         if constexpr (STEPS >= 0) {
 #pragma unroll
           for (int st = 0; st < STEPS; ++st) {
@@ -1013,7 +1046,7 @@ __global__ void __launch_bounds__(kMaxThreads)
           }
         }
         const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
-        if (root & kLeafBit) {
+        if (root & leafbit) {
           if (active && j == 0)
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(root) : "memory");
           r += NG;
@@ -1028,7 +1061,7 @@ __global__ void __launch_bounds__(kMaxThreads)
             }
           }
         } else {
-          woff = root & ~kExitBit;
+          woff = exit_off(root);
         }
       } while (__any_sync(0xffffffffu, active));
     } else if constexpr (SR == 2 && WIN_SHARED && Rec<A, kTma>::kRowLocal) {
@@ -1045,10 +1078,10 @@ __global__ void __launch_bounds__(kMaxThreads)
       uint32_t wA = 0, wB = 0;
       uint32_t bA = base_of(aA ? rA : 0u), bB = base_of(aB ? rB : 0u);
       do {
-        const uint4 eA = lds_u4(jaddr + wA), eB = lds_u4(jaddr + wB);
-        const float vA = lds_f32((eA.y & 0x00FFFFFFu) ^ bA), vB = lds_f32((eB.y & 0x00FFFFFFu) ^ bB);
-        uint32_t cA = (vA > __uint_as_float(eA.x)) ? eA.w : eA.z;
-        uint32_t cB = (vB > __uint_as_float(eB.x)) ? eB.w : eB.z;
+        const Ent eA = load_ent(wA), eB = load_ent(wB);
+        const float vA = lds_f32(ent_attr4(eA) ^ bA), vB = lds_f32(ent_attr4(eB) ^ bB);
+        uint32_t cA = ent_next(eA, vA > __uint_as_float(eA.thr));
+        uint32_t cB = ent_next(eB, vB > __uint_as_float(eB.thr));
         auto jump = [&]() {
           const uint32_t uA = __shfl_sync(0xffffffffu, cA, cA & gmask, G);
           const uint32_t uB = __shfl_sync(0xffffffffu, cB, cB & gmask, G);
@@ -1063,23 +1096,23 @@ __global__ void __launch_bounds__(kMaxThreads)
         }
         const uint32_t rtA = __shfl_sync(0xffffffffu, cA, 0, G);
         const uint32_t rtB = __shfl_sync(0xffffffffu, cB, 0, G);
-        if (rtA & kLeafBit) {
+        if (rtA & leafbit) {
           if (aA && j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rA), "r"(rtA) : "memory");
           rA += 2 * NG;
           aA = rA < rows;
           wA = 0;
           if (aA) bA = base_of(rA);
         } else {
-          wA = rtA & ~kExitBit;
+          wA = exit_off(rtA);
         }
-        if (rtB & kLeafBit) {
+        if (rtB & leafbit) {
           if (aB && j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rB), "r"(rtB) : "memory");
           rB += 2 * NG;
           aB = rB < rows;
           wB = 0;
           if (aB) bB = base_of(rB);
         } else {
-          wB = rtB & ~kExitBit;
+          wB = exit_off(rtB);
         }
       } while (__any_sync(0xffffffffu, aA || aB));
     } else {
@@ -1094,7 +1127,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     if (lane < rows) {
       uint32_t code;
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(code) : "r"(lbuf + 4u * lane));
-      const uint32_t cls = code & ~kLeafBit;
+      const uint32_t cls = code & (leafbit - 1u);
       args.labels[r0 + lane] = args.leaf_class ? __ldg(args.leaf_class + cls) : cls;
     }
     __syncwarp();

@@ -31,10 +31,10 @@ void launch_spec_steps(const SpecArgs& sa, const Staging& stg, size_t smem, int 
   }
 }
 
-template <int A, bool WS, int STEPS, int SR>
+template <int A, bool WS, int STEPS, int SR, bool CW = false>
 void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
                         uint32_t warps, cudaStream_t s) {
-  auto fn = k_spec_ring<A, WS, STEPS, SR>;
+  auto fn = k_spec_ring<A, WS, STEPS, SR, CW>;
   const uint64_t n_tiles = (ra.s.p.m + 31) / 32;
   const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles * warps, warps);
   clear_stale_error();
@@ -42,19 +42,29 @@ void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem,
   check_launch();
 }
 
-template <int A, bool WS, int STEPS>
+template <int A, bool WS, int STEPS, bool CW = false>
 void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
                          uint32_t warps, cudaStream_t s) {
   // two record streams: shared window table and records inside one 128-byte row
   if constexpr (WS && (A == 8 || A == 16 || A == 32)) {
-    if (sr >= 2) return launch_spec_ring_k<A, WS, STEPS, 2>(ra, stg, smem, dev, warps, s);
+    if (sr >= 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW>(ra, stg, smem, dev, warps, s);
   }
-  return launch_spec_ring_k<A, WS, STEPS, 1>(ra, stg, smem, dev, warps, s);
+  return launch_spec_ring_k<A, WS, STEPS, 1, CW>(ra, stg, smem, dev, warps, s);
 }
 
 template <int A>
-void launch_spec_ring(bool ws, uint32_t sr, const SpecRingArgs& ra, const Staging& stg, size_t smem,
-                      int dev, uint32_t warps, cudaStream_t s) {
+void launch_spec_ring(bool ws, uint32_t sr, bool cw, const SpecRingArgs& ra, const Staging& stg,
+                      size_t smem, int dev, uint32_t warps, cudaStream_t s) {
+  // 8-byte window entries (shared table, window loop)
+  if (cw && sr != 0) {
+    switch (ra.s.smax) {
+      case 0: return launch_spec_ring_sr<A, true, 0, true>(sr, ra, stg, smem, dev, warps, s);
+      case 1: return launch_spec_ring_sr<A, true, 1, true>(sr, ra, stg, smem, dev, warps, s);
+      case 2: return launch_spec_ring_sr<A, true, 2, true>(sr, ra, stg, smem, dev, warps, s);
+      case 3: return launch_spec_ring_sr<A, true, 3, true>(sr, ra, stg, smem, dev, warps, s);
+      default: return launch_spec_ring_sr<A, true, -1, true>(sr, ra, stg, smem, dev, warps, s);
+    }
+  }
   // the whole tree in one window (sr == 0): hoisted entry, independent
   // passes, the doubling count (<= 5 for <= 32 lanes) always compile-time so
   // the passes interleave
@@ -227,36 +237,56 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // CTA-shared ring (default for the fast path): up to 32 warps on one SM
   // share NS = warps + 12 tile slots; ~12 tiles in flight cover DRAM latency.
   if (stg.loader == kTma && !stats && g.pipeline != 1) {
+    // record streams per group (samples_per_thread): two independent
+    // window chains per lane pay off on large trees, where a record walks
+    // many windows (C5 d16: 0.61 vs 0.68 ms; C1, 1023 internal nodes: 0.038
+    // vs 0.040 ms), and cost a little on small ones (C2, 255: 0.399 vs
+    // 0.390 ms; profiles/r1_sweep_*_spec2d.json, *_spec2e.json)
+    uint32_t sr = g.samples_per_thread ? g.samples_per_thread : (t->info.internal > 511 ? 2u : 1u);
+    const bool onewin = wt->windows == 1 && win_shared && !env_u32("ST_SPEC_NO_ONEWIN", 0);
+    if (onewin) sr = 0;  // whole tree in one window
+    SpecArgs rs = sa;
+    bool ws = win_shared, cw = false;
+    // 8-byte window entries when the tree's fields fit (half the entry
+    // wavefronts); ST_SPEC_WIDE_WIN=1 keeps the 16-byte format
+    if (!onewin && wt->cw_units && !env_u32("ST_SPEC_WIDE_WIN", 0)) {
+      const uint32_t cb = round1024((size_t)wt->cw_units * sizeof(SEntry));
+      if (cb <= 96 * 1024) {
+        cw = ws = true;
+        rs.win = wdev + wt->cw_off;
+        rs.n_entries = wt->cw_units;
+        rs.win_bytes = cb;
+        const uint32_t ab = wt->cw_abits, cb2 = wt->cw_cbits;
+        rs.cw_amask = (1u << ab) - 1u;
+        rs.cw_lsh = ab;
+        rs.cw_rsh = ab + cb2;
+        rs.cw_cmask = (1u << cb2) - 1u;
+        rs.cw_leaf = 1u << (cb2 - 1u);
+        rs.cw_emask = (1u << (cb2 - 2u)) - 1u;
+        rs.cw_wstride = 8u * G;
+      }
+    }
     const size_t lb = 32 + 32 * 128;  // generation padding + ticket + per-warp label rows (<= 32 warps)
-    const size_t budget = pr.smem_optin - 1024 - sa.win_bytes - lb;
+    const size_t budget = pr.smem_optin - 1024 - rs.win_bytes - lb;
     const size_t max_slots = budget / (stg.stage_bytes + 16u);
     const uint32_t warps = (uint32_t)std::min<size_t>(32, max_slots > 12 ? max_slots - 12 : 0);
     if (warps >= 4) {
       SpecRingArgs ra{};
-      ra.s = sa;
+      ra.s = rs;
       ra.n_slots = (uint32_t)std::min<size_t>(max_slots, warps + 12);
       // development / stress knob: any ring depth >= 1 must give exact labels
       if (const uint32_t ns = env_u32("ST_SPEC_RING_SLOTS", 0)) ra.n_slots = std::min<uint32_t>(ra.n_slots, ns);
       ra.unsafe_no_gen = env_u32("ST_SPEC_RING_UNSAFE_NO_GEN", 0);  // measurement of the handshake only
-      const size_t rsmem = 1024 + sa.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 8u) +
+      const size_t rsmem = 1024 + rs.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 8u) +
                            (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128;
-      // record streams per group (samples_per_thread): two independent
-      // window chains per lane pay off on large trees, where a record walks
-      // many windows (C5 d16: 0.61 vs 0.68 ms; C1, 1023 internal nodes: 0.038
-      // vs 0.040 ms), and cost a little on small ones (C2, 255: 0.399 vs
-      // 0.390 ms; profiles/r1_sweep_*_spec2d.json, *_spec2e.json)
-      uint32_t sr = g.samples_per_thread ? g.samples_per_thread : (t->info.internal > 511 ? 2u : 1u);
-      if (wt->windows == 1 && win_shared && !env_u32("ST_SPEC_NO_ONEWIN", 0)) {
-        sr = 0;  // whole tree in one window
-        // ballot + leaf path masks unless pointer jumping is asked for
-        ra.s.pm_off = env_u32("ST_SPEC_ONEWIN_JUMP", 0) ? 0u : wt->pm_off;
-      }
+      // one window: ballot + leaf path masks unless pointer jumping is asked for
+      if (onewin) ra.s.pm_off = env_u32("ST_SPEC_ONEWIN_JUMP", 0) ? 0u : wt->pm_off;
       switch (ct_arity(a) ? a : 0) {
-        case 8: return launch_spec_ring<8>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
-        case 16: return launch_spec_ring<16>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
-        case 32: return launch_spec_ring<32>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
-        case 64: return launch_spec_ring<64>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
-        default: return launch_spec_ring<0>(win_shared, sr, ra, stg, rsmem, dev, warps, s);
+        case 8: return launch_spec_ring<8>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
+        case 16: return launch_spec_ring<16>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
+        case 32: return launch_spec_ring<32>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
+        case 64: return launch_spec_ring<64>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
+        default: return launch_spec_ring<0>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
       }
     }
   }

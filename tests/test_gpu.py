@@ -442,3 +442,28 @@ def test_single_window_speculation(cuda, co, mode, monkeypatch):
         want = co.eval_serial(nodes, x)
         for g in geoms:
             assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, m, g)
+
+
+@pytest.mark.parametrize("wide", ["0", "1"])
+def test_spec_window_formats(cuda, co, wide, monkeypatch):
+    """The ring kernel's 8-byte window entries (default when the tree's
+    fields fit) and the 16-byte format (ST_SPEC_WIDE_WIN=1): random trees
+    with many windows, group widths 2..16, one and two record streams,
+    row-local and other arities, ragged counts, large leaf payloads
+    (class ids >= 2^31 -> ordinals), against the oracle."""
+    monkeypatch.setenv("ST_SPEC_WIDE_WIN", wide)
+    for seed in range(1, 161):
+        a = (8, 16, 32, 19, 64, 3, 128, 300)[seed % 8]
+        depth = 4 + seed % 17
+        leaves = min(max(depth + 1, 40 + 37 * (seed % 60)), 2 ** depth, 4096)
+        nodes = co.gen_tree(depth, leaves, a, 2 + seed % 9, seed)
+        if seed % 10 == 0:
+            leaf = nodes["class_id"] != 0xFFFFFFFF
+            nodes["class_id"][leaf] = 0x80000000 + nodes["class_id"][leaf]  # wide class ids
+        m = (1, 33, 1000, 4097, 20011)[seed % 5]
+        x = co.gen_dataset(m, a, seed + 4000, gaussian=(seed % 2 == 0))
+        want = co.eval_serial(nodes, x)
+        for g in (st.GpuGeom(algo="speculative"),
+                  st.GpuGeom(algo="speculative", group_lanes=(2, 4, 8, 16)[seed % 4],
+                             samples_per_thread=1 + seed % 2)):
+            assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, m, g)
