@@ -232,7 +232,8 @@ def main():
         print("E2E C4", json.dumps(e2e["C4"]), flush=True)
         out["e2e"] = e2e
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", f"workloads_{FLUSH_MODE}.json"), "w") as fh:
+    tag = "" if args.only == ap.get_default("only") else "_" + args.only.replace(",", "_")
+    with open(os.path.join(ROOT, "gpurun_out", f"workloads_{FLUSH_MODE}{tag}.json"), "w") as fh:
         json.dump(out, fh, indent=1)
 
 
