@@ -10,6 +10,8 @@
 //     occupancy-derived persistent grid;
 //   * the host-buffer path (chunked H2D / kernel / D2H over two streams) and
 //     the sample-sharded multi-GPU driver.
+#include <pthread.h>
+
 #include "st_internal.cuh"
 
 namespace sti {
@@ -66,7 +68,13 @@ bool is_pinned_or_device(const void* p) {
 class HostCopyPool {
  public:
   static HostCopyPool& get() {
-    static HostCopyPool* p = new HostCopyPool();  // intentionally leaked (detached workers)
+    static HostCopyPool* p = [] {
+      auto* q = new HostCopyPool();  // intentionally leaked (detached workers)
+      // a fork()ed child has no workers: run its jobs on the caller alone
+      pthread_atfork(nullptr, nullptr, [] { reset_after_fork(); });
+      return q;
+    }();
+    instance() = p;
     return *p;
   }
   int width() const { return (int)workers_ + 1; }
@@ -109,6 +117,18 @@ class HostCopyPool {
   }
 
  private:
+  static HostCopyPool*& instance() {
+    static HostCopyPool* i = nullptr;
+    return i;
+  }
+  static void reset_after_fork() {
+    HostCopyPool* p = instance();
+    if (!p) return;
+    p->workers_ = 0;
+    new (&p->mu_) std::mutex();  // may have been held by a thread that is gone
+    new (&p->cv_) std::condition_variable();
+    new (&p->q_) std::deque<std::function<void()>>();  // drop (leak) the parent's queue
+  }
   HostCopyPool() {
     const uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
     workers_ = env_u32("ST_HOST_COPY_THREADS", std::min(16u, hw)) - 1u;
