@@ -237,14 +237,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // CTA-shared ring (default for the fast path): up to 32 warps on one SM
   // share NS = warps + 12 tile slots; ~12 tiles in flight cover DRAM latency.
   if (stg.loader == kTma && !stats && g.pipeline != 1) {
-    // record streams per group (samples_per_thread): two independent
-    // window chains per lane pay off on large trees, where a record walks
-    // many windows (C5 d16: 0.61 vs 0.68 ms; C1, 1023 internal nodes: 0.038
-    // vs 0.040 ms), and cost a little on small ones (C2, 255: 0.399 vs
-    // 0.390 ms; profiles/r1_sweep_*_spec2d.json, *_spec2e.json)
-    uint32_t sr = g.samples_per_thread ? g.samples_per_thread : (t->info.internal > 511 ? 2u : 1u);
     const bool onewin = wt->windows == 1 && win_shared && !env_u32("ST_SPEC_NO_ONEWIN", 0);
-    if (onewin) sr = 0;  // whole tree in one window
     SpecArgs rs = sa;
     bool ws = win_shared, cw = false;
     // 8-byte window entries when the tree's fields fit (half the entry
@@ -266,6 +259,14 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
         rs.cw_wstride = 8u * G;
       }
     }
+    // record streams per group (samples_per_thread): two independent window
+    // chains per lane.  With 8-byte entries they win on every canonical tree
+    // (C2 0.357 vs 0.386 ms, C5 d8 0.281 vs 0.295, C1, C3, C5 d16;
+    // profiles/r1_sweep_*_spec2_cw.json); with 16-byte entries only on large
+    // trees (C5 d16: 0.61 vs 0.68 ms; C2, 255 internal: 0.399 vs 0.390 ms;
+    // profiles/r1_sweep_*_spec2d.json, *_spec2e.json)
+    uint32_t sr = g.samples_per_thread ? g.samples_per_thread : ((cw || t->info.internal > 511) ? 2u : 1u);
+    if (onewin) sr = 0;  // whole tree in one window
     const size_t lb = 32 + 32 * 128;  // generation padding + ticket + per-warp label rows (<= 32 warps)
     const size_t budget = pr.smem_optin - 1024 - rs.win_bytes - lb;
     const size_t max_slots = budget / (stg.stage_bytes + 16u);
