@@ -89,6 +89,7 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.labels = labels;
   // records walked from registers: default for 8-attribute records; 16 on request
   d.record_regs = (g.record_regs == 1 || (g.record_regs == 0 && a == 8)) ? 1u : 0u;
+  d.bulk_tree = env_u32("ST_TREE_BULK", 1) ? 1u : 0u;
 
   // the folded tree (leaf pairs inside terminals) serves the shared-tree TMA
   // walks over 8/16/32-attribute records of large trees; every other path

@@ -332,6 +332,7 @@ struct DataArgs {
   uint32_t tree_bytes;         // shared bytes reserved for the node array (kShared)
   uint32_t stage_bytes;        // stride between stages
   uint32_t record_regs;        // host hint: 8-attribute records walk from registers (kSharedReg)
+  uint32_t bulk_tree;          // stage the shared tree with one cp.async.bulk (else per-thread loads)
 };
 
 // Shared-memory carve-out shared by the kernels:
@@ -438,13 +439,39 @@ __global__ void __launch_bounds__(kMaxThreads)
     const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
     const uint32_t n16 = (args.n_nodes * 8u + 15u) / 16u;
     const uint32_t rebase = sbase << args.abits;  // child offset -> absolute address
-    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
-      uint4 v = __ldg(src + i);
-      if (!(v.y & kLeafBit)) v.y += rebase;
-      if (!(v.w & kLeafBit)) v.w += rebase;
-      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
-                   "r"(v.y), "r"(v.z), "r"(v.w)
-                   : "memory");
+    if (args.bulk_tree) {
+      // one bulk copy (a single DRAM/L2 round trip for the whole array, in
+      // flight beside the first record tiles), then an in-place rebase pass
+      // over shared memory.  The per-thread loop below serialises one
+      // round trip per iteration (the shared store orders the next load).
+      // its mbarrier sits after the per-warp stage barriers, inside the
+      // 1024 B alignment reserve of the carve-out (no static shared memory)
+      const uint32_t bar = tiles0 + (LOADER == kDirect ? 0u : nw * args.ns * (args.stage_bytes + 8u));
+      if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(bar, 16u * n16);
+        bulk_load(sbase, src, 16u * n16, bar);
+      }
+      __syncthreads();
+      mbar_wait(bar, 0);
+      for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
+        uint4 v = lds_u4(sbase + 16u * i);
+        if (!(v.y & kLeafBit)) v.y += rebase;
+        if (!(v.w & kLeafBit)) v.w += rebase;
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
+                     "r"(v.y), "r"(v.z), "r"(v.w)
+                     : "memory");
+      }
+    } else {
+      for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
+        uint4 v = __ldg(src + i);
+        if (!(v.y & kLeafBit)) v.y += rebase;
+        if (!(v.w & kLeafBit)) v.w += rebase;
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
+                     "r"(v.y), "r"(v.z), "r"(v.w)
+                     : "memory");
+      }
     }
     __syncthreads();
   }
@@ -810,6 +837,7 @@ struct SpecRingArgs {
   SpecArgs s;
   uint32_t n_slots;       // NS
   uint32_t unsafe_no_gen; // benchmark-only: skip the slot-generation handshake
+  uint32_t bulk_win;      // stage the window table with one cp.async.bulk (else per-thread loads)
 };
 
 template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false>
@@ -865,19 +893,26 @@ __global__ void __launch_bounds__(kMaxThreads)
       asm volatile("st.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(0u) : "memory");
     }
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(ticket), "r"(0u) : "memory");
+    if (WIN_SHARED && ra.bulk_win) mbar_init(ticket + 8u, 1);
     fence_barrier_init();
+    if (WIN_SHARED && ra.bulk_win) {  // the whole table in one round trip
+      mbar_arrive_expect_tx(ticket + 8u, 16u * args.n_entries);
+      bulk_load(sbase, args.win, 16u * args.n_entries, ticket + 8u);
+    }
   }
   __syncthreads();
   if (warp == 0)
     for (uint64_t jj = 0; jj < NS && jj < my_tiles; ++jj) fill(jj);
   // window table staged while the first tiles are in flight
   if constexpr (WIN_SHARED) {
-    const uint4* src = reinterpret_cast<const uint4*>(args.win);
-    for (uint32_t i = threadIdx.x; i < args.n_entries; i += blockDim.x) {
-      const uint4 v = __ldg(src + i);
-      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
-                   "r"(v.y), "r"(v.z), "r"(v.w)
-                   : "memory");
+    if (!ra.bulk_win) {
+      const uint4* src = reinterpret_cast<const uint4*>(args.win);
+      for (uint32_t i = threadIdx.x; i < args.n_entries; i += blockDim.x) {
+        const uint4 v = __ldg(src + i);
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
+                     "r"(v.y), "r"(v.z), "r"(v.w)
+                     : "memory");
+      }
     }
   }
 
@@ -888,7 +923,10 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t gmask = G - 1;
   const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + (CW ? 8u : 16u) * j;
   const char* wglob = reinterpret_cast<const char*>(args.win) + 16u * j;
-  if constexpr (WIN_SHARED) __syncthreads();  // window table staged
+  if constexpr (WIN_SHARED) {  // window table staged
+    if (ra.bulk_win) mbar_wait(ticket + 8u, 0);
+    else __syncthreads();
+  }
   // Window entry formats.  16-byte SEntry, or (CW) 8-byte {thr, attr4 |
   // left << cw_abits | right << (cw_abits + cw_cbits)} with cw_cbits-bit
   // codes: lane (< 32), exit (bit cbits-2 | window index; windows are G

@@ -278,6 +278,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       // development / stress knob: any ring depth >= 1 must give exact labels
       if (const uint32_t ns = env_u32("ST_SPEC_RING_SLOTS", 0)) ra.n_slots = std::min<uint32_t>(ra.n_slots, ns);
       ra.unsafe_no_gen = env_u32("ST_SPEC_RING_UNSAFE_NO_GEN", 0);  // measurement of the handshake only
+      ra.bulk_win = env_u32("ST_TREE_BULK", 1) ? 1u : 0u;
       const size_t rsmem = 1024 + rs.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 8u) +
                            (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128;
       // one window: ballot + leaf path masks unless pointer jumping is asked for
