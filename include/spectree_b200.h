@@ -87,7 +87,8 @@ typedef struct st_geom {
                                   ring), 1 = per-warp TMA ring */
   uint32_t record_regs;        /* data kernel, 8/16-attribute records: 0 = auto (registers for 8),
                                   1 = walk from registers (tile released right after loading),
-                                  2 = walk from the shared tile */
+                                  2 = walk from the shared tile,
+                                  3 = transpose each tile in place to attribute-major, then walk it */
   uint32_t reserved[1];
 } st_geom;
 

@@ -26,6 +26,7 @@ void launch_data_tloc(int tloc, const DataArgs& d, const Staging& stg, const st_
   switch (tloc) {
     case ST_TREE_SHARED:
       if constexpr ((A == 8 || A == 16) && LOADER == kTma) {
+        if (d.record_regs == 2) return launch_data_t<A, S, kSharedT, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
         if (d.record_regs) return launch_data_t<A, S, kSharedReg, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
       }
       return launch_data_t<A, S, kShared, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
@@ -51,13 +52,15 @@ void launch_data_tloc(int tloc, const DataArgs& d, const Staging& stg, const st_
 }
 
 
-uint32_t choose_S(uint32_t a, uint32_t want) {
+uint32_t choose_S(uint32_t a, uint32_t want, bool small) {
   // instantiated: a=8 {1,2,4}, a=16 {1,2,4}, a=32 {1,2}, others {1}
   const uint32_t maxS = (a == 8 || a == 16) ? 4 : a == 32 ? 2 : 1;
   // predicated walk (k_data data_step): independent chains per lane pay off
   // where a tile is small -- C3 (a = 8): S = 4 0.63 ms vs S = 2 0.67 ms for 32
-  // frames; C2 (a = 32): S = 2 0.307 vs S = 1 0.321 ms (profiles/r1_sweep_*)
-  if (want == 0) want = a <= 8 ? 4 : a == 32 ? 2 : 1;
+  // frames; C2 (a = 32): S = 2 0.307 vs S = 1 0.321 ms (profiles/r1_sweep_*);
+  // C5 (a = 16, one stage per warp): S = 4 vs 1: d12 -7 %, d16 -16 %, d20
+  // -10 %, d8 even (profiles/r1_ab_stages.txt).  Small inputs (C1) keep S = 1.
+  if (want == 0) want = a <= 8 ? 4 : a == 32 ? 2 : (a == 16 && !small) ? 4 : 1;
   uint32_t S = 1;
   while (S * 2 <= std::min(want, maxS)) S *= 2;
   return S;
@@ -89,7 +92,13 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.labels = labels;
   // records walked from registers: default for 8-attribute records; 16 on request
   d.record_regs = (g.record_regs == 1 || (g.record_regs == 0 && a == 8)) ? 1u : 0u;
+  // attribute-major (transposed) tiles instead of register records
+  if ((a == 8 || a == 16) && (g.record_regs == 3 || (g.record_regs == 0 && env_u32("ST_DATA_TRANSPOSE", 0))))
+    d.record_regs = 2;
   d.bulk_tree = env_u32("ST_TREE_BULK", 1) ? 1u : 0u;
+
+  // fewer than 8 tiles of 32 records per warp at 32 warps on every SM
+  const bool small = m < (uint64_t)pr.sms * 32 * 8 * 32;
 
   // the folded tree (leaf pairs inside terminals) serves the shared-tree TMA
   // walks over 8/16/32-attribute records of large trees; every other path
@@ -100,7 +109,7 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
                     (a == 8 || a == 16 || a == 32) &&
                     !env_u32("ST_DATA_NO_FOLD", 0) &&
                     (g.tree_loc == ST_TREE_AUTO || g.tree_loc == ST_TREE_SHARED) &&
-                    tma_ok(x, m, a, ld, layout, ct_arity(a) ? choose_S(a, g.samples_per_thread) : 1);
+                    tma_ok(x, m, a, ld, layout, ct_arity(a) ? choose_S(a, g.samples_per_thread, small) : 1);
   uint32_t tree_bytes = round1024((fold ? t->folded.size() : t->nodes.size()) * sizeof(CNode));
   int tloc = g.tree_loc;
   if (!t->compact_ok) tloc = kWide;
@@ -109,12 +118,18 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // shared trees are rebased to absolute shared addresses inside the compact
   // child field: the largest address must fit below the leaf bit
   if (tloc == ST_TREE_SHARED && ((uint64_t)pr.smem_optin << t->abits) >= (1ull << 31)) tloc = ST_TREE_GLOBAL;
-  const uint32_t S0 = ct_arity(a) ? choose_S(a, g.samples_per_thread) : 1;
+  const uint32_t S0 = ct_arity(a) ? choose_S(a, g.samples_per_thread, small) : 1;
   // Records walked from registers release their tile before the walk, so one
   // stage per warp already double-buffers (next TMA in flight during the
   // walk) and the saved shared memory buys twice the warps (C3 x 32 frames:
   // 0.566 vs 0.615 ms, profiles/r1_sweep_C3x32_regs1.json).
-  const uint32_t want_ns = g.stages ? g.stages : (d.record_regs && tloc == ST_TREE_SHARED ? 1u : 0u);
+  // Shared-tree walks over large inputs: one stage per warp too -- the
+  // smem it frees holds S-record tiles for as many warps, and the S chains
+  // per lane hide the tree latency better than a second tile in flight
+  // (same-box A/B, profiles/r1_ab_stages.txt: C2 -1.9 %, C5 d16 -16 %).
+  // Small inputs are ramp-up bound and keep two (C1: 17.3 vs 17.8 us).
+  const uint32_t want_ns =
+      g.stages ? g.stages : ((d.record_regs == 1 || !small) && tloc == ST_TREE_SHARED ? 1u : 0u);
   Staging stg = plan_staging(x, m, a, ld, layout, S0, want_ns,
                              tloc == ST_TREE_SHARED ? tree_bytes : 0, pr);
   if (tloc == ST_TREE_SHARED && tree_bytes + 1024 + stg.tile_smem() > pr.smem_optin) {
@@ -135,6 +150,12 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       4 * (1024 + tree_bytes + (size_t)kWarpsPerCta * stg.ns * (stg.stage_bytes + 8u)) <= pr.smem_per_sm) {
     stg.warps = kWarpsPerCta;
     want_bps = 4;
+  }
+  // transposed tiles: the scaled attribute field widens the meta's low part
+  // by log2(32 S) bits; the absolute child address must still fit below bit 31
+  if (d.record_regs == 2) {
+    const uint32_t lr = stg.S == 4 ? 7u : stg.S == 2 ? 6u : 5u;
+    if (stg.loader != kTma || ((uint64_t)pr.smem_optin << (t->abits + lr)) >= (1ull << 31)) d.record_regs = 0;
   }
   d.ns = stg.ns;
   d.stage_bytes = stg.stage_bytes;

@@ -62,8 +62,11 @@ struct __align__(16) SEntry {
 
 enum Loader { kTma = 0, kScalar = 1, kSoa = 2, kDirect = 3 };
 // kSharedReg: shared-memory tree, records walked from registers (8-attribute
-// records; the TMA tile is released as soon as it is in registers)
-enum TreeLoc { kShared = 1, kConst = 2, kGlobal = 3, kWide = 4, kSharedReg = 5 };
+// records; the TMA tile is released as soon as it is in registers).
+// kSharedT: shared-memory tree, each warp's tile transposed in place to
+// attribute-major (feature reads conflict-free, no register select); the
+// staged tree's attribute fields are pre-scaled to the transposed stride.
+enum TreeLoc { kShared = 1, kConst = 2, kGlobal = 3, kWide = 4, kSharedReg = 5, kSharedT = 6 };
 
 // ---------------------------------------------------------------------------
 // PTX helpers (32-bit shared addresses)
@@ -300,7 +303,7 @@ struct ConstTree {
 // next-node address is (meta >> abits) + 8*(x > thr) with no base add.
 // Constant / global trees keep offsets relative to node 0.
 template <int TLOC>
-constexpr bool kAbsTree = (TLOC == kShared || TLOC == kSharedReg);
+constexpr bool kAbsTree = (TLOC == kShared || TLOC == kSharedReg || TLOC == kSharedT);
 
 template <int TLOC, int CAP>
 struct TreeRef {
@@ -314,7 +317,7 @@ struct TreeRef {
       return make_uint2(__float_as_uint(n.thr), n.meta);
     } else if constexpr (TLOC == kGlobal) {
       return __ldg(reinterpret_cast<const uint2*>(g + off));
-    } else {  // kShared, kSharedReg: absolute shared addresses
+    } else {  // kShared, kSharedReg, kSharedT: absolute shared addresses
       return lds_u2(off);
     }
   }
@@ -357,6 +360,30 @@ __device__ __forceinline__ void data_step(uint32_t& thr, uint32_t& meta, uint32_
       "setp.ge.s32 p, %1, 0;\n\t"
       "and.b32 fa, %1, %3;\n\t"
       "xor.b32 fa, fa, %2;\n\t"
+      "@p ld.shared.f32 v, [fa];\n\t"
+      "setp.gt.and.f32 q, v, %0, p;\n\t"
+      "shr.u32 ch, %1, %4;\n\t"
+      "@q add.u32 ch, ch, 8;\n\t"
+      "@p ld.shared.v2.u32 {%0, %1}, [ch];\n\t"
+      "}"
+      : "+f"(*reinterpret_cast<float*>(&thr)), "+r"(meta)
+      : "r"(bx), "r"(amask), "r"(abits)
+      : "memory");
+}
+
+// Level step over an attribute-major (transposed) tile: the staged meta holds
+// 4*attr*R in its low abits_t bits, so the feature address is bx + that
+// (bx = tile + 4*record slot): conflict-free, every lane in its own bank.
+__device__ __forceinline__ void data_step_t(uint32_t& thr, uint32_t& meta, uint32_t bx, uint32_t amask,
+                                            uint32_t abits) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q;\n\t"
+      ".reg .u32 fa, ch;\n\t"
+      ".reg .f32 v;\n\t"
+      "setp.ge.s32 p, %1, 0;\n\t"
+      "and.b32 fa, %1, %3;\n\t"
+      "add.u32 fa, fa, %2;\n\t"
       "@p ld.shared.f32 v, [fa];\n\t"
       "setp.gt.and.f32 q, v, %0, p;\n\t"
       "shr.u32 ch, %1, %4;\n\t"
@@ -435,7 +462,10 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t amask = (1u << args.abits) - 1u;
 
   // ---- stage the node array once per CTA --------------------------------
-  if constexpr (TLOC == kShared || TLOC == kSharedReg) {
+  constexpr uint32_t kLR = S == 4 ? 7u : S == 2 ? 6u : 5u;  // log2(R)
+  // kSharedT: internal meta = (abs child << abits_t) | 4*attr*R
+  const uint32_t abits_t = args.abits + (TLOC == kSharedT ? kLR : 0u);
+  if constexpr (TLOC == kShared || TLOC == kSharedReg || TLOC == kSharedT) {
     const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
     const uint32_t n16 = (args.n_nodes * 8u + 15u) / 16u;
     const uint32_t rebase = sbase << args.abits;  // child offset -> absolute address
@@ -457,8 +487,13 @@ __global__ void __launch_bounds__(kMaxThreads)
       mbar_wait(bar, 0);
       for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
         uint4 v = lds_u4(sbase + 16u * i);
-        if (!(v.y & kLeafBit)) v.y += rebase;
-        if (!(v.w & kLeafBit)) v.w += rebase;
+        if constexpr (TLOC == kSharedT) {
+          if (!(v.y & kLeafBit)) v.y = (((v.y >> args.abits) + sbase) << abits_t) | ((v.y & amask) << kLR);
+          if (!(v.w & kLeafBit)) v.w = (((v.w >> args.abits) + sbase) << abits_t) | ((v.w & amask) << kLR);
+        } else {
+          if (!(v.y & kLeafBit)) v.y += rebase;
+          if (!(v.w & kLeafBit)) v.w += rebase;
+        }
         asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
                      "r"(v.y), "r"(v.z), "r"(v.w)
                      : "memory");
@@ -466,8 +501,13 @@ __global__ void __launch_bounds__(kMaxThreads)
     } else {
       for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
         uint4 v = __ldg(src + i);
-        if (!(v.y & kLeafBit)) v.y += rebase;
-        if (!(v.w & kLeafBit)) v.w += rebase;
+        if constexpr (TLOC == kSharedT) {
+          if (!(v.y & kLeafBit)) v.y = (((v.y >> args.abits) + sbase) << abits_t) | ((v.y & amask) << kLR);
+          if (!(v.w & kLeafBit)) v.w = (((v.w >> args.abits) + sbase) << abits_t) | ((v.w & amask) << kLR);
+        } else {
+          if (!(v.y & kLeafBit)) v.y += rebase;
+          if (!(v.w & kLeafBit)) v.w += rebase;
+        }
         asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sbase + 16u * i), "r"(v.x),
                      "r"(v.y), "r"(v.z), "r"(v.w)
                      : "memory");
@@ -494,6 +534,65 @@ __global__ void __launch_bounds__(kMaxThreads)
           nd = __ldg(args.wide + c);
         }
         args.labels[r0 + r] = nd.w;
+      }
+    } else if constexpr (TLOC == kSharedT && LOADER == kTma && (A == 8 || A == 16)) {
+      // transpose the warp's tile in place to attribute-major: slot (a, r)
+      // at 4*(a*R + r), r = q*32 + lane -- every later feature read by lane l
+      // hits bank l whatever the attribute (the record-major tile puts
+      // 128/(4A) records in a row and conflicts on random attributes)
+      {
+        float f[S][A];
+#pragma unroll
+        for (int q = 0; q < S; ++q) {
+          const uint32_t b = (uint32_t)(q * 32 + lane) * (4u * A);
+#pragma unroll
+          for (int c = 0; c < A / 4; ++c) {
+            const uint4 v = lds_u4(tile + swz(b + 16u * c));
+            f[q][4 * c + 0] = __uint_as_float(v.x);
+            f[q][4 * c + 1] = __uint_as_float(v.y);
+            f[q][4 * c + 2] = __uint_as_float(v.z);
+            f[q][4 * c + 3] = __uint_as_float(v.w);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < S; ++q)
+#pragma unroll
+          for (int a = 0; a < A; ++a) sts_f32(tile + 4u * (uint32_t)(a * R + q * 32 + lane), f[q][a]);
+        __syncwarp();
+      }
+      const uint32_t amask_t = (1u << abits_t) - 1u;
+      uint32_t thr[S], meta[S], bx[S];
+      const uint2 root = tree.get(tree.root());
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        bx[q] = tile + 4u * (uint32_t)(q * 32 + lane);
+        thr[q] = root.x;
+        meta[q] = (r0 + q * 32 + lane < m) ? root.y : kLeafBit;
+      }
+      while (true) {
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < S; ++q) any |= (int)meta[q] >= 0;
+        if (!any) break;
+#pragma unroll
+        for (int q = 0; q < S; ++q) data_step_t(thr[q], meta[q], bx[q], amask_t, abits_t);
+      }
+#pragma unroll
+      for (int q = 0; q < S; ++q) {  // folded terminal (unscaled 4*attr in its low bits)
+        if (meta[q] & kPairBit) {
+          const float v = lds_f32(bx[q] + ((meta[q] & 0x3FFu) << kLR));
+          const uint32_t c = (v > __uint_as_float(thr[q])) ? (meta[q] >> 20) : (meta[q] >> 10);
+          meta[q] = kLeafBit | (c & 0x3FFu);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const uint64_t r = r0 + q * 32 + lane;
+        if (r < m) {
+          const uint32_t c = meta[q] & ~kLeafBit;
+          args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+        }
       }
     } else if constexpr (TLOC == kSharedReg && LOADER == kTma && (A == 8 || A == 16)) {
       // records -> registers (A/4 conflict-free lds.128 each), tile freed at once

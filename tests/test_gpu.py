@@ -20,7 +20,8 @@ DATA_GEOMS = [st.GpuGeom(algo="data"),
               st.GpuGeom(algo="data", tree_loc="global"),
               st.GpuGeom(algo="data", tree_loc="constant"),
               st.GpuGeom(algo="data", record_regs=1, samples_per_thread=2),   # 8/16 attrs from registers
-              st.GpuGeom(algo="data", record_regs=2, stages=3)]
+              st.GpuGeom(algo="data", record_regs=2, stages=3),
+              st.GpuGeom(algo="data", record_regs=3, samples_per_thread=4)]   # transposed tiles
 SPEC_GEOMS = [st.GpuGeom(algo="speculative"),
               st.GpuGeom(algo="speculative", group_lanes=4),
               st.GpuGeom(algo="speculative", group_lanes=8),
@@ -383,7 +384,9 @@ def test_folded_tree_walks(cuda, co, fold_min, monkeypatch):
     fold forced on for every tree size (ST_DATA_FOLD_MIN=1) and off."""
     monkeypatch.setenv("ST_DATA_FOLD_MIN", fold_min)
     geoms = [st.GpuGeom(algo="data"), st.GpuGeom(algo="data", record_regs=2),
-             st.GpuGeom(algo="data", record_regs=1, samples_per_thread=1)]
+             st.GpuGeom(algo="data", record_regs=1, samples_per_thread=1),
+             st.GpuGeom(algo="data", record_regs=3),                          # transposed tiles
+             st.GpuGeom(algo="data", record_regs=3, samples_per_thread=2, stages=1)]
     for leaves in range(1, 9):
         for shape in support.all_shapes(leaves):
             internal = support.assign_labels(shape)

@@ -59,6 +59,11 @@ if "small" in args.grid:
     for S, ns, w, bps in itertools.product([0, 1, 2, 4], [0, 3], [0, 8, 16], [0, 1, 2, 4]):
         geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, stages=ns, warps_per_cta=w,
                                 blocks_per_sm=bps))
+if "trans" in args.grid:  # transposed (attribute-major) tiles vs the defaults
+    geoms.append(st.GpuGeom(algo="data"))
+    for S, ns, w, bps in itertools.product([1, 2, 4], [1, 2], [0, 8], [0, 4]):
+        geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, record_regs=3, stages=ns,
+                                warps_per_cta=w, blocks_per_sm=bps))
 if "stages" in args.grid:
     for S, ns, w in itertools.product([0, 1, 2, 4], [2, 3, 4], [0, 16, 24]):
         geoms.append(st.GpuGeom(algo="data", samples_per_thread=S, stages=ns, warps_per_cta=w))
