@@ -98,7 +98,9 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.bulk_tree = env_u32("ST_TREE_BULK", 1) ? 1u : 0u;
 
   // fewer than 8 tiles of 32 records per warp at 32 warps on every SM
-  const bool small = m < (uint64_t)pr.sms * 32 * 8 * 32;
+  // (trees read through L1 / the constant bank keep S = 1 as well)
+  const bool small = m < (uint64_t)pr.sms * 32 * 8 * 32 || g.tree_loc == ST_TREE_GLOBAL ||
+                     g.tree_loc == ST_TREE_CONSTANT;
 
   // the folded tree (leaf pairs inside terminals) serves the shared-tree TMA
   // walks over 8/16/32-attribute records of large trees; every other path

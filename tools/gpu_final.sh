@@ -13,3 +13,8 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_sp
 timeout 1200 python tools/workloads.py --flush read > $OUT/workloads_$TAG.log 2>&1; tail -1 $OUT/workloads_$TAG.log | cut -c1-200
 timeout 1200 python tools/c5_sweep.py --gpus 1 > $OUT/c5_sweep_$TAG.log 2>&1; tail -1 $OUT/c5_sweep_$TAG.log | cut -c1-200
 ls $OUT | wc -l
+# per-config captures of the data kernel (C1 / C3 small-input paths, C5 d16 deep tree)
+for W in C1 C3 C5d16; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_data -s 2 -c 1 -o $OUT/prof_${W}_data_$TAG -f python tools/prof_one.py $W data 4 > $OUT/prof_${W}_data_$TAG.log 2>&1
+done
+ls $OUT | wc -l
