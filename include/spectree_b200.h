@@ -85,7 +85,7 @@ typedef struct st_geom {
   uint32_t warps_per_cta;      /* CTA width in warps, 1-32 (0 = auto) */
   uint32_t pipeline;           /* speculative record staging: 0 = auto (CTA-shared ticketed TMA
                                   ring), 1 = per-warp TMA ring */
-  uint32_t record_regs;        /* data kernel, 8/16-attribute records: 0 = auto (registers for 8),
+  uint32_t record_regs;        /* data kernel, 8/16-attribute records: 0 = auto (transposed tile for 8),
                                   1 = walk from registers (tile released right after loading),
                                   2 = walk from the shared tile,
                                   3 = transpose each tile in place to attribute-major, then walk it */

@@ -91,10 +91,14 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.leaf_class = dv.leaf_tbl;
   d.labels = labels;
   // records walked from registers: default for 8-attribute records; 16 on request
-  d.record_regs = (g.record_regs == 1 || (g.record_regs == 0 && a == 8)) ? 1u : 0u;
-  // attribute-major (transposed) tiles instead of register records
-  if ((a == 8 || a == 16) && (g.record_regs == 3 || (g.record_regs == 0 && env_u32("ST_DATA_TRANSPOSE", 0))))
-    d.record_regs = 2;
+  // 8/16-attribute records: walk from registers (1), from the record-major
+  // shared tile (0), or from the tile transposed in place to attribute-major
+  // (2) -- the default for 8 attributes (C3: -4 % per frame, -0.6 % on 32
+  // frames vs registers; profiles/r1_ab_stages.txt); 16-attribute records
+  // walk the record-major tile (C5 d12 / d16: transposed +10 / +11 %)
+  d.record_regs = g.record_regs == 1 ? 1u : 0u;
+  if ((a == 8 || a == 16) && (g.record_regs == 3 || (g.record_regs == 0 && a == 8)))
+    d.record_regs = env_u32("ST_DATA_TRANSPOSE", 1) ? 2u : 1u;
   d.bulk_tree = env_u32("ST_TREE_BULK", 1) ? 1u : 0u;
 
   // fewer than 8 tiles of 32 records per warp at 32 warps on every SM
@@ -154,10 +158,9 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     want_bps = 4;
   }
   // transposed tiles: the scaled attribute field widens the meta's low part
-  // by log2(32 S) bits; the absolute child address must still fit below bit 31
+  // by log2(32) bits; the absolute child address must still fit below bit 31
   if (d.record_regs == 2) {
-    const uint32_t lr = stg.S == 4 ? 7u : stg.S == 2 ? 6u : 5u;
-    if (stg.loader != kTma || ((uint64_t)pr.smem_optin << (t->abits + lr)) >= (1ull << 31)) d.record_regs = 0;
+    if (stg.loader != kTma || ((uint64_t)pr.smem_optin << (t->abits + 5u)) >= (1ull << 31)) d.record_regs = 0;
   }
   d.ns = stg.ns;
   d.stage_bytes = stg.stage_bytes;

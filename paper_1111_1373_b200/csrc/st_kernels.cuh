@@ -279,7 +279,11 @@ struct Pipe {
   }
 
   // Done with this warp's i-th tile: refill its stage with tile t + ns*step.
+  // Every lane's generic-proxy accesses to the stage (reads; the transposed
+  // walk's stores) are ordered before lane 0's async-proxy TMA write by a
+  // proxy fence on each lane, then the warp barrier.
   __device__ __forceinline__ void release(uint64_t i, uint64_t t, uint64_t step, uint64_t n_tiles) {
+    if constexpr (LOADER == kTma) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if constexpr (LOADER == kTma) {
       if (lane == 0) {
@@ -462,8 +466,8 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t amask = (1u << args.abits) - 1u;
 
   // ---- stage the node array once per CTA --------------------------------
-  constexpr uint32_t kLR = S == 4 ? 7u : S == 2 ? 6u : 5u;  // log2(R)
-  // kSharedT: internal meta = (abs child << abits_t) | 4*attr*R
+  constexpr uint32_t kLR = 5u;  // kSharedT: attribute stride 32 records (log2)
+  // kSharedT: internal meta = (abs child << abits_t) | 4*attr*32
   const uint32_t abits_t = args.abits + (TLOC == kSharedT ? kLR : 0u);
   if constexpr (TLOC == kShared || TLOC == kSharedReg || TLOC == kSharedT) {
     const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
@@ -536,37 +540,35 @@ __global__ void __launch_bounds__(kMaxThreads)
         args.labels[r0 + r] = nd.w;
       }
     } else if constexpr (TLOC == kSharedT && LOADER == kTma && (A == 8 || A == 16)) {
-      // transpose the warp's tile in place to attribute-major: slot (a, r)
-      // at 4*(a*R + r), r = q*32 + lane -- every later feature read by lane l
-      // hits bank l whatever the attribute (the record-major tile puts
-      // 128/(4A) records in a row and conflicts on random attributes)
-      {
-        float f[S][A];
+      // transpose the warp's tile in place, one 32-record chunk at a time, to
+      // attribute-major: chunk q's (a, lane) at 4*(q*32*A + a*32 + lane) --
+      // every later feature read by lane l hits bank l
+      // whatever the attribute (the record-major tile puts 128/(4A) records in
+      // a row and conflicts on random attributes).  Chunk-local, so only A
+      // floats are live at a time.
 #pragma unroll
-        for (int q = 0; q < S; ++q) {
-          const uint32_t b = (uint32_t)(q * 32 + lane) * (4u * A);
+      for (int q = 0; q < S; ++q) {
+        float f[A];
+        const uint32_t b = (uint32_t)(q * 32 + lane) * (4u * A);
 #pragma unroll
-          for (int c = 0; c < A / 4; ++c) {
-            const uint4 v = lds_u4(tile + swz(b + 16u * c));
-            f[q][4 * c + 0] = __uint_as_float(v.x);
-            f[q][4 * c + 1] = __uint_as_float(v.y);
-            f[q][4 * c + 2] = __uint_as_float(v.z);
-            f[q][4 * c + 3] = __uint_as_float(v.w);
-          }
+        for (int c = 0; c < A / 4; ++c) {
+          const uint4 v = lds_u4(tile + swz(b + 16u * c));
+          f[4 * c + 0] = __uint_as_float(v.x);
+          f[4 * c + 1] = __uint_as_float(v.y);
+          f[4 * c + 2] = __uint_as_float(v.z);
+          f[4 * c + 3] = __uint_as_float(v.w);
         }
         __syncwarp();
 #pragma unroll
-        for (int q = 0; q < S; ++q)
-#pragma unroll
-          for (int a = 0; a < A; ++a) sts_f32(tile + 4u * (uint32_t)(a * R + q * 32 + lane), f[q][a]);
-        __syncwarp();
+        for (int a = 0; a < A; ++a) sts_f32(tile + 4u * (uint32_t)(q * 32 * A + a * 32 + lane), f[a]);
       }
+      __syncwarp();
       const uint32_t amask_t = (1u << abits_t) - 1u;
       uint32_t thr[S], meta[S], bx[S];
       const uint2 root = tree.get(tree.root());
 #pragma unroll
       for (int q = 0; q < S; ++q) {
-        bx[q] = tile + 4u * (uint32_t)(q * 32 + lane);
+        bx[q] = tile + 4u * (uint32_t)(q * 32 * A + lane);
         thr[q] = root.x;
         meta[q] = (r0 + q * 32 + lane < m) ? root.y : kLeafBit;
       }
@@ -1258,6 +1260,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     } else {
       static_assert(SR >= 0 && SR <= 2, "one window, or one or two record streams per group");
     }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA refill
     __syncwarp();
     if (tk + NS < my_tiles) {
       fill(tk + NS);  // this warp freed slot b: refill it ...

@@ -56,7 +56,7 @@ class GpuGeom:
     stages: int = 0                 # TMA record-pipeline stages per warp
     warps_per_cta: int = 0          # CTA width (warps)
     pipeline: int = 0               # 0 auto, 1 per-warp TMA ring, 2 CTA-shared ring (spec)
-    record_regs: int = 0            # data, 8/16-attribute records: 0 auto, 1 registers, 2 shared tile, 3 transposed tile
+    record_regs: int = 0            # data, 8/16-attribute records: 0 auto (3 for 8), 1 registers, 2 shared tile, 3 transposed tile
 
     def to_c(self) -> st_geom:
         g = st_geom()

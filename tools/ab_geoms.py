@@ -1,5 +1,5 @@
 """A/B data-kernel geometries on canonical workloads (development aid):
-    python tools/ab_geoms.py W1,W2 'dict(record_regs=3, samples_per_thread=2, stages=1)' ... [--flush]
+    python tools/ab_geoms.py W1,W2 'dict(record_regs=3, samples_per_thread=2, stages=1)' ... [--flush] [--tile=N]
 Alternates the geometries for 5 rounds on one box; prints per-geometry ms."""
 import os
 import sys
@@ -14,21 +14,25 @@ import paper_1111_1373_b200 as st  # noqa: E402
 import workloads  # noqa: E402
 
 flush = "--flush" in sys.argv
-args = [a for a in sys.argv[1:] if a != "--flush"]
+tile = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--tile=")), 1))
+args = [a for a in sys.argv[1:] if a != "--flush" and not a.startswith("--tile=")]
 names, specs = args[0].split(","), ["dict()"] + args[1:]
 fl = workloads.make_flush() if flush else None
 for name in names:
     w = bench.WORKLOADS[name]
     tree = st.generate_synthetic_tree(*w["tree"])
-    xd = torch.from_numpy(st.generate_synthetic_dataset(w["m"], w["a"], w["seed"])).cuda()
-    out = torch.empty(w["m"], dtype=torch.int32, device="cuda")
+    x = st.generate_synthetic_dataset(w["m"], w["a"], w["seed"])
+    xd = torch.from_numpy(x).cuda().repeat(tile, 1)
+    out = torch.empty(len(xd), dtype=torch.int32, device="cuda")
     geoms = [st.GpuGeom(algo="data", **eval(s)) for s in specs]
     res = {s: [] for s in specs}
     for g, s in zip(geoms, specs):
         st.eval_device(tree, xd, out, g)
         torch.cuda.synchronize()
-        assert st.fnv1a64(out.cpu().numpy()) == w["labels_fnv"], (name, s)
+        assert st.fnv1a64(out[: w["m"]].cpu().numpy()) == w["labels_fnv"], (name, s)
+        if tile > 1:
+            assert torch.equal(out.view(tile, -1), out[: w["m"]].expand(tile, -1)), (name, s)
     for _ in range(5):
         for g, s in zip(geoms, specs):
             res[s].append(round(workloads.graph_time(lambda: st.eval_device(tree, xd, out, g), 20, fl) * 1e3, 2))
-    print(name, {s: (min(v), sorted(v)[2]) for s, v in res.items()}, "us (min, median)", flush=True)
+    print(name, f"x{tile}", {s: (min(v), sorted(v)[2]) for s, v in res.items()}, "us (min, median)", flush=True)

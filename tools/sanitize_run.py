@@ -30,6 +30,7 @@ for targs, a in cases:
     geoms = [st.GpuGeom(algo="data", tree_loc=tl, samples_per_thread=s)
              for tl in ("shared", "global", "constant") for s in (1, 2, 4)]
     geoms += [st.GpuGeom(algo="data", record_regs=1, samples_per_thread=s) for s in (1, 2)]
+    geoms += [st.GpuGeom(algo="data", record_regs=3, samples_per_thread=s, stages=n) for s in (1, 4) for n in (1, 2)]
     geoms += [st.GpuGeom(algo="speculative", pipeline=p, group_lanes=g) for p in (1, 2) for g in (0, 2, 8)]
     geoms += [st.GpuGeom(algo="speculative", samples_per_thread=2, group_lanes=g) for g in (2, 4)]
     for g in geoms:
