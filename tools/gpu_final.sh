@@ -18,3 +18,8 @@ for W in C1 C3 C5d16; do
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_data -s 2 -c 1 -o $OUT/prof_${W}_data_$TAG -f python tools/prof_one.py $W data 4 > $OUT/prof_${W}_data_$TAG.log 2>&1
 done
 ls $OUT | wc -l
+# compute-sanitizer over every kernel family (small launches)
+mkdir -p $OUT/san
+for T in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $T python tools/sanitize_run.py 3000 > $OUT/san/r1_$T.log 2>&1; echo "$T rc=$?"
+done
