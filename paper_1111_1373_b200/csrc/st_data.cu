@@ -12,7 +12,23 @@ void launch_data_t(const DataArgs& d, const Staging& stg, const ConstTree<CAP>* 
   const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles, stg.warps);
   static const ConstTree<1> dummy{};
   clear_stale_error();
-  if constexpr (CAP == 1) {
+  if (d.pdl) {
+    // programmatic dependent launch: the prologue (barrier init, tree copy)
+    // may overlap the previous kernel in the stream; the kernel waits for it
+    // (griddepcontrol.wait) before touching records or labels
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(stg.warps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if constexpr (CAP == 1) CK(cudaLaunchKernelEx(&cfg, fn, d, stg.tmap, ct ? *ct : dummy));
+    else CK(cudaLaunchKernelEx(&cfg, fn, d, stg.tmap, *ct));
+  } else if constexpr (CAP == 1) {
     fn<<<blocks, stg.warps * 32, smem, s>>>(d, stg.tmap, ct ? *ct : dummy);
   } else {
     fn<<<blocks, stg.warps * 32, smem, s>>>(d, stg.tmap, *ct);
@@ -101,6 +117,7 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     d.record_regs = env_u32("ST_DATA_TRANSPOSE", 1) ? 2u : 1u;
   d.bulk_tree = env_u32("ST_TREE_BULK", 1) ? 1u : 0u;
 
+
   // fewer than 8 tiles of 32 records per warp at 32 warps on every SM
   // (trees read through L1 / the constant bank keep S = 1 as well)
   const bool small = m < (uint64_t)pr.sms * 32 * 8 * 32 || g.tree_loc == ST_TREE_GLOBAL ||
@@ -172,6 +189,18 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.tree_bytes = tloc == ST_TREE_SHARED ? tree_bytes : 0;
   const size_t smem = 1024 + d.tree_bytes + stg.tile_smem();
   const uint32_t bps = default_bps(want_bps, stg, m, pr);
+  // Programmatic dependent launch: the prologue (barrier init, tree copy)
+  // overlaps the previous kernel's tail.  Dependents are triggered early only
+  // when one of their CTAs fits beside the ones launched per SM (small inputs:
+  // C1 -6 % per launch in a back-to-back stream); otherwise the trigger is the
+  // implicit one at exit (C1 / C3 -2 %; an early trigger without room cost
+  // C3 +5 %; tools/pdl_ab.py, profiles/r1_pdl_ab.txt).  ST_PDL: 0 off, 1 early,
+  // 2 at exit.
+  {
+    const size_t cta = smem + 1024;  // + the per-CTA shared-memory reservation
+    const bool room = bps > 0 && (size_t)(bps + 1) * cta <= pr.smem_per_sm;
+    d.pdl = env_u32("ST_PDL", room ? 1u : 2u);
+  }
   if (stg.loader == kTma && ct_arity(a)) {
     switch (a) {
       case 8: return launch_data_a<8>(stg, tloc, d, t, smem, dev, bps, s);

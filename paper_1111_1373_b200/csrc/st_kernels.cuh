@@ -340,6 +340,7 @@ struct DataArgs {
   uint32_t stage_bytes;        // stride between stages
   uint32_t record_regs;        // host hint: 8-attribute records walk from registers (kSharedReg)
   uint32_t bulk_tree;          // stage the shared tree with one cp.async.bulk (else per-thread loads)
+  uint32_t pdl;                // launched as a programmatic dependent (griddepcontrol)
 };
 
 // Shared-memory carve-out shared by the kernels:
@@ -460,35 +461,43 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint64_t n_tiles = (m + R - 1) / R;
   const uint64_t step = (uint64_t)gridDim.x * nw;
   const uint64_t first = (uint64_t)blockIdx.x * nw + warp;
-  // first record tiles in flight before the tree is staged (the TMA does not
-  // depend on it): the tree copy hides under the DRAM latency of the records
-  pipe.start(first, step, n_tiles);
   const uint32_t amask = (1u << args.abits) - 1u;
+  constexpr bool kSmemTree = (TLOC == kShared || TLOC == kSharedReg || TLOC == kSharedT);
+  const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
+  const uint32_t n16 = (args.n_nodes * 8u + 15u) / 16u;
+  // The tree bulk copy: one DRAM/L2 round trip for the whole array, in flight
+  // beside the first record tiles, then an in-place rebase pass over shared
+  // memory (a per-thread ld.global -> st.shared loop serialises one round trip
+  // per iteration).  Its mbarrier sits after the per-warp stage barriers,
+  // inside the 1024 B alignment reserve of the carve-out.
+  const uint32_t tbar = tiles0 + (LOADER == kDirect ? 0u : nw * args.ns * (args.stage_bytes + 8u));
+  if (kSmemTree && args.bulk_tree && threadIdx.x == 0) {
+    mbar_init(tbar, 1);
+    fence_barrier_init();
+    mbar_arrive_expect_tx(tbar, 16u * n16);
+    bulk_load(sbase, src, 16u * n16, tbar);
+  }
+  // Programmatic dependent launch (args.pdl): everything above reads only the
+  // tree (immutable after st_tree_create) -- records and labels are touched
+  // after the previous grid in the stream has completed; dependents may be
+  // scheduled from here on (they wait for this grid's completion in turn).
+  if (args.pdl) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (args.pdl == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
+  // first record tiles in flight before the tree is rebased (the TMA does not
+  // depend on it)
+  pipe.start(first, step, n_tiles);
 
   // ---- stage the node array once per CTA --------------------------------
   constexpr uint32_t kLR = 5u;  // kSharedT: attribute stride 32 records (log2)
   // kSharedT: internal meta = (abs child << abits_t) | 4*attr*32
   const uint32_t abits_t = args.abits + (TLOC == kSharedT ? kLR : 0u);
-  if constexpr (TLOC == kShared || TLOC == kSharedReg || TLOC == kSharedT) {
-    const uint4* src = reinterpret_cast<const uint4*>(args.nodes);
-    const uint32_t n16 = (args.n_nodes * 8u + 15u) / 16u;
+  if constexpr (kSmemTree) {
     const uint32_t rebase = sbase << args.abits;  // child offset -> absolute address
     if (args.bulk_tree) {
-      // one bulk copy (a single DRAM/L2 round trip for the whole array, in
-      // flight beside the first record tiles), then an in-place rebase pass
-      // over shared memory.  The per-thread loop below serialises one
-      // round trip per iteration (the shared store orders the next load).
-      // its mbarrier sits after the per-warp stage barriers, inside the
-      // 1024 B alignment reserve of the carve-out (no static shared memory)
-      const uint32_t bar = tiles0 + (LOADER == kDirect ? 0u : nw * args.ns * (args.stage_bytes + 8u));
-      if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        fence_barrier_init();
-        mbar_arrive_expect_tx(bar, 16u * n16);
-        bulk_load(sbase, src, 16u * n16, bar);
-      }
-      __syncthreads();
-      mbar_wait(bar, 0);
+      __syncthreads();  // the barrier's init is visible before anyone waits on it
+      mbar_wait(tbar, 0);
       for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) {
         uint4 v = lds_u4(sbase + 16u * i);
         if constexpr (TLOC == kSharedT) {

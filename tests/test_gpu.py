@@ -470,3 +470,26 @@ def test_spec_window_formats(cuda, co, wide, monkeypatch):
                   st.GpuGeom(algo="speculative", group_lanes=(2, 4, 8, 16)[seed % 4],
                              samples_per_thread=1 + seed % 2)):
             assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, m, g)
+
+
+@pytest.mark.parametrize("pdl", ["0", "1", "2"])
+def test_programmatic_dependent_launch_ordering(cuda, co, pdl, monkeypatch):
+    """Data launches are programmatic dependents of the previous kernel in
+    the stream: records written by that kernel (an elementwise torch kernel
+    here, no host sync in between) must be read only after it completed, and
+    labels must not be overwritten early.  Small inputs with room for a
+    dependent CTA (early trigger), large ones (trigger at exit), forced off."""
+    monkeypatch.setenv("ST_PDL", pdl)
+    for depth, leaves, a, m in ((10, 1024, 16, 300_000), (12, 2048, 8, 200_000), (24, 256, 32, 2_000_000)):
+        nodes = co.gen_tree(depth, leaves, a, 8, 900 + depth)
+        tree = st.EncodedTree(nodes)
+        srcs = [torch.from_numpy(co.gen_dataset(m, a, 910 + k)).to(cuda) for k in range(4)]
+        wants = [co.eval_serial(nodes, s.cpu().numpy()) for s in srcs]
+        xd = torch.empty_like(srcs[0])
+        outs = [torch.empty(m, dtype=torch.int32, device=cuda) for _ in srcs]
+        for s, o in zip(srcs, outs):
+            torch.add(s, 0.0, out=xd)  # producer kernel immediately before the launch
+            st.eval_device(tree, xd, o, st.GpuGeom(algo="data"))
+        torch.cuda.synchronize()
+        for o, want in zip(outs, wants):
+            assert np.array_equal(o.cpu().numpy().view(np.uint32), want), (depth, pdl)
