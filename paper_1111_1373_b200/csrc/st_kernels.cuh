@@ -1133,12 +1133,31 @@ __global__ void __launch_bounds__(kMaxThreads)
         // same speculation), and the lane whose leaf path mask matches --
         // exactly one per group in a tree -- stores its class.  No shuffles.
         const uint32_t gsh = g * G;
+        if (rows == 32u) {
+          // full tile (warp-uniform): no row clamp, the feature and label
+          // addresses advance by a constant per record, and the path masks
+          // are pre-shifted to the group's lanes -- the loop is issue-bound,
+          // so every instruction per record counts
+          const uint32_t want = pm1.w << gsh, care = pm1.z << gsh;
+          const bool has_leaf = pm1.y != 0u;
+          const uint32_t a4 = 4u * (A > 0 ? (uint32_t)A : args.p.a);
+          const uint32_t df = NG * a4, dl = 4u * NG;
+          uint32_t f = tile + g * a4 + attr4, la = lbuf + 4u * g;
 #pragma unroll 4
-        for (uint32_t r = g; r < 32u; r += NG) {
-          const float v = feature(r);
-          const uint32_t preds = __ballot_sync(0xffffffffu, v > __uint_as_float(thr)) >> gsh;
-          if (pm1.y != 0u && ((preds ^ pm1.w) & pm1.z) == 0u && r < rows)
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(pm1.y) : "memory");
+          for (uint32_t r = g; r < 32u; r += NG, f += df, la += dl) {
+            const float v = lds_f32(f ^ ((f >> 3) & 0x70u));  // swizzled (tile 1024-aligned)
+            const uint32_t preds = __ballot_sync(0xffffffffu, v > __uint_as_float(thr));
+            if (has_leaf && ((preds ^ want) & care) == 0u)
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(la), "r"(pm1.y) : "memory");
+          }
+        } else {
+#pragma unroll 4
+          for (uint32_t r = g; r < 32u; r += NG) {
+            const float v = feature(r);
+            const uint32_t preds = __ballot_sync(0xffffffffu, v > __uint_as_float(thr)) >> gsh;
+            if (pm1.y != 0u && ((preds ^ pm1.w) & pm1.z) == 0u && r < rows)
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(pm1.y) : "memory");
+          }
         }
       } else {
 #pragma unroll 4
