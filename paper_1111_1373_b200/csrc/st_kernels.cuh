@@ -773,7 +773,8 @@ struct SpecArgs {
   uint32_t cw_amask, cw_lsh, cw_rsh, cw_cmask, cw_leaf, cw_emask, cw_wstride;
 };
 
-// Window codes: lane index (< 32), kExitBit | byte offset of the next
+// Window codes: lane index (< 32; a width-G shuffle uses its low log2(G)
+// bits as the group lane), kExitBit | byte offset of the next
 // window's first entry, or kLeafBit | class.  Every lane of a record group
 // evaluates its window node's predicate (speculatively: all of them, not
 // just the ones on the path), then ceil(log2 h) __shfl_sync pointer-jumping
@@ -821,7 +822,6 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t NG = 32u / G;        // record groups per warp
   const uint32_t g = lane / G;        // my group
   const uint32_t j = lane & (G - 1);  // my lane in the group = window-local node
-  const uint32_t gmask = G - 1;
   // byte address of my entry in window 0 (codes carry window byte offsets)
   const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + 16u * j;
   const char* wglob = reinterpret_cast<const char*>(args.win) + 16u * j;
@@ -867,12 +867,12 @@ __global__ void __launch_bounds__(kMaxThreads)
           if constexpr (STEPS >= 0) {
 #pragma unroll
             for (int s = 0; s < STEPS; ++s) {
-              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c, G);
               c = (c < 32u) ? u : c;
             }
           } else {
             for (uint32_t s = 0; s < args.smax; ++s) {
-              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c, G);
               c = (c < 32u) ? u : c;
             }
           }
@@ -885,7 +885,7 @@ __global__ void __launch_bounds__(kMaxThreads)
             const bool need = rt < 32u;
             if (!__any_sync(0xffffffffu, need)) break;
             for (uint32_t s = 0; s < args.k; ++s) {
-              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c, G);
               if (need && c < 32u) c = u;
             }
             if (need && active) {
@@ -1030,7 +1030,6 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t NG = 32u / G;
   const uint32_t g = lane / G;
   const uint32_t j = lane & (G - 1);
-  const uint32_t gmask = G - 1;
   const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + (CW ? 8u : 16u) * j;
   const char* wglob = reinterpret_cast<const char*>(args.win) + 16u * j;
   if constexpr (WIN_SHARED) {  // window table staged
@@ -1047,9 +1046,11 @@ __global__ void __launch_bounds__(kMaxThreads)
   // wavefronts of the entry loads.
   struct Ent { uint32_t thr, w, l, r; };
   const uint32_t leafbit = CW ? args.cw_leaf : kLeafBit;
+  // CW: `woff` is the window index (entry address = one IMAD); otherwise a
+  // byte offset
   auto load_ent = [&](uint32_t woff) -> Ent {
     if constexpr (CW) {
-      const uint2 t = lds_u2(jaddr + woff);
+      const uint2 t = lds_u2(jaddr + woff * args.cw_wstride);
       return {t.x, t.y, 0u, 0u};
     } else {
       uint4 t;
@@ -1067,7 +1068,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     else return right ? e.r : e.l;
   };
   auto exit_off = [&](uint32_t root) -> uint32_t {
-    if constexpr (CW) return (root & args.cw_emask) * args.cw_wstride;
+    if constexpr (CW) return root & args.cw_emask;
     else return root & ~kExitBit;
   };
   // SR == 0: the whole tree is one window (the paper's Proc. 5 geometry):
@@ -1167,12 +1168,12 @@ __global__ void __launch_bounds__(kMaxThreads)
           if constexpr (STEPS >= 0) {
 #pragma unroll
             for (int st = 0; st < STEPS; ++st) {
-              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c, G);
               c = (c < 32u) ? u : c;
             }
           } else {
             for (uint32_t st = 0; st < args.smax; ++st) {
-              const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+              const uint32_t u = __shfl_sync(0xffffffffu, c, c, G);
               c = (c < 32u) ? u : c;
             }
           }
@@ -1206,12 +1207,12 @@ __global__ void __launch_bounds__(kMaxThreads)
         if constexpr (STEPS >= 0) {
 #pragma unroll
           for (int st = 0; st < STEPS; ++st) {
-            const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+            const uint32_t u = __shfl_sync(0xffffffffu, c, c, G);
             c = (c < 32u) ? u : c;
           }
         } else {
           for (uint32_t st = 0; st < args.smax; ++st) {
-            const uint32_t u = __shfl_sync(0xffffffffu, c, c & gmask, G);
+            const uint32_t u = __shfl_sync(0xffffffffu, c, c, G);
             c = (c < 32u) ? u : c;
           }
         }
@@ -1253,8 +1254,8 @@ __global__ void __launch_bounds__(kMaxThreads)
         uint32_t cA = ent_next(eA, vA > __uint_as_float(eA.thr));
         uint32_t cB = ent_next(eB, vB > __uint_as_float(eB.thr));
         auto jump = [&]() {
-          const uint32_t uA = __shfl_sync(0xffffffffu, cA, cA & gmask, G);
-          const uint32_t uB = __shfl_sync(0xffffffffu, cB, cB & gmask, G);
+          const uint32_t uA = __shfl_sync(0xffffffffu, cA, cA, G);
+          const uint32_t uB = __shfl_sync(0xffffffffu, cB, cB, G);
           cA = (cA < 32u) ? uA : cA;
           cB = (cB < 32u) ? uB : cB;
         };
