@@ -61,6 +61,10 @@ def inputs(name, gen_tree, gen_data):
 def run():
     import torch
 
+    # The reference model walks node by node; a folded tree (leaf pairs inside
+    # terminal nodes) skips the last level's node load by
+    # construction, so the cross-check runs the unfolded walk.
+    os.environ["ST_DATA_NO_FOLD"] = "1"
     import paper_1111_1373_b200 as st
 
     order = []
