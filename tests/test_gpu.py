@@ -493,3 +493,22 @@ def test_programmatic_dependent_launch_ordering(cuda, co, pdl, monkeypatch):
         torch.cuda.synchronize()
         for o, want in zip(outs, wants):
             assert np.array_equal(o.cpu().numpy().view(np.uint32), want), (depth, pdl)
+
+
+@pytest.mark.parametrize("bulk", ["0", "1"])
+def test_tree_staging_paths(cuda, co, bulk, monkeypatch):
+    """Shared trees / window tables staged by one cp.async.bulk (default) or
+    by the per-thread copy loop (ST_TREE_BULK=0): identical labels for the
+    record-major, attribute-major and register walks, folded and plain trees,
+    and the speculative ring (8- and 16-byte window tables, one window)."""
+    monkeypatch.setenv("ST_TREE_BULK", bulk)
+    geoms = [st.GpuGeom(algo="data"), st.GpuGeom(algo="data", record_regs=1),
+             st.GpuGeom(algo="data", record_regs=3), st.GpuGeom(algo="data", record_regs=2),
+             st.GpuGeom(algo="speculative"), st.GpuGeom(algo="speculative", samples_per_thread=1)]
+    for depth, leaves, a, seed in ((10, 1024, 16, 31), (12, 2048, 8, 32), (24, 256, 32, 33), (11, 16, 19, 1)):
+        nodes = co.gen_tree(depth, leaves, a, 8, seed)
+        x = co.gen_dataset(50_001, a, seed + 100)
+        want = co.eval_serial(nodes, x)
+        xd = torch.from_numpy(x).to(cuda)
+        for g in geoms:
+            assert np.array_equal(_dev_eval(nodes, xd, g, len(x)), want), (depth, a, g, bulk)
