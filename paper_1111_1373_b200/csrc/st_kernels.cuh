@@ -948,15 +948,20 @@ struct SpecRingArgs {
   uint32_t n_slots;       // NS
   uint32_t unsafe_no_gen; // benchmark-only: skip the slot-generation handshake
   uint32_t bulk_win;      // stage the window table with one cp.async.bulk (else per-thread loads)
+  uint32_t tile_mult;     // host: records per ring slot / 32 (the kernel's RT)
 };
 
-template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false>
+// RT: records per ring slot / 32.  Two-stream groups over 64-record slots
+// (RT = 2) walk 4 records per stream instead of 2, which evens out the
+// streams' window counts on skewed trees and halves the per-slot overhead.
+template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false, int RT = 1>
 __global__ void __launch_bounds__(kMaxThreads)
     k_spec_ring(const SpecRingArgs ra, const __grid_constant__ CUtensorMap tmap) {
   static_assert(!CW || (WIN_SHARED && SR >= 1), "8-byte windows: shared table, window-loop paths");
+  static_assert(RT == 1 || SR == 2, "multi-chunk slots: two-stream loop only");
   extern __shared__ __align__(1024) unsigned char smem[];
   const SpecArgs& args = ra.s;
-  constexpr int R = 32;
+  constexpr int R = 32 * RT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t NS = ra.n_slots;
   const uint32_t sbase = align1024(smem_u32(smem));
@@ -967,7 +972,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t gen0 = full0 + 8u * NS;
   const uint32_t ticket = gen0 + ((4u * NS + 15u) & ~15u);
   uint32_t lbuf;  // opaque copy: keeps the per-warp label row in a register (no S2R remat in the walk)
-  asm("mov.u32 %0, %1;" : "=r"(lbuf) : "r"(ticket + 16u + (uint32_t)warp * 128u));
+  asm("mov.u32 %0, %1;" : "=r"(lbuf) : "r"(ticket + 16u + (uint32_t)warp * (4u * R)));
 
   const uint64_t m = args.p.m;
   const uint64_t n_tiles = (m + R - 1) / R;
@@ -1110,8 +1115,11 @@ __global__ void __launch_bounds__(kMaxThreads)
     }
     mbar_wait(full0 + 8u * b, (tk / NS) & 1u);
     if (args.root_code & kLeafBit) {  // N == 1
-      if (lane < rows)
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * lane), "r"(args.root_code) : "memory");
+#pragma unroll
+      for (int k = 0; k < RT; ++k)
+        if (lane + 32u * k < rows)
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * (lane + 32u * k)), "r"(args.root_code)
+                       : "memory");
     } else if constexpr (SR == 0) {
       // One window: every record resolves in one pass, so the passes over
       // the tile's records are independent chains (feature load -> compare
@@ -1296,11 +1304,15 @@ __global__ void __launch_bounds__(kMaxThreads)
       if (lane == 0)  // ... and publish that generation tk / NS + 1 is on its way
         asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(tk / NS + 1u) : "memory");
     }
-    if (lane < rows) {
-      uint32_t code;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(code) : "r"(lbuf + 4u * lane));
-      const uint32_t cls = code & (leafbit - 1u);
-      args.labels[r0 + lane] = args.leaf_class ? __ldg(args.leaf_class + cls) : cls;
+#pragma unroll
+    for (int k = 0; k < RT; ++k) {
+      const uint32_t rr = lane + 32u * k;
+      if (rr < rows) {
+        uint32_t code;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(code) : "r"(lbuf + 4u * rr));
+        const uint32_t cls = code & (leafbit - 1u);
+        args.labels[r0 + rr] = args.leaf_class ? __ldg(args.leaf_class + cls) : cls;
+      }
     }
     __syncwarp();
   }

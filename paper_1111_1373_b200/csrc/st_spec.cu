@@ -31,11 +31,11 @@ void launch_spec_steps(const SpecArgs& sa, const Staging& stg, size_t smem, int 
   }
 }
 
-template <int A, bool WS, int STEPS, int SR, bool CW = false>
+template <int A, bool WS, int STEPS, int SR, bool CW = false, int RT = 1>
 void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
                         uint32_t warps, cudaStream_t s) {
-  auto fn = k_spec_ring<A, WS, STEPS, SR, CW>;
-  const uint64_t n_tiles = (ra.s.p.m + 31) / 32;
+  auto fn = k_spec_ring<A, WS, STEPS, SR, CW, RT>;
+  const uint64_t n_tiles = (ra.s.p.m + 32 * RT - 1) / (32 * RT);
   const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles * warps, warps);
   clear_stale_error();
   fn<<<blocks, warps * 32, smem, s>>>(ra, stg.tmap);
@@ -47,6 +47,9 @@ void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg
                          uint32_t warps, cudaStream_t s) {
   // two record streams: shared window table and records inside one 128-byte row
   if constexpr (WS && (A == 8 || A == 16 || A == 32)) {
+    if constexpr (CW) {
+      if (sr >= 2 && ra.tile_mult == 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 2>(ra, stg, smem, dev, warps, s);
+    }
     if (sr >= 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW>(ra, stg, smem, dev, warps, s);
   }
   return launch_spec_ring_k<A, WS, STEPS, 1, CW>(ra, stg, smem, dev, warps, s);
@@ -267,9 +270,23 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     // profiles/r1_sweep_*_spec2d.json, *_spec2e.json)
     uint32_t sr = g.samples_per_thread ? g.samples_per_thread : ((cw || t->info.internal > 511) ? 2u : 1u);
     if (onewin) sr = 0;  // whole tree in one window
-    const size_t lb = 32 + 32 * 128;  // generation padding + ticket + per-warp label rows (<= 32 warps)
+    // 64-record ring slots for the two-stream 8-byte-window loop: the slot's
+    // records are shared by 16 streams, 4 each instead of 2, which evens out
+    // the streams' window counts and halves the per-slot overhead -- taken
+    // when the slot stays at 4 KB (16 attributes: C5 d8 / d12 / d16 / d20
+    // -5 / -10 / -8 / -6 %, C1 even).  Larger slots cost resident warps (C2,
+    // 8 KB: +44 %); 2 KB ones gained nothing (C3 +2 %).  ST_SPEC_TILE=1 / 2
+    // forces 32 / 64 (profiles/r1_spec_tile_ab.txt).
+    uint32_t rt = 1;
+    Staging rstg = stg;
+    const uint32_t want_rt = env_u32("ST_SPEC_TILE", a == 16 ? 2u : 1u);
+    if (cw && sr >= 2 && (a == 8 || a == 16 || a == 32) && want_rt == 2 && m >= 64) {
+      Staging s2 = plan_staging(x, m, a, ld, layout, 2, g.stages, rs.win_bytes, pr);
+      if (s2.loader == kTma && s2.S == 2) rt = 2, rstg = s2;
+    }
+    const size_t lb = 32 + 32 * 128 * rt;  // generation padding + ticket + per-warp label rows (<= 32 warps)
     const size_t budget = pr.smem_optin - 1024 - rs.win_bytes - lb;
-    const size_t max_slots = budget / (stg.stage_bytes + 16u);
+    const size_t max_slots = budget / (rstg.stage_bytes + 16u);
     const uint32_t warps = (uint32_t)std::min<size_t>(32, max_slots > 12 ? max_slots - 12 : 0);
     if (warps >= 4) {
       SpecRingArgs ra{};
@@ -279,16 +296,18 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       if (const uint32_t ns = env_u32("ST_SPEC_RING_SLOTS", 0)) ra.n_slots = std::min<uint32_t>(ra.n_slots, ns);
       ra.unsafe_no_gen = env_u32("ST_SPEC_RING_UNSAFE_NO_GEN", 0);  // measurement of the handshake only
       ra.bulk_win = env_u32("ST_TREE_BULK", 1) ? 1u : 0u;
-      const size_t rsmem = 1024 + rs.win_bytes + (size_t)ra.n_slots * (stg.stage_bytes + 8u) +
-                           (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128;
+      ra.tile_mult = rt;
+      ra.s.stage_bytes = rstg.stage_bytes;
+      const size_t rsmem = 1024 + rs.win_bytes + (size_t)ra.n_slots * (rstg.stage_bytes + 8u) +
+                           (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128 * rt;
       // one window: ballot + leaf path masks unless pointer jumping is asked for
       if (onewin) ra.s.pm_off = env_u32("ST_SPEC_ONEWIN_JUMP", 0) ? 0u : wt->pm_off;
       switch (ct_arity(a) ? a : 0) {
-        case 8: return launch_spec_ring<8>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
-        case 16: return launch_spec_ring<16>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
-        case 32: return launch_spec_ring<32>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
-        case 64: return launch_spec_ring<64>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
-        default: return launch_spec_ring<0>(ws, sr, cw, ra, stg, rsmem, dev, warps, s);
+        case 8: return launch_spec_ring<8>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
+        case 16: return launch_spec_ring<16>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
+        case 32: return launch_spec_ring<32>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
+        case 64: return launch_spec_ring<64>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
+        default: return launch_spec_ring<0>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
       }
     }
   }

@@ -512,3 +512,21 @@ def test_tree_staging_paths(cuda, co, bulk, monkeypatch):
         xd = torch.from_numpy(x).to(cuda)
         for g in geoms:
             assert np.array_equal(_dev_eval(nodes, xd, g, len(x)), want), (depth, a, g, bulk)
+
+
+@pytest.mark.parametrize("tile", ["1", "2"])
+def test_spec_ring_slot_sizes(cuda, co, tile, monkeypatch):
+    """Speculative ring slots of 32 or 64 records (ST_SPEC_TILE) for the
+    two-stream 8-byte-window loop: skewed and complete trees, 8/16/32
+    attributes, ragged record counts (partial last slot, fewer records than
+    one slot), single-leaf tree."""
+    monkeypatch.setenv("ST_SPEC_TILE", tile)
+    cases = ((24, 256, 32, 41), (16, 4096, 16, 42), (12, 2048, 8, 43), (0, 1, 16, 44))
+    for depth, leaves, a, seed in cases:
+        nodes = co.gen_tree(depth, leaves, a, 8, seed)
+        for m in (1, 63, 64, 65, 4097, 100_003):
+            x = co.gen_dataset(m, a, seed + m)
+            want = co.eval_serial(nodes, x)
+            xd = torch.from_numpy(x).to(cuda)
+            for g in (st.GpuGeom(algo="speculative"), st.GpuGeom(algo="speculative", group_lanes=8)):
+                assert np.array_equal(_dev_eval(nodes, xd, g, m), want), (depth, a, m, g, tile)
