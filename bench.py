@@ -1,21 +1,38 @@
 #!/usr/bin/env python
-"""Benchmark: samples classified/sec per B200 (and N x B200, weak scaling).
+"""Benchmark: samples classified/sec per B200 and N x B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload C2] [--algo auto|data|speculative]
+                    [--workload C2|C1|C3|C4|C5|C5d8..C5d20|PAPER]
+                    [--algo auto|data|speculative] [--c5-depth D]
 
 One "step" = one pass of the hot path (tree evaluation) over one batch of
-synthetic records: the BASELINE.json configs[1] workload by default, C2 =
+synthetic records.  Default workload: BASELINE.json configs[1], C2 = the
 unbalanced depth-24 tree (reference generator tree(24,256,32,8,201)) over
-16,000,000 records x 32 float32 attributes (data(16e6,32,202) on rank 0;
-rank r > 0 uses seed 202 + 1000 r), one batch per GPU (weak scaling).
+16,000,000 records x 32 float32 attributes per GPU; rank r's batch is
+data(16e6, 32, 202 + 1000 r) (weak scaling; every rank's labels are checked
+against the reference hashes in tests/golden/shard_hashes.json).
+--workload C5 is BASELINE configs[4]: 64 shards data(15.625e6, 16, 5000 + s)
+= 10^9 records resident in HBM, split over the ranks by the Proc. 3 range
+rule (rank r owns shards [64r/N, 64(r+1)/N): strong scaling), one step = one
+launch per rank over its block with tree(D, min(2^D, 4096), 16, 8, 500 + D);
+every depth 8..20 is timed for both algorithms (spec/data ratio per depth)
+and every shard's labels are checked against the reference hashes.
+
+Multi-GPU: one process per GPU.  Under torchrun (RANK/WORLD_SIZE set) the
+ranks join a process group (NCCL when every rank has its own GPU, gloo when
+ranks share one) used only for the barrier, the max-over-ranks timing and
+the parity gather -- the path itself has no collective (samples are
+independent; the tree is replicated).  Without torchrun, --gpus N > 1
+re-launches this script under torch.distributed.run with N ranks.
 
 value  -- device-timed (CUDA events on the launching stream, barrier + sync on
-          both sides, max over ranks) with the records resident in HBM; the
-          2.05 GB/GPU input exceeds the 126 MB L2, so no flush is needed.
+          both sides, max over ranks) with the records resident in HBM and
+          larger than L2 (no flush needed).
 e2e    -- the same metric through the public host API (st_eval: pinned host
-          records -> H2D -> kernel -> D2H labels), copies inside the timed region;
-          e2e.pageable: the same call from pageable host memory.
+          records -> H2D -> kernel -> D2H labels) on every rank concurrently,
+          copies inside the timed region; e2e.pageable from pageable memory;
+          e2e.sharded: the C++ drop-in's single-process path over every
+          visible GPU (st_eval_sharded, GpuConfig.devices) when there are > 1.
 roofline -- algorithmic bytes (4*A per record) per launch / the
           kernel's average event-timed duration, against MEASURED_PEAKS.json.
 cpu_baseline -- the reference's eval_serial (oracle/_ref, compiled from the
@@ -26,9 +43,12 @@ cpu_baseline -- the reference's eval_serial (oracle/_ref, compiled from the
 from __future__ import annotations
 
 import argparse
+import concurrent.futures as cf
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -41,7 +61,7 @@ sys.path.insert(0, ROOT)
 WORKLOADS = {
     "C2": dict(desc="unbalanced depth-24 tree (skewed splits), 32 float32 attributes, "
                     "16M samples per GPU: divergence stress for data decomposition",
-               tree=(24, 256, 32, 8, 201), m=16_000_000, a=32, seed=202,
+               tree=(24, 256, 32, 8, 201), m=16_000_000, a=32, seed=202, golden="c2",
                labels_fnv=0x9e7e87e9cc15c4e0),
     "C1": dict(desc="complete depth-10 tree, 16 float32 attributes, 1M samples",
                tree=(10, 1024, 16, 8, 101), m=1_000_000, a=16, seed=102,
@@ -49,19 +69,16 @@ WORKLOADS = {
     "C3": dict(desc="per-pixel segmentation: 1920x1080 frame, 8 features/pixel, depth-12 tree",
                tree=(12, 2048, 8, 8, 301), m=2_073_600, a=8, seed=302,
                labels_fnv=0xd57c3eb045278e36),
-    "C5d8": dict(desc="C5 shard: depth-8 tree, 16 attributes, 15.625M samples",
-                 tree=(8, 256, 16, 8, 508), m=15_625_000, a=16, seed=5000,
-                 labels_fnv=0xa41b18f5886a3516),
-    "C5d12": dict(desc="C5 shard: depth-12 tree, 16 attributes, 15.625M samples",
-                  tree=(12, 4096, 16, 8, 512), m=15_625_000, a=16, seed=5000,
-                  labels_fnv=0x8a36c71851f61114),
-    "C5d16": dict(desc="C5 shard: depth-16 tree, 16 attributes, 15.625M samples",
-                  tree=(16, 4096, 16, 8, 516), m=15_625_000, a=16, seed=5000,
-                  labels_fnv=0x4bbe70e47d70a501),
-    "C5d20": dict(desc="C5 shard: depth-20 tree, 16 attributes, 15.625M samples",
-                  tree=(20, 4096, 16, 8, 520), m=15_625_000, a=16, seed=5000,
-                  labels_fnv=0x894ffd1cd01ac0a5),
+    "PAPER": dict(desc="the paper's workload: tree(11,16,19,7,1) (15 internal nodes, one speculative "
+                       "window) over 1024 copies of data(16384,19,2) = 16.8M samples",
+                  tree=(11, 16, 19, 7, 1), m=16384 * 1024, a=19, seed=2, tile=16384,
+                  labels_fnv=0xc90f17638d0c1525),  # hash of the first 4 tiles (Appendix A)
 }
+for _d in (8, 12, 16, 20):
+    WORKLOADS[f"C5d{_d}"] = dict(desc=f"C5 shard: depth-{_d} tree, 16 attributes, 15.625M samples per GPU",
+                                 tree=(_d, min(2 ** _d, 4096), 16, 8, 500 + _d), m=15_625_000, a=16,
+                                 seed=5000, seed_step=1, golden=f"c5:{_d}")
+C5_SHARD, C5_SHARDS, C5_A, C5_DEPTHS = 15_625_000, 64, 16, (8, 10, 12, 14, 16, 18, 20)
 METRIC = "samples classified/sec per B200 and 8xB200 (+% of HBM roofline) vs CPU serial"
 UNIT = "samples/s"
 L2_BYTES = 126 * 2**20
@@ -81,14 +98,43 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-class ClockSampler(threading.Thread):
-    """NVML SM clock + throttle-reason sampler run during the timed region."""
+def golden():
+    """Reference label hashes (tests/golden/make_shard_golden.py, generated
+    from oracle/_ref): per C2 / C4 rank batch and per C5 shard and depth."""
+    try:
+        return json.load(open(os.path.join(ROOT, "tests", "golden", "shard_hashes.json")))
+    except Exception:
+        return {}
 
-    def __init__(self, cuda_index: int, period: float = 0.005):
+
+def golden_labels(W, rank):
+    g = golden()
+    key = W.get("golden")
+    if key == "c2":
+        v = g.get("c2_ranks", {}).get("labels_fnv", [])
+        return int(v[rank], 16) if rank < len(v) else None
+    if key and key.startswith("c5:"):
+        v = g.get("c5", {}).get("depths", {}).get(key[3:], {}).get("labels_fnv", [])
+        return int(v[rank], 16) if rank < len(v) else None
+    # tiled workloads give every rank the same records
+    return W.get("labels_fnv") if rank == 0 or "tile" in W else None
+
+
+class ClockSampler(threading.Thread):
+    """NVML SM clock + throttle-reason sampler.  A background thread samples
+    every `period` s; mark() takes a synchronous sample (called while the
+    timed launches are in flight); summary() waits for one sample after the
+    region so a short region still gets bracketed.  NVML failures are
+    counted and reported, never swallowed silently."""
+
+    def __init__(self, cuda_index: int, period: float = 0.002):
         super().__init__(daemon=True)
         self.period = period
         self.samples = []
+        self.errors = 0
+        self.last_error = None
         self.stop_ev = threading.Event()
+        self.lock = threading.Lock()
         self.ok = False
         try:
             import pynvml
@@ -105,41 +151,62 @@ class ClockSampler(threading.Thread):
             self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.ok = True
-        except Exception as e:  # pragma: no cover - reported in JSON
-            self.err = repr(e)
+        except Exception as e:  # reported in the JSON line
+            self.last_error = repr(e)
 
     def read(self):
         t = time.perf_counter()
-        mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
         try:
-            reasons = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-        except Exception:
-            reasons = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-        self.samples.append((t, mhz, reasons))
+            mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+            try:
+                reasons = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                reasons = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        except Exception as e:
+            with self.lock:
+                self.errors += 1
+                self.last_error = repr(e)
+            return
+        with self.lock:
+            self.samples.append((t, mhz, reasons))
+
+    def mark(self):
+        if self.ok:
+            self.read()
 
     def run(self):
         while self.ok and not self.stop_ev.is_set():
-            try:
-                self.read()
-            except Exception:
-                pass
+            self.read()
             time.sleep(self.period)
 
     def summary(self, t0, t1):
         if not self.ok:
-            return {"error": getattr(self, "err", "nvml unavailable")}
-        win = [s for s in self.samples if t0 <= s[0] <= t1]
-        if not win:  # very short timed region: the nearest sample on each side
-            before = [s for s in self.samples if s[0] < t0][-1:]
-            after = [s for s in self.samples if s[0] > t1][:1]
-            win = before + after
+            return {"sm_mhz": None, "samples": 0, "error": self.last_error or "nvml unavailable"}
+        deadline = time.perf_counter() + 0.5
+        while time.perf_counter() < deadline:
+            with self.lock:
+                if any(s[0] > t1 for s in self.samples):
+                    break
+            time.sleep(self.period)
+        with self.lock:
+            samples = list(self.samples)
+        win = [s for s in samples if t0 <= s[0] <= t1]
+        how = "inside the timed region"
+        if not win:  # very short region: the nearest sample on each side
+            win = [s for s in samples if s[0] < t0][-1:] + [s for s in samples if s[0] > t1][:1]
+            how = "nearest samples around the timed region"
         reasons = set()
         for _, _, r in win:
             for bit, name in NVML_REASONS.items():
                 if r & bit and name != "gpu_idle":
                     reasons.add(name)
-        return {"sm_mhz": statistics.median([s[1] for s in win]) if win else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons), "samples": len(win)}
+        out = {"sm_mhz": statistics.median([s[1] for s in win]) if win else None,
+               "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons), "samples": len(win),
+               "window": how, "period_ms": self.period * 1e3}
+        if self.errors:
+            out["nvml_errors"] = self.errors
+            out["last_error"] = self.last_error
+        return out
 
 
 def dist_env():
@@ -150,8 +217,10 @@ def dist_env():
 
 
 def ncu_traffic(workload, algo):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the newest
-    committed ncu --set full summary (profiles/r<N>_ncu_<workload>_<algo>.json)."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel
+    and workload from the newest committed `ncu --set full` summary
+    (profiles/r<N>_ncu_<workload>_<algo>.json): the capture cannot run inside
+    a timed bench, so the value and its file are reported together."""
     import glob
     import re
 
@@ -159,125 +228,202 @@ def ncu_traffic(workload, algo):
     files.sort(key=lambda f: int(re.search(r"/r(\d+)_ncu_", f).group(1)))
     for p in reversed(files):
         try:
-            return float(json.load(open(p))["dram_bytes_per_launch"])
+            return float(json.load(open(p))["dram_bytes_per_launch"]), os.path.relpath(p, ROOT)
         except Exception:
             continue
-    return None
+    return None, None
+
+
+class Dist:
+    """Process-group plumbing for N > 1 (barrier, max over ranks, gather);
+    every call is a no-op at N = 1."""
+
+    def __init__(self, dev, backend):
+        import torch
+        import torch.distributed as dist
+
+        self.world, self.rank, _ = dist_env()
+        self.dist = dist
+        self.dev = dev
+        if backend == "auto":
+            backend = "nccl" if torch.cuda.device_count() >= self.world else "gloo"
+        self.backend = backend
+        if self.world > 1:
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=dev)
+            else:
+                dist.init_process_group(backend)
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v):
+        if self.world == 1:
+            return v
+        import torch
+
+        t = torch.tensor([v], dtype=torch.float64, device=self.dev if self.backend == "nccl" else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def _setup_device():
+    import torch
+
+    world, rank, local = dist_env()
+    # one process per GPU; ranks beyond the visible GPUs wrap around (a
+    # smaller box validating the multi-rank path; the group then uses gloo)
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    return torch.device("cuda", local), local
+
+
+def _hash_many(arrays, threads=None):
+    """FNV-1a-64 of several host arrays in parallel (the native hash drops the GIL)."""
+    import paper_1111_1373_b200 as st
+
+    with cf.ThreadPoolExecutor(max_workers=threads or min(16, os.cpu_count() or 1)) as pool:
+        return list(pool.map(st.fnv1a64, arrays))
+
+
+def time_launches(launch, steps, warmup, stream, pg, sampler=None):
+    """Device time of `steps` back-to-back launches (CUDA events on the
+    launching stream, barrier + synchronize on both sides), max over ranks.
+    Returns (t_max, t_local, launches, (host t0, t1))."""
+    import torch
+
+    for _ in range(warmup):
+        launch()
+    torch.cuda.synchronize()
+    pg.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    n = 0
+    t0 = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(steps):
+        n += launch()
+    ev1.record(stream)
+    if sampler is not None:
+        sampler.mark()  # launches are in flight: the GPU is under load now
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    pg.barrier()
+    torch.cuda.synchronize()
+    t_local = ev0.elapsed_time(ev1) / 1e3
+    return pg.max(t_local), t_local, n, (t0, t1)
 
 
 # --------------------------------------------------------------- our arm ---
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     import paper_1111_1373_b200 as st
 
-    world, rank, local = dist_env()
-    # one process per GPU; ranks beyond the visible GPUs wrap around (only for
-    # validating the multi-rank path on a smaller box with --backend gloo)
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(args.backend)
+    dev, local = _setup_device()
+    pg = Dist(dev, args.backend)
+    world, rank = pg.world, pg.rank
     W = WORKLOADS[args.workload]
     m, a = W["m"], W["a"]
     tree = st.generate_synthetic_tree(*W["tree"])
-    seed = W["seed"] + 1000 * rank
+    seed = W["seed"] + W.get("seed_step", 1000) * rank
     x_host = torch.empty((m, a), dtype=torch.float32, pin_memory=True)
-    st.generate_synthetic_dataset(m, a, seed, out=x_host.numpy())
+    if "tile" in W:  # the paper's workload: copies of one small dataset
+        base = st.generate_synthetic_dataset(W["tile"], a, W["seed"])
+        x_host.numpy()[:] = np.tile(base, (m // W["tile"], 1))
+    else:
+        st.generate_synthetic_dataset(m, a, seed, out=x_host.numpy())
     x_dev = x_host.to(dev, non_blocking=False)
     labels = torch.empty(m, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    one_window = st.tree_info(tree)["spec_windows"] == 1
+    algos = {"data": st.GpuGeom(algo="data"), "speculative": st.GpuGeom(algo="speculative")}
+    if one_window:  # the default one-window reduction is the ballot; time pointer jumping beside it
+        algos["speculative_pointer_jumping"] = st.GpuGeom(algo="speculative", variant=("spec_jump",))
 
-    def max_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    # correctness of the measured configuration, every rank against the
+    # reference hash of its own batch
+    want = golden_labels(W, rank)
+    ok = {}
+    for name, g in algos.items():
+        st.eval_device(tree, x_dev, labels, g, stream=stream)
+        torch.cuda.synchronize()
+        if "tile" in W:
+            lab = labels.view(-1, W["tile"])
+            periodic = bool((lab == lab[:1]).all().item())
+            ok[name] = periodic and st.fnv1a64(labels[: 4 * W["tile"]].cpu().numpy()) == want
+        else:
+            ok[name] = None if want is None else st.fnv1a64(labels.cpu().numpy()) == want
+    per_rank = pg.gather(ok)
 
-    def timed(algo, steps, warmup, sampler=None):
-        geom = st.GpuGeom(algo=algo)
-        for _ in range(warmup):
-            st.eval_device(tree, x_dev, labels, geom, stream=stream)
-        torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        launches = 0
-        t0 = time.perf_counter()
-        ev0.record(stream)
-        for _ in range(steps):
-            st.eval_device(tree, x_dev, labels, geom, stream=stream)
-            launches += st.last_launch_count()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        barrier()
-        torch.cuda.synchronize()
-        local_s = ev0.elapsed_time(ev1) / 1e3
-        return max_over_ranks(local_s), local_s, launches, (t0, t1)
-
-    # correctness of the measured configuration (rank 0 = canonical records)
-    labels_ok = {}
-    for algo in ("data", "speculative"):
-        st.eval_device(tree, x_dev, labels, st.GpuGeom(algo=algo), stream=stream)
-        torch.cuda.synchronize()
-        if rank == 0:
-            h = st.fnv1a64(labels.cpu().numpy())
-            labels_ok[algo] = h == W["labels_fnv"]
+    def launcher(g):
+        def launch():
+            st.eval_device(tree, x_dev, labels, g, stream=stream)
+            return st.last_launch_count()
+        return launch
 
     sampler = ClockSampler(local)
     sampler.start()
     headline = args.algo if args.algo != "auto" else "data"
-    t_max, t_local, launches, (c0, c1) = timed(args.algo, args.steps, args.warmup)
+    t_max, t_local, launches, (c0, c1) = time_launches(
+        launcher(st.GpuGeom(algo=args.algo)), args.steps, args.warmup, stream, pg, sampler)
     clocks = sampler.summary(c0, c1)
-    by_algo = {}
+    sampler.stop_ev.set()
     peak, peak_src = peaks()
     bytes_per_launch = 4.0 * a * m
-    for algo in ("data", "speculative"):
-        if algo == headline:
+    by_algo = {}
+    for name, g in algos.items():
+        if name == headline:
             tm, tl, k = t_max, t_local, args.steps
         else:
             k = max(3, min(args.steps, args.alt_steps))
-            tm, tl, _, _ = timed(algo, k, max(3, min(args.warmup, 10)))
-        by_algo[algo] = {"value": world * m * k / tm, "ms_per_step": tm / k * 1e3,
+            tm, tl, _, _ = time_launches(launcher(g), k, max(3, min(args.warmup, 10)), stream, pg)
+        by_algo[name] = {"value": world * m * k / tm, "ms_per_step": tm / k * 1e3,
                          "roofline_frac": (bytes_per_launch / (tl / k) / 1e9) / peak}
-    sampler.stop_ev.set()
+    by_algo["speculative"]["reduction"] = (
+        "ballot + leaf path masks over one window (every internal node's predicate in one vote)"
+        if one_window else "warp-shuffle pointer jumping inside G-lane windows")
+    by_algo["speculative_over_data_time"] = by_algo["speculative"]["ms_per_step"] / by_algo["data"]["ms_per_step"]
 
-    # e2e through the public host API: pinned host records -> labels on host
+    # e2e through the public host API on every rank at once: pinned host
+    # records -> labels on host
     e2e_steps = max(1, args.e2e_steps)
     labels_host = torch.empty(m, dtype=torch.int32, pin_memory=True)
     geom = st.GpuGeom(algo=args.algo)
     xnp = x_host.numpy()
-    st.eval_gpu(tree, xnp, geom, out=labels_host.numpy().view(np.uint32))  # warm
-    barrier()
+    lnp = labels_host.numpy().view(np.uint32)
+    st.eval_gpu(tree, xnp, geom, out=lnp)  # warm
+    pg.barrier()
     e0 = time.perf_counter()
     for _ in range(e2e_steps):
-        st.eval_gpu(tree, xnp, geom, out=labels_host.numpy().view(np.uint32))
-    e_local = time.perf_counter() - e0
-    barrier()
-    e_max = max_over_ranks(e_local)
-    # the same call from pageable host memory (what a drop-in caller with a
-    # std::vector / numpy dataset passes): records packed into pinned staging
-    # by the library's host copy threads
+        st.eval_gpu(tree, xnp, geom, out=lnp)
+    e_max = pg.max(time.perf_counter() - e0)
+    e2e_ok = want is None or "tile" in W or st.fnv1a64(lnp) == want
+    # the same call from pageable host memory (a drop-in caller's std::vector
+    # / numpy dataset): records packed into pinned staging by the library's
+    # host copy threads
     x_page = np.array(xnp, copy=True)
     labels_page = np.empty(m, np.uint32)
     st.eval_gpu(tree, x_page, geom, out=labels_page)  # warm
-    barrier()
+    pg.barrier()
     e0 = time.perf_counter()
     for _ in range(e2e_steps):
         st.eval_gpu(tree, x_page, geom, out=labels_page)
-    p_max = max_over_ranks(time.perf_counter() - e0)
+    p_max = pg.max(time.perf_counter() - e0)
     del x_page
 
     # PCIe roofline for e2e: measured pinned H2D copy bandwidth of this GPU
@@ -292,11 +438,39 @@ def run_ours(args):
         torch.cuda.synchronize()
         h2d_peak = max(h2d_peak, probe.numel() * 4 / (p0.elapsed_time(p1) / 1e3) / 1e9)
     del probe_dev
-    e2e_s_per_step = e_max / e2e_steps
-    e2e_h2d_gbs = 4 * a * m / e2e_s_per_step / 1e9
+    e2e_h2d_gbs = 4 * a * m / (e_max / e2e_steps) / 1e9
+
+    # single-process multi-GPU drop-in (st_eval_sharded over every visible
+    # GPU: the C++ eval_data_parallel with GpuConfig.devices), rank 0 while
+    # the other ranks wait
+    sharded = None
+    ndev = torch.cuda.device_count()
+    if ndev > 1 and not args.no_sharded_e2e:
+        pg.barrier()
+        if rank == 0:
+            reps = max(1, min(ndev, 8))
+            xs = torch.empty((m * reps, a), dtype=torch.float32, pin_memory=True)
+            xs.view(reps, m, a)[:] = x_host
+            ls = np.empty(m * reps, np.uint32)
+            devs = list(range(ndev))
+            st.eval_sharded(tree, xs.numpy(), devs, geom)  # warm (replicas, slots)
+            s0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                out = st.eval_sharded(tree, xs.numpy(), devs, geom)
+            s_el = time.perf_counter() - s0
+            sh_ok = want is None or "tile" in W or all(
+                h == want for h in _hash_many([out[i * m:(i + 1) * m] for i in range(reps)]))
+            sharded = {"value": m * reps * e2e_steps / s_el, "unit": UNIT, "devices": ndev,
+                       "records_per_call": m * reps, "labels_ok": bool(sh_ok),
+                       "api": "st_eval_sharded (pinned host records, one process, every GPU)"}
+            del xs
+        pg.barrier()
 
     kernel_s = t_local / args.steps
     achieved = bytes_per_launch / kernel_s / 1e9
+    traffic, traffic_src = ncu_traffic(args.workload, headline)
+    per_rank_ok = {name: [r.get(name) for r in per_rank] for name in algos}
+    e2e_ok_all = pg.gather(bool(e2e_ok))
     line = {
         "metric": METRIC,
         "value": world * m * args.steps / t_max,
@@ -315,29 +489,39 @@ def run_ours(args):
             "tree": "generate_synthetic_tree{} -> {} nodes, depth {}".format(
                 W["tree"], tree.size(), tree.depth()),
             "records_per_gpu": m, "arity": a, "layout": "AoS float32",
+            "rank_seed": f"{W['seed']} + {W.get('seed_step', 1000)} * rank" if "tile" not in W else "tiled",
             "algo": args.algo if args.algo != "auto" else "auto(data)",
-            "parallelism": f"sample-sharded x{world} (weak), tree replicated, no collective",
+            "parallelism": f"sample-sharded x{world} (weak), tree replicated, no collective "
+                           f"(process group: {pg.backend if world > 1 else 'none'}, timing only)",
             "l2": f"inputs {4 * a * m / 1e9:.2f} GB/GPU > L2 126 MB: no flush needed"
                   if 4 * a * m > 2 * L2_BYTES else "inputs L2-resident: results optimistic",
         },
-        "labels_match_reference_hash": labels_ok if rank == 0 else None,
+        "labels_match_reference_hash": {
+            **{name: (all(v is True for v in vals) if all(v is not None for v in vals) else None)
+               for name, vals in per_rank_ok.items()},
+            "per_rank": per_rank_ok, "e2e": all(e2e_ok_all)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "frac_vs_8TBs": achieved / 8000.0,
-                     "traffic": ncu_traffic(args.workload, headline),
+                     "traffic": traffic,
+                     "traffic_source": (f"{traffic_src}: ncu --set full dram__bytes_read.sum + "
+                                        f"dram__bytes_write.sum of the same kernel and workload, per launch "
+                                        f"(a profiled run cannot be the timed one)") if traffic_src else None,
                      "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "kernel_ms": kernel_s * 1e3},
         "by_algorithm": by_algo,
         "e2e": {"value": world * m * e2e_steps / e_max, "unit": UNIT,
-                "h2d_bytes_per_step": 4 * a * m, "d2h_bytes_per_step": 4 * m,
-                "steps": e2e_steps, "api": "st_eval (host pinned buffers, chunked H2D/kernel/D2H)",
+                "h2d_bytes_per_step": 4 * a * m * world, "d2h_bytes_per_step": 4 * m * world,
+                "steps": e2e_steps,
+                "api": "st_eval on every rank (host pinned buffers, chunked H2D/kernel/D2H over 3 streams)",
                 "roofline": {"bound": "pcie_h2d", "achieved": e2e_h2d_gbs, "peak": h2d_peak,
                              "unit": "GB/s", "frac": e2e_h2d_gbs / h2d_peak if h2d_peak else None,
-                             "peak_source": "measured: pinned 1 GiB H2D copy_, best of 4 (CUDA events)"},
+                             "peak_source": "measured: pinned 1 GiB H2D copy_, best of 4 (CUDA events), rank 0"},
                 "pageable": {"value": world * m * e2e_steps / p_max, "unit": UNIT, "steps": e2e_steps,
                              "h2d_GBs": 4 * a * m * e2e_steps / p_max / 1e9,
                              "api": "st_eval (pageable host buffers: host-thread packing into pinned "
-                                    "staging, chunked H2D/kernel/D2H)"}},
+                                    "staging, chunked H2D/kernel/D2H)"},
+                "sharded": sharded},
         "clocks": clocks,
         "gpu_launches": launches,
     }
@@ -345,8 +529,140 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(args, tree.nodes(), xnp)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    pg.close()
+
+
+# ------------------------------------------------------------ C5 (10^9) ---
+def run_c5(args):
+    """BASELINE configs[4]: 10^9 records (64 shards) resident in HBM, split
+    over the ranks by the Proc. 3 range rule (strong scaling); depth sweep
+    8..20, both algorithms, every shard checked against the reference."""
+    import torch
+
+    import paper_1111_1373_b200 as st
+
+    dev, local = _setup_device()
+    pg = Dist(dev, args.backend)
+    world, rank = pg.world, pg.rank
+    S = args.c5_shards
+    lo, hi = (S * rank) // world, (S * (rank + 1)) // world
+    m = (hi - lo) * C5_SHARD
+    x = torch.empty((m, C5_A), dtype=torch.float32, device=dev)
+    labels = torch.empty(m, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    # host generation with the reference generator: one thread per shard into
+    # a ring of pinned staging buffers, copied to this rank's block
+    t_gen = time.perf_counter()
+    ring = [torch.empty((C5_SHARD, C5_A), dtype=torch.float32, pin_memory=True)
+            for _ in range(min(8, max(1, hi - lo)))]
+
+    def gen(s, buf):
+        st.generate_synthetic_dataset(C5_SHARD, C5_A, 5000 + s, out=buf.numpy())
+        return s
+
+    with cf.ThreadPoolExecutor(max_workers=len(ring)) as pool:
+        pending, free, nxt = {}, list(ring), lo
+        while nxt < hi or pending:
+            while nxt < hi and free:
+                buf = free.pop()
+                pending[pool.submit(gen, nxt, buf)] = (nxt, buf)
+                nxt += 1
+            done, _ = cf.wait(list(pending), return_when=cf.FIRST_COMPLETED)
+            for f in done:
+                s, buf = pending.pop(f)
+                f.result()
+                x[(s - lo) * C5_SHARD:(s - lo + 1) * C5_SHARD].copy_(buf)
+                free.append(buf)
+    del ring
+    t_gen = time.perf_counter() - t_gen
+    gold = golden().get("c5", {}).get("depths", {})
+    peak, peak_src = peaks()
+    depths = [args.c5_depth] + [d for d in C5_DEPTHS if d != args.c5_depth]
+    if args.c5_depths:
+        depths = [args.c5_depth] + [int(d) for d in args.c5_depths.split(",") if int(d) != args.c5_depth]
+    by_depth, parity = {}, {}
+    sampler = ClockSampler(local)
+    sampler.start()
+    headline = args.algo if args.algo != "auto" else "data"
+    main = None
+    for D in depths:
+        tree = st.generate_synthetic_tree(D, min(2 ** D, 4096), C5_A, 8, 500 + D)
+        row = {"tree": {"nodes": tree.size(), "depth": tree.depth()}}
+        want = gold.get(str(D), {}).get("labels_fnv", [])
+        want_dsum = gold.get(str(D), {}).get("depth_sum", [])
+        for algo in ("data", "speculative"):
+            g = st.GpuGeom(algo=algo)
+
+            def launch():
+                st.eval_device(tree, x, labels, g, stream=stream)
+                return st.last_launch_count()
+
+            launch()
+            torch.cuda.synchronize()
+            host = labels.cpu().numpy()
+            hashes = _hash_many([host[(s - lo) * C5_SHARD:(s - lo + 1) * C5_SHARD] for s in range(lo, hi)])
+            ok = [None if s >= len(want) else h == int(want[s], 16) for s, h in zip(range(lo, hi), hashes)]
+            parity[f"d{D}_{algo}"] = ok
+            k = args.steps if (D == args.c5_depth and algo == headline) else max(3, min(args.steps, args.alt_steps))
+            tm, tl, n, win = time_launches(launch, k, args.warmup if k == args.steps else 3, stream, pg,
+                                           sampler if (D == args.c5_depth and algo == headline) else None)
+            row[algo] = {"value": S * C5_SHARD * k / tm, "ms_per_step": tm / k * 1e3,
+                         "roofline_frac": (4.0 * C5_A * m / (tl / k) / 1e9) / peak}
+            if D == args.c5_depth and algo == headline:
+                main = (tm, tl, n, k, win, algo, D)
+        # traversal depths on the GPU (row a11) at full size, every shard's
+        # sum and maximum against the reference
+        dep = torch.empty(m, dtype=torch.int32, device=dev)
+        st.eval_depths_device(tree, x, labels, dep, stream=stream)
+        torch.cuda.synchronize()
+        dv = dep.view(hi - lo, C5_SHARD).to(torch.int64)
+        sums, maxs = dv.sum(dim=1).tolist(), dv.max(dim=1).values.tolist()
+        parity[f"d{D}_depths"] = [None if s >= len(want_dsum) else
+                                  (sums[s - lo] == want_dsum[s] and maxs[s - lo] == gold[str(D)]["depth_max"][s])
+                                  for s in range(lo, hi)]
+        row["d_mu"] = float(sum(sums)) / m
+        del dep, dv
+        row["speculative_over_data_time"] = row["speculative"]["ms_per_step"] / row["data"]["ms_per_step"]
+        by_depth[f"d{D}"] = row
+    tm, tl, launches, steps, (c0, c1), algo, D = main
+    clocks = sampler.summary(c0, c1)
+    sampler.stop_ev.set()
+    all_parity = pg.gather(parity)
+    merged = {key: sum((p[key] for p in all_parity), []) for key in parity}
+    kernel_s = tl / steps
+    achieved = 4.0 * C5_A * m / kernel_s / 1e9
+    ratios = {d: r["speculative_over_data_time"] for d, r in by_depth.items()}
+    line = {
+        "metric": METRIC, "value": S * C5_SHARD * steps / tm, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": tm / steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: reference generators, 64 shards data(15.625e6, 16, 5000 + s)",
+        "config": {"workload": f"C5: {S} shards x {C5_SHARD} = {S * C5_SHARD} records resident in HBM, "
+                               f"depth sweep {min(C5_DEPTHS)}-{max(C5_DEPTHS)}; headline depth {D} ({algo})",
+                   "tree": f"generate_synthetic_tree({D}, {min(2 ** D, 4096)}, 16, 8, {500 + D})",
+                   "records_per_gpu": m, "arity": C5_A, "layout": "AoS float32",
+                   "parallelism": f"Proc. 3 shard ranges x{world} (strong), tree replicated, no collective",
+                   "l2": f"inputs {4 * C5_A * m / 1e9:.1f} GB/GPU > L2 126 MB: no flush needed",
+                   "generation_s": t_gen},
+        "labels_match_reference_hash": {
+            "all_shards_all_depths": all(v is True for vals in merged.values() for v in vals),
+            "checked": {k: f"{sum(v is True for v in vals)}/{len(vals)}" for k, vals in merged.items()}},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "frac_vs_8TBs": achieved / 8000.0, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": 4.0 * C5_A * m, "kernel_ms": kernel_s * 1e3},
+        "by_depth": by_depth,
+        "speculative_over_data_time_by_depth": ratios,
+        "crossover": ("none: speculative is slower at every depth" if all(r > 1 for r in ratios.values())
+                      else [d for d, r in ratios.items() if r <= 1]),
+        "clocks": clocks, "gpu_launches": launches,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = st.generate_synthetic_dataset(min(args.cpu_sample, C5_SHARD), C5_A, 5000)
+        line["cpu_baseline"] = cpu_baseline(args, st.generate_synthetic_tree(D, min(2 ** D, 4096), C5_A, 8,
+                                                                             500 + D).nodes(), sample)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    pg.close()
 
 
 def _ref_or_port():
@@ -359,8 +675,6 @@ def _ref_or_port():
 
 def cpu_baseline(args, nodes, x):
     """oracle/_ref eval_serial on ONE host core over a bounded sample."""
-    import oracle
-
     impl, kind = _ref_or_port()
     sample = min(len(x), args.cpu_sample)
     xs = np.ascontiguousarray(x[:sample])
@@ -413,13 +727,22 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return  # rank 0 alone runs the CPU reference
-    W = WORKLOADS[args.workload]
+    if args.workload == "C5":
+        D = args.c5_depth
+        W = dict(desc=f"C5 (10^9 records, depth {D}; the reference times a sample of shard 0)",
+                 tree=(D, min(2 ** D, 4096), 16, 8, 500 + D), m=C5_SHARD, a=C5_A, seed=5000)
+    else:
+        W = WORKLOADS[args.workload]
     impl, kind = _ref_or_port()
     a = W["a"]
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     sample = min(W["m"], args.ref_sample)
     nodes = impl.gen_tree(*W["tree"])
-    x = impl.gen_dataset(sample, a, W["seed"])  # = the first `sample` canonical records
+    if "tile" in W:
+        base = impl.gen_dataset(W["tile"], a, W["seed"])
+        x = np.ascontiguousarray(np.tile(base, (-(-sample // W["tile"]), 1))[:sample])
+    else:
+        x = impl.gen_dataset(sample, a, W["seed"])  # = the first `sample` canonical records
     chunk = -(-sample // cores)
     if kind == "reference":
         with impl.tree(nodes) as t, impl.data(x) as d:
@@ -441,7 +764,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if args.workload == "C5" else "weak",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: reference generators, canonical seeds",
         "config": {"workload": f"{args.workload}: {W['desc']}", "records_per_step": sample,
                    "arity": a, "algo": "spectree::eval_data_parallel (CPU threads)"},
@@ -461,23 +785,18 @@ FOREST = dict(desc="random forest of 128 depth-12 trees, 64 float32 attributes, 
 
 def run_forest(args):
     """--workload C4 (BASELINE configs[3]): one step = the 128-tree forest vote
-    over the rank's 8M records; same timing rules as run_ours.  The forest is
-    shared-memory bound, so `roofline` reports the HBM fraction for the record
-    bytes (4*A per sample) beside node visits/s."""
+    over the rank's 8M records (seed 499 + 1000 r); same timing rules as
+    run_ours.  The forest is bound by shared-memory wavefronts of the node
+    loads, so `roofline` carries that bound (ncu-measured wavefronts per
+    cycle per SM, from the committed profile) beside the HBM fraction of the
+    record bytes (4*A per sample) and node visits/s."""
     import torch
-    import torch.distributed as dist
 
     import paper_1111_1373_b200 as st
 
-    world, rank, local = dist_env()
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(args.backend)
+    dev, local = _setup_device()
+    pg = Dist(dev, args.backend)
+    world, rank = pg.world, pg.rank
     F = FOREST
     m, a = F["m"], F["a"]
     forest = st.Forest([st.generate_synthetic_tree(*t) for t in F["trees"]], F["classes"])
@@ -486,59 +805,42 @@ def run_forest(args):
     x_dev = x_host.to(dev)
     labels = torch.empty(m, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
     st.eval_forest_device(forest, x_dev, labels, stream=stream)
     torch.cuda.synchronize()
-    labels_ok = (st.fnv1a64(labels.cpu().numpy()) == F["labels_fnv"]) if rank == 0 else None
+    gv = golden().get("c4_ranks", {}).get("vote_fnv", [])
+    want = int(gv[rank], 16) if rank < len(gv) else (F["labels_fnv"] if rank == 0 else None)
+    ok = None if want is None else st.fnv1a64(labels.cpu().numpy()) == want
+    per_rank = pg.gather(ok)
     steps = max(1, min(args.steps, 50))
-    for _ in range(args.warmup):
+
+    def launch():
         st.eval_forest_device(forest, x_dev, labels, stream=stream)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
+        return st.last_launch_count()
+
     sampler = ClockSampler(local)
     sampler.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches = 0
-    c0 = time.perf_counter()
-    ev0.record(stream)
-    for _ in range(steps):
-        st.eval_forest_device(forest, x_dev, labels, stream=stream)
-        launches += st.last_launch_count()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    c1 = time.perf_counter()
-    barrier()
-    torch.cuda.synchronize()
-    t_local = ev0.elapsed_time(ev1) / 1e3
-    t_max = t_local
-    if world > 1:
-        t = torch.tensor([t_local], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
-    sampler.stop_ev.set()
+    t_max, t_local, launches, (c0, c1) = time_launches(launch, steps, args.warmup, stream, pg, sampler)
     clocks = sampler.summary(c0, c1)
+    sampler.stop_ev.set()
     # end to end: pinned host records -> H2D -> forest -> D2H votes (st_forest_eval)
     e_steps = max(1, args.e2e_steps)
     xnp = x_host.numpy()
     st.eval_forest(forest, xnp)
-    barrier()
+    pg.barrier()
     e0 = time.perf_counter()
     for _ in range(e_steps):
         st.eval_forest(forest, xnp)
-    e_local = time.perf_counter() - e0
-    e_max = e_local
-    if world > 1:
-        t = torch.tensor([e_local], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_max = float(t.item())
+    e_max = pg.max(time.perf_counter() - e0)
     peak, peak_src = peaks()
     kernel_s = t_local / steps
     achieved = 4.0 * a * m / kernel_s / 1e9
+    smem = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "r2_ncu_C4_forest.json")))
+        smem = {k: prof.get(k) for k in ("shared_wavefronts_per_clk_per_sm", "shared_conflict_fraction",
+                                         "shared_wavefronts", "source")}
+    except Exception:
+        pass
     line = {
         "metric": METRIC, "value": world * m * steps / t_max, "unit": UNIT, "n_gpus": world,
         "steps": steps, "warmup": args.warmup, "ms_per_step": t_max / steps * 1e3,
@@ -548,18 +850,20 @@ def run_forest(args):
                    "records_per_gpu": m, "arity": a, "layout": "AoS float32", "algo": "forest vote (k_forest_smem)",
                    "parallelism": f"sample-sharded x{world} (weak), forest replicated, no collective",
                    "l2": f"inputs {4 * a * m / 1e9:.2f} GB/GPU > L2 126 MB: no flush needed"},
-        "labels_match_reference_hash": {"forest_vote": labels_ok} if rank == 0 else None,
-        "roofline": {"bound": "smem (node loads); hbm fraction reported", "achieved": achieved, "peak": peak,
+        "labels_match_reference_hash": {"forest_vote": all(v is True for v in per_rank), "per_rank": per_rank},
+        "roofline": {"bound": "smem (node-load wavefronts); hbm fraction of the record bytes reported",
+                     "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "smem": smem,
+                     "node_visits_per_s": None,
                      "algorithmic_bytes_per_launch": 4.0 * a * m, "kernel_ms": kernel_s * 1e3},
-        "e2e": {"value": world * m * e_steps / e_max, "unit": UNIT, "h2d_bytes_per_step": 4 * a * m,
-                "d2h_bytes_per_step": 4 * m, "steps": e_steps, "api": "st_forest_eval (host pinned buffers)"},
+        "e2e": {"value": world * m * e_steps / e_max, "unit": UNIT, "h2d_bytes_per_step": 4 * a * m * world,
+                "d2h_bytes_per_step": 4 * m * world, "steps": e_steps, "api": "st_forest_eval (host pinned buffers)"},
         "clocks": clocks, "gpu_launches": launches,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    pg.close()
 
 
 def run_reference_forest(args):
@@ -608,25 +912,59 @@ def run_reference_forest(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}), flush=True)
 
 
-def main():
+# ------------------------------------------------------------ launching ---
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(n, argv, env=None):
+    """Re-launch this script as n ranks under torch.distributed.run (one
+    process per GPU, rendezvous on 127.0.0.1).  NCCL's communicator-init
+    lines go to stderr so the rank count is visible without touching the
+    JSON line on stdout.  Returns the launcher's exit status."""
+    env = dict(os.environ if env is None else env)
+    if "NCCL_DEBUG" not in env:
+        env.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT", NCCL_DEBUG_FILE="/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["C4"], default="C2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS) + ["C4", "C5"], default="C2")
     ap.add_argument("--algo", choices=["auto", "data", "speculative"], default="auto")
     ap.add_argument("--alt-steps", type=int, default=200,
-                    help="timed steps for the non-headline algorithm in by_algorithm")
+                    help="timed steps for the non-headline algorithms / depths")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     ap.add_argument("--ref-sample", type=int, default=2_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
-                    help="process-group backend for barrier / max-over-ranks (timing only)")
-    args = ap.parse_args()
+    ap.add_argument("--no-sharded-e2e", action="store_true")
+    ap.add_argument("--c5-depth", type=int, default=16, help="C5: headline tree depth")
+    ap.add_argument("--c5-depths", default="", help="C5: comma list of depths to sweep (default 8..20)")
+    ap.add_argument("--c5-shards", type=int, default=C5_SHARDS, help="C5: shards (64 = 10^9 records)")
+    ap.add_argument("--backend", default="auto", choices=["auto", "nccl", "gloo"],
+                    help="process group for barrier / max-over-ranks / parity gather (not the data path); "
+                         "auto = nccl when every rank has its own GPU")
+    args = ap.parse_args(argv)
     args.warmup = max(3, args.warmup)  # timing rule: >= 3 untimed warm-up steps
+    return args
+
+
+def main():
+    args = parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:]))
     if args.impl == "reference":
         if args.workload == "C4":
             run_reference_forest(args)
@@ -634,6 +972,8 @@ def main():
         run_reference(args)
     elif args.workload == "C4":
         run_forest(args)
+    elif args.workload == "C5":
+        run_c5(args)
     else:
         run_ours(args)
 

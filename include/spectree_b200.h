@@ -89,8 +89,28 @@ typedef struct st_geom {
                                   1 = walk from registers (tile released right after loading),
                                   2 = walk from the shared tile,
                                   3 = transpose each tile in place to attribute-major, then walk it */
-  uint32_t reserved[1];
+  uint32_t variant;            /* ST_VAR_* bit flags: A/B variants of the tuned defaults (0 = defaults) */
+  uint32_t ring_slots;         /* speculative ring: cap on the tile-slot count (0 = auto; stress tests) */
+  uint32_t slot_records;       /* speculative ring: records per slot / 32, 1 or 2 (0 = auto) */
+  uint32_t fold_min;           /* data kernel: fold trees of at least this many nodes (0 = auto: 2047) */
+  uint32_t pdl;                /* data kernel: programmatic dependent launch, 0 = auto,
+                                  1 = trigger dependents early, 2 = at exit, 3 = off */
+  uint32_t forest_chains;      /* forest: trees walked per lane at once, 1-4 (0 = auto) */
+  uint32_t forest_slots;       /* forest: shared-memory tree ring slots (0 = auto) */
+  uint32_t reserved[6];
 } st_geom;
+
+/* st_geom.variant flags.  Every combination gives identical labels; they
+ * select the implementation variants the tuned defaults were measured
+ * against, so tests and A/B tools reach them per call. */
+enum st_variant {
+  ST_VAR_NO_FOLD = 1u,      /* data / forest: never fold leaf pairs into terminal nodes */
+  ST_VAR_TREE_LOOP = 2u,    /* stage trees / window tables with per-thread loads, not one bulk copy */
+  ST_VAR_SPEC_GENERAL = 4u, /* speculative, one-window trees: the general window loop */
+  ST_VAR_SPEC_JUMP = 8u,    /* speculative, one-window trees: shfl pointer jumping instead of
+                               the ballot + leaf path-mask reduction */
+  ST_VAR_SPEC_WIDE = 16u    /* speculative: 16-byte window entries instead of 8-byte ones */
+};
 
 /* Optional per-record speculative counters (SpeculativeStats,
  * eval_speculative.hpp:73-77).  Arrays of m uint32, in the same memory space
@@ -133,7 +153,8 @@ void st_forest_destroy(st_forest* forest);
 
 /* Host-buffer evaluation ("outer" window of bench.cpp:267-296): copies the
  * records in, runs the kernel on the current CUDA device, copies labels out;
- * chunked and double-buffered over two streams.  x is m records of arity a
+ * chunked and pipelined over three streams (H2D of chunk c+1 beside the
+ * kernel and D2H of chunk c).  x is m records of arity a
  * (AoS: ld >= a floats between records; SoA: ld >= m floats between
  * attributes; ld = 0 means packed).  labels: m uint32.  Throws the
  * reference's ArgumentError (code 2) before any work when
@@ -157,10 +178,28 @@ int st_eval_sharded(const st_tree* tree, const float* x, uint64_t m, uint32_t a,
                     int layout, const st_geom* geom, const int* devices, int ndev,
                     uint32_t* labels);
 
+/* Forest evaluation: host buffers (st_forest_eval, same pipeline as st_eval)
+ * or device pointers on `stream`.  geom (nullable) carries warps_per_cta,
+ * forest_chains, forest_slots and ST_VAR_NO_FOLD; other fields are ignored. */
 int st_forest_eval(const st_forest* forest, const float* x, uint64_t m, uint32_t a,
-                   uint64_t ld, int layout, uint32_t* labels);
+                   uint64_t ld, int layout, const st_geom* geom, uint32_t* labels);
 int st_forest_eval_device(const st_forest* forest, const float* x, uint64_t m, uint32_t a,
-                          uint64_t ld, int layout, uint32_t* labels, void* stream);
+                          uint64_t ld, int layout, const st_geom* geom, uint32_t* labels,
+                          void* stream);
+
+/* Traversal depths (reference traversal_depths, eval_serial.cpp:77-105): per
+ * record, the number of edges from the root to the leaf it reaches, written
+ * by the data-decomposition kernel beside the labels (one pass over the
+ * records).  st_eval_depths takes host buffers (same pipeline as st_eval);
+ * st_eval_depths_device device pointers on `stream`.  labels and depths: m
+ * uint32 each.  The reference's mean_traversal_depth (:99-110) is the mean of
+ * `depths` (the C++ / Python mirrors throw ArgumentError on an empty
+ * dataset, as the reference does).  geom->algo is ignored (always data). */
+int st_eval_depths(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                   int layout, const st_geom* geom, uint32_t* labels, uint32_t* depths);
+int st_eval_depths_device(const st_tree* tree, const float* x, uint64_t m, uint32_t a,
+                          uint64_t ld, int layout, const st_geom* geom, uint32_t* labels,
+                          uint32_t* depths, void* stream);
 
 /* One unpipelined host round trip with per-phase timing: the GPU edition of
  * the reference bench windows (bench.hpp:50-56, bench.cpp:228-262) and of the

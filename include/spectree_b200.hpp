@@ -152,9 +152,36 @@ inline spectree::ClassAssignment eval_speculative_basic(const spectree::EncodedT
   return detail::speculative(tree, data, config, stats, true, gpu);
 }
 
+/// traversal_depths (eval_serial.hpp:23-25, eval_serial.cpp:77-97): root-to-leaf
+/// edge count per record, computed on the GPU by the data kernel
+/// (st_eval_depths).  Attribute range checked first, as the reference does.
+inline std::vector<std::uint32_t> traversal_depths(const spectree::EncodedTree& tree,
+                                                   const spectree::Dataset& data,
+                                                   const GpuConfig& gpu = {}) {
+  spectree::check_attribute_range(tree, data);
+  std::vector<std::uint32_t> depths(data.count()), labels(data.count());
+  if (data.count() == 0) return depths;
+  detail::TreeHandle h = detail::make_handle(tree);
+  detail::check(st_eval_depths(h.get(), data.values().data(), data.count(), data.arity(), 0,
+                               ST_LAYOUT_AOS, &gpu.geom, labels.data(), depths.data()));
+  return depths;
+}
+
+/// mean_traversal_depth (eval_serial.hpp:27-29, eval_serial.cpp:99-110): the
+/// d_mu of the cost model; an empty dataset throws ArgumentError.
+inline double mean_traversal_depth(const spectree::EncodedTree& tree, const spectree::Dataset& data,
+                                   const GpuConfig& gpu = {}) {
+  if (data.count() == 0) throw spectree::ArgumentError("mean traversal depth of an empty dataset");
+  const auto depths = traversal_depths(tree, data, gpu);
+  std::uint64_t total = 0;
+  for (const std::uint32_t d : depths) total += d;
+  return static_cast<double>(total) / static_cast<double>(depths.size());
+}
+
 /// Random forest with a per-record majority vote (smallest class id on ties).
 inline spectree::ClassAssignment eval_forest(const std::vector<spectree::EncodedTree>& trees,
-                                             const spectree::Dataset& data, uint32_t n_classes) {
+                                             const spectree::Dataset& data, uint32_t n_classes,
+                                             const GpuConfig& gpu = {}) {
   std::vector<const st_node*> ptrs;
   std::vector<uint32_t> sizes;
   for (const auto& t : trees) {
@@ -168,7 +195,7 @@ inline spectree::ClassAssignment eval_forest(const std::vector<spectree::Encoded
   spectree::ClassAssignment out(data.count());
   if (data.count())
     detail::check(st_forest_eval(f, data.values().data(), data.count(), data.arity(), 0,
-                                 ST_LAYOUT_AOS, out.data()));
+                                 ST_LAYOUT_AOS, &gpu.geom, out.data()));
   return out;
 }
 

@@ -12,6 +12,10 @@
 //     GPU speculative kernel vs the law ceil(log2 depth) (and the paired
 //     k = 2 law), on the reference's own workload (39 internal nodes: the
 //     CTA-scope exact kernel) and 40 trees that fit one warp group (shfl);
+//   traversal depths: spectree_b200::traversal_depths (the data kernel's
+//     depth output) vs the reference traversal_depths on the same corpus;
+//   sharded: eval_data_parallel through GpuConfig.devices (every GPU of the
+//     box, or device 0 twice on a one-GPU box) vs the oracle;
 //   error behaviour: ArgumentError before any work, with the reference text.
 //
 // Built by oracle/Makefile into oracle/_ref/gpu_acceptance (needs the GPU
@@ -63,6 +67,16 @@ std::string check_all(const EncodedTree& tree, const LinkedNode& root, const Dat
   dp.workers = 3 + salt % 5;
   dp.chunk = std::max(1u, div_ceil(static_cast<std::uint32_t>(data.count()), dp.workers));
   if (spectree_b200::eval_data_parallel(tree, data, dp) != expected) return "gpu data-parallel";
+  if (spectree_b200::traversal_depths(tree, data) != traversal_depths(tree, data))
+    return "gpu traversal depths";
+  {
+    spectree_b200::GpuConfig sharded;
+    int n = 1;
+    st_device_count(&n);
+    for (int d = 0; d < std::max(2, n); ++d) sharded.devices.push_back(d % n);
+    if (spectree_b200::eval_data_parallel(tree, data, dp, sharded) != expected)
+      return "gpu data-parallel sharded over " + std::to_string(sharded.devices.size()) + " devices";
+  }
   SpeculativeConfig basic;
   basic.group_lanes = tree.size();
   basic.records_per_group = 1 + salt % 4;
@@ -194,6 +208,19 @@ void errors() {
   DataParallelConfig one;
   report(spectree_b200::eval_data_parallel(tree, empty, one).empty(), "empty",
          "empty dataset -> empty assignment");
+  std::string ref_d, gpu_d;
+  try {
+    mean_traversal_depth(tree, empty);
+  } catch (const ArgumentError& e) {
+    ref_d = e.what();
+  }
+  try {
+    spectree_b200::mean_traversal_depth(tree, empty);
+  } catch (const ArgumentError& e) {
+    gpu_d = e.what();
+  }
+  report(!ref_d.empty() && ref_d == gpu_d, "empty-depth",
+         "mean traversal depth of an empty dataset -> ArgumentError \"" + gpu_d + "\"");
 }
 
 }  // namespace

@@ -10,12 +10,13 @@ of that boundary; the C++ mirror is include/spectree_b200.hpp.
 from .dataset import ClassAssignment, Dataset, tile_dataset
 from .errors import (ArgumentError, CudaError, Error, IoError, NoDeviceError, ParseError,
                      SchemaError, StructureError)
-from .evaluate import (DataParallelConfig, Forest, GpuGeom, ReductionMode, SpeculativeConfig,
-                       SpeculativeStats, check_attribute_range, default_data_parallel,
-                       default_speculative, eval_data_parallel, eval_device, eval_forest,
-                       eval_forest_device, eval_gpu, eval_sharded, eval_speculative,
-                       eval_speculative_basic, last_launch_count, tree_info,
-                       validate_data_parallel, validate_speculative)
+from .evaluate import (VARIANTS, DataParallelConfig, Forest, GpuGeom, ReductionMode,
+                       SpeculativeConfig, SpeculativeStats, check_attribute_range,
+                       default_data_parallel, default_speculative, eval_data_parallel,
+                       eval_depths_device, eval_device, eval_forest, eval_forest_device, eval_gpu,
+                       eval_sharded, eval_speculative, eval_speculative_basic, last_launch_count,
+                       mean_traversal_depth, traversal_depths, tree_info, validate_data_parallel,
+                       validate_speculative)
 from .files import (dataset_info, eval_file, load_dataset_bin, load_labels_bin,
                     save_dataset_bin, save_labels_bin)
 from .synthetic import (dataset_checksum, fnv1a64, generate_synthetic_dataset,

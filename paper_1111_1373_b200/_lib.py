@@ -43,8 +43,23 @@ class st_geom(C.Structure):
         ("warps_per_cta", C.c_uint32),
         ("pipeline", C.c_uint32),
         ("record_regs", C.c_uint32),
-        ("reserved", C.c_uint32 * 1),
+        ("variant", C.c_uint32),
+        ("ring_slots", C.c_uint32),
+        ("slot_records", C.c_uint32),
+        ("fold_min", C.c_uint32),
+        ("pdl", C.c_uint32),
+        ("forest_chains", C.c_uint32),
+        ("forest_slots", C.c_uint32),
+        ("reserved", C.c_uint32 * 6),
     ]
+
+
+# st_variant flags (st_geom.variant)
+ST_VAR_NO_FOLD = 1
+ST_VAR_TREE_LOOP = 2
+ST_VAR_SPEC_GENERAL = 4
+ST_VAR_SPEC_JUMP = 8
+ST_VAR_SPEC_WIDE = 16
 
 
 class st_stats(C.Structure):
@@ -85,6 +100,7 @@ EXPORTS = (
     "st_synthetic_tree", "st_synthetic_dataset", "st_dataset_checksum", "st_fnv1a64",
     "st_eval_timed", "st_dataset_save", "st_dataset_info_read", "st_dataset_load",
     "st_labels_save", "st_labels_load", "st_eval_file",
+    "st_eval_depths", "st_eval_depths_device",
 )
 
 _lib = None
@@ -124,9 +140,13 @@ def load() -> C.CDLL:
     L.st_eval_sharded.argtypes = [vp, vp, u64, u32, u64, i32, C.POINTER(st_geom),
                                   C.POINTER(i32), i32, vp]
     L.st_forest_eval.restype = i32
-    L.st_forest_eval.argtypes = [vp, vp, u64, u32, u64, i32, vp]
+    L.st_forest_eval.argtypes = [vp, vp, u64, u32, u64, i32, C.POINTER(st_geom), vp]
     L.st_forest_eval_device.restype = i32
-    L.st_forest_eval_device.argtypes = [vp, vp, u64, u32, u64, i32, vp, vp]
+    L.st_forest_eval_device.argtypes = [vp, vp, u64, u32, u64, i32, C.POINTER(st_geom), vp, vp]
+    L.st_eval_depths.restype = i32
+    L.st_eval_depths.argtypes = [vp, vp, u64, u32, u64, i32, C.POINTER(st_geom), vp, vp]
+    L.st_eval_depths_device.restype = i32
+    L.st_eval_depths_device.argtypes = [vp, vp, u64, u32, u64, i32, C.POINTER(st_geom), vp, vp, vp]
     L.st_last_launch_count.restype = u32
     L.st_synthetic_tree.restype = i32
     L.st_synthetic_tree.argtypes = [u32, u32, u32, u32, u64, vp, u32, C.POINTER(u32)]

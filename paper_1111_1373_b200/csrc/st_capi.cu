@@ -8,7 +8,7 @@
 //     GPU);
 //   * dispatch to the sm_100a kernels in st_kernels.cuh with an
 //     occupancy-derived persistent grid;
-//   * the host-buffer path (chunked H2D / kernel / D2H over two streams) and
+//   * the host-buffer path (chunked H2D / kernel / D2H over three streams) and
 //     the sample-sharded multi-GPU driver.
 #include <pthread.h>
 
@@ -32,20 +32,23 @@ uint32_t resolve_algo(const st_tree* t, const st_geom& g, bool want_stats) {
   return want_stats ? ST_ALGO_SPECULATIVE : ST_ALGO_DATA;
 }
 
+// depths != null: the data kernel also writes traversal depths (the algorithm
+// field is then ignored).
 void eval_device_impl(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
-                      const st_geom* geom, uint32_t* labels, st_stats* stats, cudaStream_t s) {
+                      const st_geom* geom, uint32_t* labels, st_stats* stats, cudaStream_t s,
+                      uint32_t* depths = nullptr) {
   if (!t) fail(ST_ERR_ARGUMENT, "null tree");
   check_common(m, a, ld, layout, t->info.max_attribute);
   st_geom g{};
   if (geom) g = *geom;
-  const uint32_t algo = resolve_algo(t, g, stats != nullptr);
+  const uint32_t algo = depths ? (uint32_t)ST_ALGO_DATA : resolve_algo(t, g, stats != nullptr);
   if (stats && algo != ST_ALGO_SPECULATIVE)
     fail(ST_ERR_ARGUMENT, "per-record stats are produced by the speculative kernel only");
   if (m == 0) return;  // empty dataset: empty output, no launch
   if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
   const int dev = current_device();
   if (algo == ST_ALGO_DATA)
-    eval_data_device(t, x, m, a, ld, layout, g, labels, s, dev);
+    eval_data_device(t, x, m, a, ld, layout, g, labels, depths, s, dev);
   else
     eval_spec_device(t, x, m, a, ld, layout, g, labels, stats, s, dev);
 }
@@ -131,7 +134,10 @@ class HostCopyPool {
   }
   HostCopyPool() {
     const uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
-    workers_ = env_u32("ST_HOST_COPY_THREADS", std::min(16u, hw)) - 1u;
+    // read once, when the pool is first used (process-wide width of the
+    // host packing threads; never consulted on the launch path)
+    const char* env = std::getenv("ST_HOST_COPY_THREADS");
+    workers_ = (env && *env ? (uint32_t)std::strtoul(env, nullptr, 10) : std::min(16u, hw)) - 1u;
     if (workers_ > 63) workers_ = 0;  // ST_HOST_COPY_THREADS=0 -> single-threaded
     for (uint32_t i = 0; i < workers_; ++i)
       std::thread([this] {
@@ -444,35 +450,39 @@ int st_forest_create(const st_node* const* trees, const uint32_t* sizes, uint32_
     for (uint32_t k = 0; k < t; ++k) maxn = std::max(maxn, sizes[k]);
     if (!compact_fits(maxn, maxattr, &f->abits) || total >= (1ull << 32))
       fail(ST_ERR_ARGUMENT, "forest too large for the compact device format");
-    // Trees are folded (leaf pairs inside terminal nodes, fold_tree) when the
-    // encoding allows: ~40 % fewer tree bytes to stream through the ring and
-    // one node load fewer per walk that ends in a pair (C4).
-    const bool fold = 4ull * maxattr < 1024 && !env_u32("ST_FOREST_NO_FOLD", 0);
-    f->compact.reserve(total + t);
-    std::vector<CNode> ft;
-    for (uint32_t k = 0; k < t; ++k) {
-      if (f->compact.size() & 1u) f->compact.push_back(CNode{0.0f, kLeafBit});  // 16-byte align
-      f->offsets.push_back((uint32_t)f->compact.size());
-      if (fold && sizes[k] > 1 && fold_tree(trees[k], sizes[k], f->abits, ft)) {
-        f->compact.insert(f->compact.end(), ft.begin(), ft.end());
-      } else {
-        ft.clear();
-        for (uint32_t i = 0; i < sizes[k]; ++i) {
-          const st_node& nd = trees[k][i];
-          if (nd.class_id != ST_NO_CLASS)
-            ft.push_back(CNode{nd.threshold, kLeafBit | nd.class_id});
-          else
-            ft.push_back(CNode{nd.threshold, ((8u * nd.child) << f->abits) | (4u * nd.attribute)});
+    // Layout 0 folds trees (leaf pairs inside terminal nodes, fold_tree) when
+    // the encoding allows: ~40 % fewer tree bytes to stream through the ring
+    // and one node load fewer per walk that ends in a pair (C4).  Layout 1
+    // keeps every tree plain (ST_VAR_NO_FOLD).
+    for (int l = 0; l < 2; ++l) {
+      st_forest::Layout& L = f->lay[l];
+      const bool fold = l == 0 && 4ull * maxattr < 1024;
+      L.compact.reserve(total + t);
+      std::vector<CNode> ft;
+      for (uint32_t k = 0; k < t; ++k) {
+        if (L.compact.size() & 1u) L.compact.push_back(CNode{0.0f, kLeafBit});  // 16-byte align
+        L.offsets.push_back((uint32_t)L.compact.size());
+        if (fold && sizes[k] > 1 && fold_tree(trees[k], sizes[k], f->abits, ft)) {
+          L.compact.insert(L.compact.end(), ft.begin(), ft.end());
+        } else {
+          ft.clear();
+          for (uint32_t i = 0; i < sizes[k]; ++i) {
+            const st_node& nd = trees[k][i];
+            if (nd.class_id != ST_NO_CLASS)
+              ft.push_back(CNode{nd.threshold, kLeafBit | nd.class_id});
+            else
+              ft.push_back(CNode{nd.threshold, ((8u * nd.child) << f->abits) | (4u * nd.attribute)});
+          }
+          L.compact.insert(L.compact.end(), ft.begin(), ft.end());
         }
-        f->compact.insert(f->compact.end(), ft.begin(), ft.end());
+        const uint32_t tb = (uint32_t)((ft.size() * sizeof(CNode) + 15) & ~size_t(15));
+        L.tree_bytes.push_back(tb);
+        L.max_tree_bytes = std::max(L.max_tree_bytes, tb);
       }
-      const uint32_t tb = (uint32_t)((ft.size() * sizeof(CNode) + 15) & ~size_t(15));
-      f->tree_bytes.push_back(tb);
-      f->max_tree_bytes = std::max(f->max_tree_bytes, tb);
+      if (L.compact.size() & 1u) L.compact.push_back(CNode{0.0f, kLeafBit});
+      L.compact.push_back(CNode{0.0f, kLeafBit});  // tail padding for the last 16-byte copy
+      L.offsets.push_back((uint32_t)L.compact.size());
     }
-    if (f->compact.size() & 1u) f->compact.push_back(CNode{0.0f, kLeafBit});
-    f->compact.push_back(CNode{0.0f, kLeafBit});  // tail padding for the last 16-byte copy
-    f->offsets.push_back((uint32_t)f->compact.size());
     *out = f.release();
   });
 }
@@ -489,41 +499,73 @@ int st_eval_device(const st_tree* tree, const float* x, uint64_t m, uint32_t a, 
   });
 }
 
+}  // extern "C"
+
+namespace sti {
+// st_eval / st_eval_depths: the host-buffer pipeline around eval_device_impl
+// (stats and depths come back beside the labels, through the same slots).
+void eval_host(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+               const st_geom* geom, uint32_t* labels, st_stats* stats, uint32_t* depths) {
+  g_launches = 0;
+  st_tree* t = const_cast<st_tree*>(tree);
+  if (!t) fail(ST_ERR_ARGUMENT, "null tree");
+  uint64_t ld2 = ld;
+  check_common(m, a, ld2, layout, t->info.max_attribute);
+  st_geom g{};
+  if (geom) g = *geom;
+  if (!depths) resolve_algo(t, g, stats != nullptr);
+  if (m == 0) return;
+  if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
+  current_device();
+  std::vector<std::pair<uint32_t*, uint32_t*>> extra;
+  if (stats) {
+    if (!stats->iterations || !stats->doubling_steps)
+      fail(ST_ERR_ARGUMENT, "st_stats requires both arrays");
+    extra.push_back({stats->iterations, nullptr});
+    extra.push_back({stats->doubling_steps, nullptr});
+  }
+  if (depths) extra.push_back({depths, nullptr});
+  uint32_t launches = 0;
+  host_pipeline(x, m, a, ld2, layout, labels, extra,
+                [&](const float* xd, uint64_t rows, uint64_t ldd, uint32_t* lab,
+                    std::vector<uint32_t*>& ex, cudaStream_t s) {
+                  st_stats sd{};
+                  if (stats) {
+                    sd.iterations = ex[0];
+                    sd.doubling_steps = ex[1];
+                  }
+                  eval_device_impl(t, xd, rows, a, ldd, layout, &g, lab, stats ? &sd : nullptr, s,
+                                   depths ? ex.back() : nullptr);
+                  launches += g_launches;
+                  g_launches = 0;
+                });
+  g_launches = launches;
+}
+}  // namespace sti
+
+extern "C" {
+
 int st_eval(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
             const st_geom* geom, uint32_t* labels, st_stats* stats) {
+  return guarded([&] { eval_host(tree, x, m, a, ld, layout, geom, labels, stats, nullptr); });
+}
+
+int st_eval_depths(const st_tree* tree, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                   int layout, const st_geom* geom, uint32_t* labels, uint32_t* depths) {
+  return guarded([&] {
+    if (m && !depths) fail(ST_ERR_ARGUMENT, "null depth output");
+    eval_host(tree, x, m, a, ld, layout, geom, labels, nullptr, depths);
+  });
+}
+
+int st_eval_depths_device(const st_tree* tree, const float* x, uint64_t m, uint32_t a,
+                          uint64_t ld, int layout, const st_geom* geom, uint32_t* labels,
+                          uint32_t* depths, void* stream) {
   return guarded([&] {
     g_launches = 0;
-    st_tree* t = const_cast<st_tree*>(tree);
-    if (!t) fail(ST_ERR_ARGUMENT, "null tree");
-    uint64_t ld2 = ld;
-    check_common(m, a, ld2, layout, t->info.max_attribute);
-    st_geom g{};
-    if (geom) g = *geom;
-    resolve_algo(t, g, stats != nullptr);
-    if (m == 0) return;
-    if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
-    current_device();
-    std::vector<std::pair<uint32_t*, uint32_t*>> extra;
-    if (stats) {
-      if (!stats->iterations || !stats->doubling_steps)
-        fail(ST_ERR_ARGUMENT, "st_stats requires both arrays");
-      extra.push_back({stats->iterations, nullptr});
-      extra.push_back({stats->doubling_steps, nullptr});
-    }
-    uint32_t launches = 0;
-    host_pipeline(x, m, a, ld2, layout, labels, extra,
-                  [&](const float* xd, uint64_t rows, uint64_t ldd, uint32_t* lab,
-                      std::vector<uint32_t*>& ex, cudaStream_t s) {
-                    st_stats sd{};
-                    if (stats) {
-                      sd.iterations = ex[0];
-                      sd.doubling_steps = ex[1];
-                    }
-                    eval_device_impl(t, xd, rows, a, ldd, layout, &g, lab, stats ? &sd : nullptr, s);
-                    launches += g_launches;
-                    g_launches = 0;
-                  });
-    g_launches = launches;
+    if (m && !depths) fail(ST_ERR_ARGUMENT, "null depth output");
+    eval_device_impl(const_cast<st_tree*>(tree), x, m, a, ld, layout, geom, labels, nullptr,
+                     static_cast<cudaStream_t>(stream), depths);
   });
 }
 
@@ -661,16 +703,19 @@ int st_eval_timed(const st_tree* tree, const float* x, uint64_t m, uint32_t a, u
 }
 
 int st_forest_eval_device(const st_forest* forest, const float* x, uint64_t m, uint32_t a,
-                          uint64_t ld, int layout, uint32_t* labels, void* stream) {
+                          uint64_t ld, int layout, const st_geom* geom, uint32_t* labels,
+                          void* stream) {
   return guarded([&] {
     g_launches = 0;
-    forest_device_impl(const_cast<st_forest*>(forest), x, m, a, ld, layout, labels,
+    st_geom g{};
+    if (geom) g = *geom;
+    forest_device_impl(const_cast<st_forest*>(forest), x, m, a, ld, layout, g, labels,
                        static_cast<cudaStream_t>(stream));
   });
 }
 
 int st_forest_eval(const st_forest* forest, const float* x, uint64_t m, uint32_t a, uint64_t ld,
-                   int layout, uint32_t* labels) {
+                   int layout, const st_geom* geom, uint32_t* labels) {
   return guarded([&] {
     g_launches = 0;
     st_forest* f = const_cast<st_forest*>(forest);
@@ -680,11 +725,13 @@ int st_forest_eval(const st_forest* forest, const float* x, uint64_t m, uint32_t
     if (m == 0) return;
     if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
     current_device();
+    st_geom g{};
+    if (geom) g = *geom;
     uint32_t launches = 0;
     host_pipeline(x, m, a, ld2, layout, labels, {},
                   [&](const float* xd, uint64_t rows, uint64_t ldd, uint32_t* lab,
                       std::vector<uint32_t*>&, cudaStream_t s) {
-                    forest_device_impl(f, xd, rows, a, ldd, layout, lab, s);
+                    forest_device_impl(f, xd, rows, a, ldd, layout, g, lab, s);
                     launches += g_launches;
                     g_launches = 0;
                   });

@@ -4,10 +4,10 @@
 namespace sti {
 
 // ---- data kernel dispatch ------------------------------------------------
-template <int A, int S, int TLOC, int LOADER, int CAP>
+template <int A, int S, int TLOC, int LOADER, int CAP, bool DEPTH>
 void launch_data_t(const DataArgs& d, const Staging& stg, const ConstTree<CAP>* ct, size_t smem,
                    int dev, uint32_t bps, cudaStream_t s) {
-  auto fn = k_data<A, S, TLOC, LOADER, CAP>;
+  auto fn = k_data<A, S, TLOC, LOADER, CAP, DEPTH>;
   const uint64_t n_tiles = (d.p.m + 32 * S - 1) / (32 * S);
   const int blocks = blocks_for((const void*)fn, smem, dev, bps, n_tiles, stg.warps);
   static const ConstTree<1> dummy{};
@@ -36,35 +36,37 @@ void launch_data_t(const DataArgs& d, const Staging& stg, const ConstTree<CAP>* 
   check_launch();
 }
 
-template <int A, int S, int LOADER>
+// DEPTH (traversal depths beside the labels): record-major walks only, the
+// tree in shared memory, global memory (L1) or the 16-byte original nodes.
+template <int A, int S, int LOADER, bool DEPTH>
 void launch_data_tloc(int tloc, const DataArgs& d, const Staging& stg, const st_tree* t,
                       size_t smem, int dev, uint32_t bps, cudaStream_t s) {
   switch (tloc) {
     case ST_TREE_SHARED:
-      if constexpr ((A == 8 || A == 16) && LOADER == kTma) {
-        if (d.record_regs == 2) return launch_data_t<A, S, kSharedT, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
-        if (d.record_regs) return launch_data_t<A, S, kSharedReg, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
+      if constexpr ((A == 8 || A == 16) && LOADER == kTma && !DEPTH) {
+        if (d.record_regs == 2) return launch_data_t<A, S, kSharedT, LOADER, 1, DEPTH>(d, stg, nullptr, smem, dev, bps, s);
+        if (d.record_regs) return launch_data_t<A, S, kSharedReg, LOADER, 1, DEPTH>(d, stg, nullptr, smem, dev, bps, s);
       }
-      return launch_data_t<A, S, kShared, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
+      return launch_data_t<A, S, kShared, LOADER, 1, DEPTH>(d, stg, nullptr, smem, dev, bps, s);
     case ST_TREE_GLOBAL:
-      return launch_data_t<A, S, kGlobal, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
+      return launch_data_t<A, S, kGlobal, LOADER, 1, DEPTH>(d, stg, nullptr, smem, dev, bps, s);
     case ST_TREE_CONSTANT: {
-      if constexpr (LOADER == kTma) {
+      if constexpr (LOADER == kTma && !DEPTH) {
         if (t->compact.size() <= 512) {
           ConstTree<512> ct{};
           std::copy(t->compact.begin(), t->compact.end(), ct.n);
-          return launch_data_t<A, S, kConst, LOADER, 512>(d, stg, &ct, smem, dev, bps, s);
+          return launch_data_t<A, S, kConst, LOADER, 512, DEPTH>(d, stg, &ct, smem, dev, bps, s);
         }
         auto ct = std::make_unique<ConstTree<4000>>();
         std::copy(t->compact.begin(), t->compact.end(), ct->n);
-        return launch_data_t<A, S, kConst, LOADER, 4000>(d, stg, ct.get(), smem, dev, bps, s);
+        return launch_data_t<A, S, kConst, LOADER, 4000, DEPTH>(d, stg, ct.get(), smem, dev, bps, s);
       }
       break;
     }
     default:
       break;
   }
-  return launch_data_t<A, S, kWide, LOADER, 1>(d, stg, nullptr, smem, dev, bps, s);
+  return launch_data_t<A, S, kWide, LOADER, 1, DEPTH>(d, stg, nullptr, smem, dev, bps, s);
 }
 
 
@@ -82,20 +84,49 @@ uint32_t choose_S(uint32_t a, uint32_t want, bool small) {
   return S;
 }
 
-template <int A>
+template <int A, bool DEPTH>
 void launch_data_a(const Staging& stg, int tloc, const DataArgs& d, const st_tree* t, size_t smem,
                    int dev, uint32_t bps, cudaStream_t s) {
   if constexpr (A == 8 || A == 16) {
-    if (stg.S == 4) return launch_data_tloc<A, 4, kTma>(tloc, d, stg, t, smem, dev, bps, s);
+    if (stg.S == 4) return launch_data_tloc<A, 4, kTma, DEPTH>(tloc, d, stg, t, smem, dev, bps, s);
   }
   if constexpr (A == 8 || A == 16 || A == 32) {
-    if (stg.S == 2) return launch_data_tloc<A, 2, kTma>(tloc, d, stg, t, smem, dev, bps, s);
+    if (stg.S == 2) return launch_data_tloc<A, 2, kTma, DEPTH>(tloc, d, stg, t, smem, dev, bps, s);
   }
-  return launch_data_tloc<A, 1, kTma>(tloc, d, stg, t, smem, dev, bps, s);
+  return launch_data_tloc<A, 1, kTma, DEPTH>(tloc, d, stg, t, smem, dev, bps, s);
+}
+
+template <bool DEPTH>
+void launch_data(const Staging& stg, int tloc, const DataArgs& d, const st_tree* t, size_t smem,
+                 int dev, uint32_t bps, cudaStream_t s, uint32_t a) {
+  if (stg.loader == kTma && ct_arity(a)) {
+    switch (a) {
+      case 8: return launch_data_a<8, DEPTH>(stg, tloc, d, t, smem, dev, bps, s);
+      case 16: return launch_data_a<16, DEPTH>(stg, tloc, d, t, smem, dev, bps, s);
+      case 32: return launch_data_a<32, DEPTH>(stg, tloc, d, t, smem, dev, bps, s);
+      case 64: return launch_data_a<64, DEPTH>(stg, tloc, d, t, smem, dev, bps, s);
+    }
+  }
+  switch (stg.loader) {
+    case kTma: return launch_data_tloc<0, 1, kTma, DEPTH>(tloc, d, stg, t, smem, dev, bps, s);
+    case kDirect:
+      return launch_data_tloc<0, 1, kDirect, DEPTH>(tloc == ST_TREE_CONSTANT ? ST_TREE_GLOBAL : tloc, d,
+                                                    stg, t, smem, dev, bps, s);
+    default:
+      return launch_data_tloc<0, 1, kScalar, DEPTH>(tloc == ST_TREE_CONSTANT ? ST_TREE_GLOBAL : tloc, d,
+                                                    stg, t, smem, dev, bps, s);
+  }
 }
 
 void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
-                      const st_geom& g, uint32_t* labels, cudaStream_t s, int dev) {
+                      const st_geom& g0, uint32_t* labels, uint32_t* depths, cudaStream_t s, int dev) {
+  st_geom g = g0;
+  if (depths) {
+    // traversal depths come from the record-major walks; the constant-bank
+    // tree is a paper comparison variant without a depth counter
+    g.record_regs = 2;
+    if (g.tree_loc == ST_TREE_CONSTANT) g.tree_loc = ST_TREE_GLOBAL;
+  }
   st_tree::Dev& dv = t->device(dev);
   const DevProps pr = dev_props(dev);
   DataArgs d{};
@@ -106,6 +137,7 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   d.abits = t->abits;
   d.leaf_class = dv.leaf_tbl;
   d.labels = labels;
+  d.depths = depths;
   // records walked from registers: default for 8-attribute records; 16 on request
   // 8/16-attribute records: walk from registers (1), from the record-major
   // shared tile (0), or from the tile transposed in place to attribute-major
@@ -113,9 +145,8 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // frames vs registers; profiles/r1_ab_stages.txt); 16-attribute records
   // walk the record-major tile (C5 d12 / d16: transposed +10 / +11 %)
   d.record_regs = g.record_regs == 1 ? 1u : 0u;
-  if ((a == 8 || a == 16) && (g.record_regs == 3 || (g.record_regs == 0 && a == 8)))
-    d.record_regs = env_u32("ST_DATA_TRANSPOSE", 1) ? 2u : 1u;
-  d.bulk_tree = env_u32("ST_TREE_BULK", 1) ? 1u : 0u;
+  if ((a == 8 || a == 16) && (g.record_regs == 3 || (g.record_regs == 0 && a == 8))) d.record_regs = 2u;
+  d.bulk_tree = (g.variant & ST_VAR_TREE_LOOP) ? 0u : 1u;
 
 
   // fewer than 8 tiles of 32 records per warp at 32 warps on every SM
@@ -128,9 +159,9 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // reads `compact`.  Same-box A/B (profiles/r1_fold_ab.txt): C5 d12 -6 %,
   // C1 -5 %, C5 d16 / d20 -3 / -2 %; on small trees the post-loop terminal
   // step only lengthens each tile (C2 +4 %, C5 d8 +3 %), hence >= 2047 nodes.
-  const bool fold = t->fold_ok && t->nodes.size() >= env_u32("ST_DATA_FOLD_MIN", 2047) &&
+  const bool fold = t->fold_ok && t->nodes.size() >= (g.fold_min ? g.fold_min : 2047u) &&
                     (a == 8 || a == 16 || a == 32) &&
-                    !env_u32("ST_DATA_NO_FOLD", 0) &&
+                    !(g.variant & ST_VAR_NO_FOLD) &&
                     (g.tree_loc == ST_TREE_AUTO || g.tree_loc == ST_TREE_SHARED) &&
                     tma_ok(x, m, a, ld, layout, ct_arity(a) ? choose_S(a, g.samples_per_thread, small) : 1);
   uint32_t tree_bytes = round1024((fold ? t->folded.size() : t->nodes.size()) * sizeof(CNode));
@@ -194,30 +225,16 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // when one of their CTAs fits beside the ones launched per SM (small inputs:
   // C1 -6 % per launch in a back-to-back stream); otherwise the trigger is the
   // implicit one at exit (C1 / C3 -2 %; an early trigger without room cost
-  // C3 +5 %; tools/pdl_ab.py, profiles/r1_pdl_ab.txt).  ST_PDL: 0 off, 1 early,
-  // 2 at exit.
+  // C3 +5 %; tools/pdl_ab.py, profiles/r1_pdl_ab.txt).  st_geom.pdl: 0 auto,
+  // 1 early, 2 at exit, 3 off.
   {
     const size_t cta = smem + 1024;  // + the per-CTA shared-memory reservation
     const bool room = bps > 0 && (size_t)(bps + 1) * cta <= pr.smem_per_sm;
-    d.pdl = env_u32("ST_PDL", room ? 1u : 2u);
+    if (g.pdl > 3) fail(ST_ERR_ARGUMENT, "pdl must be 0-3");
+    d.pdl = g.pdl == 0 ? (room ? 1u : 2u) : g.pdl == 3 ? 0u : g.pdl;
   }
-  if (stg.loader == kTma && ct_arity(a)) {
-    switch (a) {
-      case 8: return launch_data_a<8>(stg, tloc, d, t, smem, dev, bps, s);
-      case 16: return launch_data_a<16>(stg, tloc, d, t, smem, dev, bps, s);
-      case 32: return launch_data_a<32>(stg, tloc, d, t, smem, dev, bps, s);
-      case 64: return launch_data_a<64>(stg, tloc, d, t, smem, dev, bps, s);
-    }
-  }
-  switch (stg.loader) {
-    case kTma: return launch_data_tloc<0, 1, kTma>(tloc, d, stg, t, smem, dev, bps, s);
-    case kDirect:
-      return launch_data_tloc<0, 1, kDirect>(tloc == ST_TREE_CONSTANT ? ST_TREE_GLOBAL : tloc, d,
-                                             stg, t, smem, dev, bps, s);
-    default:
-      return launch_data_tloc<0, 1, kScalar>(tloc == ST_TREE_CONSTANT ? ST_TREE_GLOBAL : tloc, d,
-                                             stg, t, smem, dev, bps, s);
-  }
+  if (depths) return launch_data<true>(stg, tloc, d, t, smem, dev, bps, s, a);
+  return launch_data<false>(stg, tloc, d, t, smem, dev, bps, s, a);
 }
 
 

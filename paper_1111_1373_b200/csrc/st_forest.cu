@@ -48,9 +48,11 @@ void launch_forest_u(uint32_t U, const Forest2Args& fa, const Staging& stg, size
 
 
 // Trees streamed through shared memory (packed votes, TMA-staged records).
-bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint64_t ld,
-                      int layout, uint32_t* labels, cudaStream_t s, int dev, const DevProps& pr) {
-  if (!(f->n_classes <= 8 && f->t_count <= 255) || f->max_tree_bytes > 48 * 1024) return false;
+bool forest_smem_path(st_forest* f, int lay, const float* x, uint64_t m, uint32_t a, uint64_t ld,
+                      int layout, const st_geom& g, uint32_t* labels, cudaStream_t s, int dev,
+                      const DevProps& pr) {
+  const st_forest::Layout& L = f->lay[lay];
+  if (!(f->n_classes <= 8 && f->t_count <= 255) || L.max_tree_bytes > 48 * 1024) return false;
   // one record per lane (the tile is transposed to attribute-major once per
   // round, which needs the record in registers); parallelism from wide CTAs
   const uint32_t S = 1;
@@ -68,18 +70,19 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   // walk is bound by shared-memory wavefronts of the node loads, so more
   // chains only add ring slots at the expense of record tiles.
   const bool transposed = S == 1 && a <= 64 && ct_arity(a);
-  const uint32_t U = std::max<uint32_t>(1, std::min<uint32_t>(4, env_u32("ST_FOREST_U", transposed ? 3 : 1)));
-  uint32_t nt = env_u32("ST_FOREST_NT", 0);
+  const uint32_t U = std::max<uint32_t>(1, std::min<uint32_t>(4, g.forest_chains ? g.forest_chains
+                                                                                 : (transposed ? 3u : 1u)));
+  uint32_t nt = g.forest_slots;
   if (nt == 0) nt = U + 3;
   if (!transposed && U != 1) return false;
   stg.warps = 0;
   size_t fixed = 0;
   for (uint32_t n = nt; n >= std::max<uint32_t>(2, U) && !stg.warps; --n) {
-    const size_t region = round1024((uint64_t)n * f->max_tree_bytes);
+    const size_t region = round1024((uint64_t)n * L.max_tree_bytes);
     const size_t base = 1024 + region + 16u * n;
     if (base >= pr.smem_optin) continue;
     uint32_t w = (uint32_t)std::min<size_t>(32, 1 + (pr.smem_optin - base) / (stg.stage_bytes + 8u));
-    if (const uint32_t ww = env_u32("ST_FOREST_W", 0)) w = std::min(w, ww);
+    if (g.warps_per_cta) w = std::min(w, g.warps_per_cta);
     if (w < 2) continue;
     stg.warps = w;
     nt = n;
@@ -87,7 +90,7 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   }
   if (!stg.warps) return false;
   make_tmap(stg, x, m, a);
-  st_forest::Dev& dv = f->device(dev);
+  st_forest::Dev& dv = f->device(dev, lay);
   Forest2Args fa{};
   fa.p = pipe_args(x, m, a, ld, layout);
   fa.nodes = dv.nodes;
@@ -97,9 +100,9 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
   fa.abits = f->abits;
   fa.labels = labels;
   fa.stage_bytes = stg.stage_bytes;
-  fa.tree_buf_bytes = f->max_tree_bytes;
+  fa.tree_buf_bytes = L.max_tree_bytes;
   fa.n_tree_bufs = nt;
-  fa.tree_region = round1024((uint64_t)nt * f->max_tree_bytes);
+  fa.tree_region = round1024((uint64_t)nt * L.max_tree_bytes);
   fa.tree_bytes = dv.tree_bytes;
   const size_t smem = fixed + (size_t)(stg.warps - 1) * (stg.stage_bytes + 8u);
   switch (a) {
@@ -112,15 +115,17 @@ bool forest_smem_path(st_forest* f, const float* x, uint64_t m, uint32_t a, uint
 }
 
 void forest_device_impl(st_forest* f, const float* x, uint64_t m, uint32_t a, uint64_t ld,
-                        int layout, uint32_t* labels, cudaStream_t s) {
+                        int layout, const st_geom& g, uint32_t* labels, cudaStream_t s) {
   if (!f) fail(ST_ERR_ARGUMENT, "null forest");
   check_common(m, a, ld, layout, f->max_attribute);
   if (m == 0) return;
   if (!x || !labels) fail(ST_ERR_ARGUMENT, "null data or label pointer");
+  if (g.forest_chains > 4) fail(ST_ERR_ARGUMENT, "forest_chains must be 0-4");
   const int dev = current_device();
   const DevProps pr = dev_props(dev);
-  if (forest_smem_path(f, x, m, a, ld, layout, labels, s, dev, pr)) return;
-  st_forest::Dev& dv = f->device(dev);
+  const int lay = (g.variant & ST_VAR_NO_FOLD) ? 1 : 0;
+  if (forest_smem_path(f, lay, x, m, a, ld, layout, g, labels, s, dev, pr)) return;
+  st_forest::Dev& dv = f->device(dev, lay);
   ForestArgs fa{};
   fa.p = pipe_args(x, m, a, ld, layout);
   fa.nodes = dv.nodes;

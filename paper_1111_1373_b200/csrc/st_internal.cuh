@@ -29,6 +29,7 @@
 using namespace stk;
 
 static_assert(sizeof(st_node) == 16, "st_node must match spectree::EncodedNode");
+static_assert(sizeof(st_geom) == 96, "st_geom is part of the ABI (24 uint32 fields)");
 static_assert(offsetof(st_node, attribute) == 0 && offsetof(st_node, threshold) == 4 &&
                   offsetof(st_node, child) == 8 && offsetof(st_node, class_id) == 12,
               "st_node field offsets must match spectree::EncodedNode");
@@ -149,7 +150,7 @@ struct st_tree {
   st_tree_info info{};
   uint32_t abits = 1;
   bool compact_ok = true;
-  bool leaf_table = false;            // some class >= 2^31: leaves carry ordinals
+  bool leaf_table = false;            // some class >= 2^30: leaves carry ordinals
   std::vector<uint32_t> leaf_classes;  // ordinal -> class
   std::vector<uint32_t> leaf_code;     // node -> code payload (class or ordinal)
   std::vector<CNode> compact;
@@ -408,10 +409,15 @@ struct st_tree {
 };
 
 struct st_forest {
-  std::vector<CNode> compact;      // trees concatenated, each starting 16-byte aligned
-  std::vector<uint32_t> offsets;   // first node of each tree (+ end sentinel)
-  std::vector<uint32_t> tree_bytes;  // bytes per tree rounded up to 16 (bulk-copy size)
-  uint32_t max_tree_bytes = 0;
+  // Two node layouts of the same trees: [0] folded where the encoding allows
+  // (leaf pairs inside terminal nodes, fold_tree; the default), [1] plain
+  // compact nodes (ST_VAR_NO_FOLD).  Labels are identical.
+  struct Layout {
+    std::vector<CNode> compact;        // trees concatenated, each starting 16-byte aligned
+    std::vector<uint32_t> offsets;     // first node of each tree (+ end sentinel)
+    std::vector<uint32_t> tree_bytes;  // bytes per tree rounded up to 16 (bulk-copy size)
+    uint32_t max_tree_bytes = 0;
+  } lay[2];
   uint32_t t_count = 0, n_classes = 0, abits = 1, max_attribute = 0;
   std::mutex mu;
   struct Dev {
@@ -419,30 +425,31 @@ struct st_forest {
     uint32_t* offsets = nullptr;
     uint32_t* tree_bytes = nullptr;
   };
-  std::map<int, Dev> dev;
+  std::map<std::pair<int, int>, Dev> dev;  // (device, layout)
   ~st_forest() {
     int cur = -1;
     cudaGetDevice(&cur);
     for (auto& kv : dev) {
-      if (cudaSetDevice(kv.first) != cudaSuccess) continue;
+      if (cudaSetDevice(kv.first.first) != cudaSuccess) continue;
       cudaFree(kv.second.nodes);
       cudaFree(kv.second.offsets);
       cudaFree(kv.second.tree_bytes);
     }
     if (cur >= 0) cudaSetDevice(cur);
   }
-  Dev& device(int d) {
+  Dev& device(int d, int l) {
     std::lock_guard<std::mutex> lk(mu);
-    auto it = dev.find(d);
+    auto it = dev.find({d, l});
     if (it != dev.end()) return it->second;
+    const Layout& L = lay[l];
     Dev dv;
-    CK(cudaMalloc(&dv.nodes, compact.size() * sizeof(CNode) + 16));
-    CK(cudaMemcpy(dv.nodes, compact.data(), compact.size() * sizeof(CNode), cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&dv.offsets, offsets.size() * 4));
-    CK(cudaMemcpy(dv.offsets, offsets.data(), offsets.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&dv.tree_bytes, tree_bytes.size() * 4));
-    CK(cudaMemcpy(dv.tree_bytes, tree_bytes.data(), tree_bytes.size() * 4, cudaMemcpyHostToDevice));
-    return dev.emplace(d, dv).first->second;
+    CK(cudaMalloc(&dv.nodes, L.compact.size() * sizeof(CNode) + 16));
+    CK(cudaMemcpy(dv.nodes, L.compact.data(), L.compact.size() * sizeof(CNode), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&dv.offsets, L.offsets.size() * 4));
+    CK(cudaMemcpy(dv.offsets, L.offsets.data(), L.offsets.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&dv.tree_bytes, L.tree_bytes.size() * 4));
+    CK(cudaMemcpy(dv.tree_bytes, L.tree_bytes.data(), L.tree_bytes.size() * 4, cudaMemcpyHostToDevice));
+    return dev.emplace(std::make_pair(d, l), dv).first->second;
   }
 };
 
@@ -520,7 +527,10 @@ inline std::unique_ptr<st_tree> make_tree(const st_node* nodes, uint32_t n) {
       ++in.leaves;
       in.depth = std::max(in.depth, depth[i]);
       in.max_class = std::max(in.max_class, nd.class_id);
-      if (nd.class_id >= kLeafBit) t->leaf_table = true;
+      // classes >= 2^30 would collide with the folded-terminal marker
+      // (kPairBit) in the inline leaf encoding: leaves then carry ordinals
+      // into a class table instead
+      if (nd.class_id >= kPairBit) t->leaf_table = true;
     } else {
       ++in.internal;
       depth[nd.child] = std::max(depth[nd.child], depth[i] + 1);
@@ -746,20 +756,17 @@ inline PipeArgs pipe_args(const float* x, uint64_t m, uint32_t a, uint64_t ld, i
   return p;
 }
 
-inline uint32_t env_u32(const char* name, uint32_t dflt) {  // development knobs for sweeps
-  const char* v = std::getenv(name);
-  return v && *v ? (uint32_t)std::strtoul(v, nullptr, 10) : dflt;
-}
 // Compile-time arities with a TMA fast path; everything else runs A = 0.
 inline bool ct_arity(uint32_t a) { return a == 8 || a == 16 || a == 32 || a == 64; }
 
 // ---- cross-translation-unit entry points ------------------------------------
 void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
-                      const st_geom& g, uint32_t* labels, cudaStream_t s, int dev);   // st_data.cu
+                      const st_geom& g, uint32_t* labels, uint32_t* depths, cudaStream_t s,
+                      int dev);                                                         // st_data.cu
 void spec_geometry(const st_tree* t, const st_geom& g, uint32_t& G, uint32_t& H);     // st_spec.cu
 void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
                       const st_geom& g, uint32_t* labels, st_stats* stats, cudaStream_t s,
                       int dev);                                                         // st_spec.cu
 void forest_device_impl(st_forest* f, const float* x, uint64_t m, uint32_t a, uint64_t ld,
-                        int layout, uint32_t* labels, cudaStream_t s);                 // st_forest.cu
+                        int layout, const st_geom& g, uint32_t* labels, cudaStream_t s);  // st_forest.cu
 }  // namespace sti

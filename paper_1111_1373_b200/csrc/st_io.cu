@@ -118,7 +118,10 @@ st_dataset_info read_info(int fd, const std::string& path) {
     fail(ST_ERR_IO, path + ": bad layout " + std::to_string(layout));
   if (arity == 0) fail(ST_ERR_IO, path + ": dataset arity must be >= 1");
   const off_t end = ::lseek(fd, 0, SEEK_END);
-  if (end < 0 || (uint64_t)end != kRecHeader + count * (uint64_t)arity * 4)
+  // count * arity * 4 must not wrap: a crafted header could otherwise pass
+  // the size check on a short file and size the caller's allocations
+  if (count > (UINT64_MAX - kRecHeader) / (4ull * arity) || end < 0 ||
+      (uint64_t)end != kRecHeader + count * (uint64_t)arity * 4)
     fail(ST_ERR_IO, path + ": file size does not match " + std::to_string(count) + " records of arity " +
                         std::to_string(arity));
   st_dataset_info in{};
@@ -304,7 +307,8 @@ int st_labels_load(const char* path, uint32_t* out, uint64_t cap, uint64_t* coun
     std::memcpy(&m, hd + 16, 8);
     if (version != 1 || (w != 1 && w != 4)) fail(ST_ERR_IO, std::string(path) + ": bad label header");
     const off_t end = ::lseek(fd.fd, 0, SEEK_END);
-    if (end < 0 || (uint64_t)end != kLabHeader + m * w) fail(ST_ERR_IO, std::string(path) + ": truncated label file");
+    if (m > (UINT64_MAX - kLabHeader) / w || end < 0 || (uint64_t)end != kLabHeader + m * w)
+      fail(ST_ERR_IO, std::string(path) + ": truncated label file");
     if (count) *count = m;
     if (width) *width = w;
     if (!out) return;

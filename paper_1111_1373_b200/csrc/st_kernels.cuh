@@ -341,6 +341,7 @@ struct DataArgs {
   uint32_t record_regs;        // host hint: 8-attribute records walk from registers (kSharedReg)
   uint32_t bulk_tree;          // stage the shared tree with one cp.async.bulk (else per-thread loads)
   uint32_t pdl;                // launched as a programmatic dependent (griddepcontrol)
+  uint32_t* depths;            // k_data<DEPTH>: per-record traversal depth (edges root -> leaf)
 };
 
 // Shared-memory carve-out shared by the kernels:
@@ -372,6 +373,30 @@ __device__ __forceinline__ void data_step(uint32_t& thr, uint32_t& meta, uint32_
       "@p ld.shared.v2.u32 {%0, %1}, [ch];\n\t"
       "}"
       : "+f"(*reinterpret_cast<float*>(&thr)), "+r"(meta)
+      : "r"(bx), "r"(amask), "r"(abits)
+      : "memory");
+}
+
+// data_step that also counts the edges taken (traversal depth,
+// eval_serial.cpp:77-105): one predicated add on the internal-node predicate.
+__device__ __forceinline__ void data_step_d(uint32_t& thr, uint32_t& meta, uint32_t bx, uint32_t amask,
+                                            uint32_t abits, uint32_t& depth) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p, q;\n\t"
+      ".reg .u32 fa, ch;\n\t"
+      ".reg .f32 v;\n\t"
+      "setp.ge.s32 p, %1, 0;\n\t"
+      "and.b32 fa, %1, %4;\n\t"
+      "xor.b32 fa, fa, %3;\n\t"
+      "@p ld.shared.f32 v, [fa];\n\t"
+      "setp.gt.and.f32 q, v, %0, p;\n\t"
+      "shr.u32 ch, %1, %5;\n\t"
+      "@q add.u32 ch, ch, 8;\n\t"
+      "@p add.u32 %2, %2, 1;\n\t"
+      "@p ld.shared.v2.u32 {%0, %1}, [ch];\n\t"
+      "}"
+      : "+f"(*reinterpret_cast<float*>(&thr)), "+r"(meta), "+r"(depth)
       : "r"(bx), "r"(amask), "r"(abits)
       : "memory");
 }
@@ -435,10 +460,14 @@ __device__ __forceinline__ float pick_reg(const float (&f)[A], uint32_t meta) {
   return v[0];
 }
 
-template <int A, int S, int TLOC, int LOADER, int CAP>
+// DEPTH: also write each record's traversal depth (edges root -> leaf,
+// eval_serial.cpp:77-105) to args.depths; the host never pairs it with the
+// register / transposed walks (kSharedReg, kSharedT).
+template <int A, int S, int TLOC, int LOADER, int CAP, bool DEPTH = false>
 __global__ void __launch_bounds__(kMaxThreads)
     k_data(const DataArgs args, const __grid_constant__ CUtensorMap tmap,
            const __grid_constant__ ConstTree<CAP> ctree) {
+  static_assert(!DEPTH || (TLOC != kSharedReg && TLOC != kSharedT), "depth output: record-major walks");
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int R = 32 * S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -542,11 +571,14 @@ __global__ void __launch_bounds__(kMaxThreads)
         Rec<A, LOADER> rec;
         rec.init(tile, r, args.p.a, args.p.x, r0 + r, args.p.ld, args.p.layout_soa);
         uint4 nd = __ldg(args.wide);
+        uint32_t dep = 0;
         while (nd.w == kNoClass) {
           const uint32_t c = nd.z + (uint32_t)(rec.get(nd.x * 4u) > __uint_as_float(nd.y));
           nd = __ldg(args.wide + c);
+          ++dep;
         }
         args.labels[r0 + r] = nd.w;
+        if constexpr (DEPTH) args.depths[r0 + r] = dep;
       }
     } else if constexpr (TLOC == kSharedT && LOADER == kTma && (A == 8 || A == 16)) {
       // transpose the warp's tile in place, one 32-record chunk at a time, to
@@ -655,7 +687,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       continue;  // stage already released
     } else if constexpr (TLOC == kShared && LOADER == kTma && Rec<A, LOADER>::kRowLocal) {
       // S independent predicated chains per lane (no per-level branches)
-      uint32_t thr[S], meta[S], bx[S];
+      uint32_t thr[S], meta[S], bx[S], dep[S];
       const uint2 root = tree.get(tree.root());
 #pragma unroll
       for (int q = 0; q < S; ++q) {
@@ -665,6 +697,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         bx[q] = rec.base | rec.xm;
         thr[q] = root.x;
         meta[q] = (r0 + r < m) ? root.y : kLeafBit;  // idle slot in the tail tile
+        dep[q] = 0;
       }
       while (true) {
         bool any = false;
@@ -672,7 +705,10 @@ __global__ void __launch_bounds__(kMaxThreads)
         for (int q = 0; q < S; ++q) any |= (int)meta[q] >= 0;
         if (!any) break;
 #pragma unroll
-        for (int q = 0; q < S; ++q) data_step(thr[q], meta[q], bx[q], amask, args.abits);
+        for (int q = 0; q < S; ++q) {
+          if constexpr (DEPTH) data_step_d(thr[q], meta[q], bx[q], amask, args.abits, dep[q]);
+          else data_step(thr[q], meta[q], bx[q], amask, args.abits);
+        }
       }
 #pragma unroll
       for (int q = 0; q < S; ++q) {  // folded terminal: last predicate picks the leaf of the pair
@@ -680,6 +716,7 @@ __global__ void __launch_bounds__(kMaxThreads)
           const float v = lds_f32((meta[q] & 0x3FFu) ^ bx[q]);
           const uint32_t c = (v > __uint_as_float(thr[q])) ? (meta[q] >> 20) : (meta[q] >> 10);
           meta[q] = kLeafBit | (c & 0x3FFu);
+          dep[q] += 1;  // the terminal's edge to the leaf it picks
         }
       }
 #pragma unroll
@@ -688,6 +725,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         if (r < m) {
           const uint32_t c = meta[q] & ~kLeafBit;
           args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+          if constexpr (DEPTH) args.depths[r] = dep[q];
         }
       }
     } else if constexpr (S == 1) {
@@ -698,21 +736,24 @@ __global__ void __launch_bounds__(kMaxThreads)
       uint2 nd = tree.get(tree.root());
       uint32_t meta = valid ? nd.y : kLeafBit;
       float thr = __uint_as_float(nd.x);
+      uint32_t dep = 0;
       // Branch-free successor per level: child + (x > thr), as byte offsets.
       while (!(meta & kLeafBit)) {
         const float v = rec.get(meta & amask);
         nd = tree.get((meta >> args.abits) + (v > thr ? 8u : 0u));
         thr = __uint_as_float(nd.x);
         meta = nd.y;
+        ++dep;
       }
       if (valid) {
         const uint32_t c = meta & ~kLeafBit;
         args.labels[r0 + r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+        if constexpr (DEPTH) args.depths[r0 + r] = dep;
       }
     } else {
       Rec<A, LOADER> rec[S];
       float thr[S];
-      uint32_t meta[S];
+      uint32_t meta[S], dep[S];
       const uint2 root = tree.get(tree.root());
 #pragma unroll
       for (int q = 0; q < S; ++q) {
@@ -720,6 +761,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         rec[q].init(tile, r, args.p.a, args.p.x, r0 + (r0 + r < m ? r : 0), args.p.ld, args.p.layout_soa);
         thr[q] = __uint_as_float(root.x);
         meta[q] = (r0 + r < m) ? root.y : kLeafBit;  // idle slot in the tail tile
+        dep[q] = 0;
       }
       // Branch-free successor per level: child + (x > thr), as byte offsets.
       while (true) {
@@ -732,6 +774,7 @@ __global__ void __launch_bounds__(kMaxThreads)
             const uint2 nd = tree.get(off);
             thr[q] = __uint_as_float(nd.x);
             meta[q] = nd.y;
+            dep[q] += 1;
             any = true;
           }
         }
@@ -743,6 +786,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         if (r < m) {
           const uint32_t c = meta[q] & ~kLeafBit;
           args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+          if constexpr (DEPTH) args.depths[r] = dep[q];
         }
       }
     }
@@ -946,7 +990,6 @@ __global__ void __launch_bounds__(kMaxThreads)
 struct SpecRingArgs {
   SpecArgs s;
   uint32_t n_slots;       // NS
-  uint32_t unsafe_no_gen; // benchmark-only: skip the slot-generation handshake
   uint32_t bulk_win;      // stage the window table with one cp.async.bulk (else per-thread loads)
   uint32_t tile_mult;     // host: records per ring slot / 32 (the kernel's RT)
 };
@@ -1102,11 +1145,10 @@ __global__ void __launch_bounds__(kMaxThreads)
     // finished tk - NS publishes it), then the parity wait is unambiguous.
     // The generation word only gates *which* phase to wait for; the tile's
     // bytes are published by the mbarrier (complete_tx, acquire on the wait),
-    // so plain volatile shared accesses suffice.  (ra.unsafe_no_gen skips the
-    // handshake: racy, for measuring its cost only.)
+    // so plain volatile shared accesses suffice.
     // Every lane polls the same word (one broadcast wavefront, warp-uniform
     // exit): no divergent lane-0 section before the walk's shuffles.
-    if (!ra.unsafe_no_gen) {
+    {
       const uint32_t g = tk / NS;
       uint32_t have;
       do {
@@ -1680,12 +1722,15 @@ struct SpecExactArgs {
   uint32_t* labels;
   uint32_t* iters;
   uint32_t* steps;
+  uint32_t* gbuf;          // null: path buffers in shared memory; else 2n + 1 words per CTA
+                           // in global memory (trees whose two path arrays exceed shared memory)
 };
 
 template <int = 0>  // a template so every translation unit may include this header
 __global__ void __launch_bounds__(kMaxThreads) k_spec_exact_cta(const SpecExactArgs args) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  uint32_t* buf_a = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* buf_a = args.gbuf ? args.gbuf + (uint64_t)blockIdx.x * (2ull * args.n + 1)
+                              : reinterpret_cast<uint32_t*>(smem);
   uint32_t* buf_b = buf_a + args.n;
   uint32_t& root_val = buf_b[args.n];  // dynamic smem only: opt-in size stays valid
   for (uint32_t i = threadIdx.x; i < args.n; i += blockDim.x) buf_a[i] = buf_b[i] = i;

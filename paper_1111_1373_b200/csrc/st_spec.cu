@@ -157,8 +157,10 @@ void eval_spec_exact_cta(st_tree* t, const float* x, uint64_t m, uint32_t a, uin
   ea.labels = labels;
   ea.iters = stats->iterations;
   ea.steps = stats->doubling_steps;
-  const size_t smem = 8ull * t->nodes.size() + 16;
-  if (smem > pr.smem_optin) fail(ST_ERR_ARGUMENT, "tree too large for exact speculative counters");
+  // the two path arrays (+ the root word) per CTA: shared memory when they
+  // fit, else a per-CTA slice of a stream-ordered global buffer
+  const bool global_bufs = 8ull * t->nodes.size() + 16 > pr.smem_optin;
+  const size_t smem = global_bufs ? 0 : 8ull * t->nodes.size() + 16;
   const uint32_t threads = std::min<uint32_t>(1024, std::max<uint32_t>(32, (ea.I + 31) / 32 * 32));
   auto fn = k_spec_exact_cta<0>;
   static std::mutex mu;
@@ -174,9 +176,14 @@ void eval_spec_exact_cta(st_tree* t, const float* x, uint64_t m, uint32_t a, uin
   int occ = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, (int)threads, smem));
   const uint64_t blocks = std::min<uint64_t>(m, (uint64_t)pr.sms * std::max(occ, 1));
+  if (global_bufs) {
+    const size_t bytes = (size_t)blocks * (2ull * t->nodes.size() + 1) * 4;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&ea.gbuf), bytes, s));
+  }
   clear_stale_error();
   fn<<<(unsigned)blocks, threads, smem, s>>>(ea);
   check_launch();
+  if (global_bufs) CK(cudaFreeAsync(ea.gbuf, s));
 }
 
 void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
@@ -240,12 +247,12 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // CTA-shared ring (default for the fast path): up to 32 warps on one SM
   // share NS = warps + 12 tile slots; ~12 tiles in flight cover DRAM latency.
   if (stg.loader == kTma && !stats && g.pipeline != 1) {
-    const bool onewin = wt->windows == 1 && win_shared && !env_u32("ST_SPEC_NO_ONEWIN", 0);
+    const bool onewin = wt->windows == 1 && win_shared && !(g.variant & ST_VAR_SPEC_GENERAL);
     SpecArgs rs = sa;
     bool ws = win_shared, cw = false;
     // 8-byte window entries when the tree's fields fit (half the entry
-    // wavefronts); ST_SPEC_WIDE_WIN=1 keeps the 16-byte format
-    if (!onewin && wt->cw_units && !env_u32("ST_SPEC_WIDE_WIN", 0)) {
+    // wavefronts); ST_VAR_SPEC_WIDE keeps the 16-byte format
+    if (!onewin && wt->cw_units && !(g.variant & ST_VAR_SPEC_WIDE)) {
       const uint32_t cb = round1024((size_t)wt->cw_units * sizeof(SEntry));
       if (cb <= 96 * 1024) {
         cw = ws = true;
@@ -275,11 +282,11 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     // the streams' window counts and halves the per-slot overhead -- taken
     // when the slot stays at 4 KB (16 attributes: C5 d8 / d12 / d16 / d20
     // -5 / -10 / -8 / -6 %, C1 even).  Larger slots cost resident warps (C2,
-    // 8 KB: +44 %); 2 KB ones gained nothing (C3 +2 %).  ST_SPEC_TILE=1 / 2
-    // forces 32 / 64 (profiles/r1_spec_tile_ab.txt).
+    // 8 KB: +44 %); 2 KB ones gained nothing (C3 +2 %).  st_geom.slot_records
+    // = 1 / 2 forces 32 / 64 (profiles/r1_spec_tile_ab.txt).
     uint32_t rt = 1;
     Staging rstg = stg;
-    const uint32_t want_rt = env_u32("ST_SPEC_TILE", a == 16 ? 2u : 1u);
+    const uint32_t want_rt = g.slot_records ? g.slot_records : (a == 16 ? 2u : 1u);
     if (cw && sr >= 2 && (a == 8 || a == 16 || a == 32) && want_rt == 2 && m >= 64) {
       Staging s2 = plan_staging(x, m, a, ld, layout, 2, g.stages, rs.win_bytes, pr);
       if (s2.loader == kTma && s2.S == 2) rt = 2, rstg = s2;
@@ -292,16 +299,15 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       SpecRingArgs ra{};
       ra.s = rs;
       ra.n_slots = (uint32_t)std::min<size_t>(max_slots, warps + 12);
-      // development / stress knob: any ring depth >= 1 must give exact labels
-      if (const uint32_t ns = env_u32("ST_SPEC_RING_SLOTS", 0)) ra.n_slots = std::min<uint32_t>(ra.n_slots, ns);
-      ra.unsafe_no_gen = env_u32("ST_SPEC_RING_UNSAFE_NO_GEN", 0);  // measurement of the handshake only
-      ra.bulk_win = env_u32("ST_TREE_BULK", 1) ? 1u : 0u;
+      // stress knob: any ring depth >= 1 must give exact labels
+      if (g.ring_slots) ra.n_slots = std::min<uint32_t>(ra.n_slots, g.ring_slots);
+      ra.bulk_win = (g.variant & ST_VAR_TREE_LOOP) ? 0u : 1u;
       ra.tile_mult = rt;
       ra.s.stage_bytes = rstg.stage_bytes;
       const size_t rsmem = 1024 + rs.win_bytes + (size_t)ra.n_slots * (rstg.stage_bytes + 8u) +
                            (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128 * rt;
       // one window: ballot + leaf path masks unless pointer jumping is asked for
-      if (onewin) ra.s.pm_off = env_u32("ST_SPEC_ONEWIN_JUMP", 0) ? 0u : wt->pm_off;
+      if (onewin) ra.s.pm_off = (g.variant & ST_VAR_SPEC_JUMP) ? 0u : wt->pm_off;
       switch (ct_arity(a) ? a : 0) {
         case 8: return launch_spec_ring<8>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
         case 16: return launch_spec_ring<16>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);

@@ -35,6 +35,11 @@ _ALGOS = {"auto": _lib.ST_ALGO_AUTO, "data": _lib.ST_ALGO_DATA,
           "speculative": _lib.ST_ALGO_SPECULATIVE, "spec": _lib.ST_ALGO_SPECULATIVE}
 _TREE_LOCS = {"auto": _lib.ST_TREE_AUTO, "shared": _lib.ST_TREE_SHARED,
               "constant": _lib.ST_TREE_CONSTANT, "global": _lib.ST_TREE_GLOBAL}
+# st_geom.variant flags (spectree_b200.h st_variant): implementation variants
+# the tuned defaults were measured against; labels never depend on them.
+VARIANTS = {"no_fold": _lib.ST_VAR_NO_FOLD, "tree_loop": _lib.ST_VAR_TREE_LOOP,
+            "spec_general": _lib.ST_VAR_SPEC_GENERAL, "spec_jump": _lib.ST_VAR_SPEC_JUMP,
+            "spec_wide": _lib.ST_VAR_SPEC_WIDE}
 
 
 def _check(rc: int) -> None:
@@ -57,6 +62,13 @@ class GpuGeom:
     warps_per_cta: int = 0          # CTA width (warps)
     pipeline: int = 0               # 0 auto, 1 per-warp TMA ring, 2 CTA-shared ring (spec)
     record_regs: int = 0            # data, 8/16-attribute records: 0 auto (3 for 8), 1 registers, 2 shared tile, 3 transposed tile
+    variant: tuple = ()             # names from VARIANTS (A/B implementation variants)
+    ring_slots: int = 0             # speculative ring: cap on tile slots (stress tests)
+    slot_records: int = 0           # speculative ring: records per slot / 32 (1 or 2)
+    fold_min: int = 0               # data: fold trees with >= this many nodes (0 = 2047)
+    pdl: int = 0                    # data: 0 auto, 1 early trigger, 2 at exit, 3 off
+    forest_chains: int = 0          # forest: trees per lane at once (1-4)
+    forest_slots: int = 0           # forest: tree ring slots
 
     def to_c(self) -> st_geom:
         g = st_geom()
@@ -75,6 +87,19 @@ class GpuGeom:
         g.warps_per_cta = self.warps_per_cta
         g.pipeline = self.pipeline
         g.record_regs = self.record_regs
+        names = (self.variant,) if isinstance(self.variant, str) else tuple(self.variant)
+        flags = 0
+        for n in names:
+            if n not in VARIANTS:
+                raise ArgumentError(f"unknown variant '{n}' (known: {', '.join(sorted(VARIANTS))})")
+            flags |= VARIANTS[n]
+        g.variant = flags
+        g.ring_slots = self.ring_slots
+        g.slot_records = self.slot_records
+        g.fold_min = self.fold_min
+        g.pdl = self.pdl
+        g.forest_chains = self.forest_chains
+        g.forest_slots = self.forest_slots
         return g
 
 
@@ -118,6 +143,45 @@ def check_attribute_range(tree: EncodedTree, dataset: Dataset) -> None:
                             f"arity {dataset.arity()}")
 
 
+def _u32_out(out, m, what="out"):
+    if out is None:
+        return np.empty(m, dtype=np.uint32)
+    if out.dtype != np.uint32 or out.size != m or not out.flags.c_contiguous:
+        raise ArgumentError(f"{what} must be a contiguous uint32 array of one entry per record")
+    return out
+
+
+def traversal_depths(tree, dataset, geom: Optional[GpuGeom] = None,
+                     labels_out: Optional[np.ndarray] = None) -> np.ndarray:
+    """Per-record traversal depth -- edges from the root to the leaf reached
+    (reference traversal_depths, eval_serial.cpp:77-105) -- computed on the GPU
+    by the data kernel beside the labels (``st_eval_depths``)."""
+    tree = _as_tree(tree)
+    dataset = _as_data(dataset)
+    check_attribute_range(tree, dataset)
+    m = dataset.count()
+    depths = np.empty(m, dtype=np.uint32)
+    labels = _u32_out(labels_out, m, "labels_out")
+    g = (geom or GpuGeom()).to_c()
+    x = dataset.values()
+    L = _lib.load()
+    h = tree.handle()
+    _check(L.st_eval_depths(h.h, x.ctypes.data_as(C.c_void_p) if m else None, m, dataset.arity(), 0,
+                            _lib.ST_LAYOUT_AOS, C.byref(g), labels.ctypes.data_as(C.c_void_p) if m else None,
+                            depths.ctypes.data_as(C.c_void_p) if m else None))
+    return depths
+
+
+def mean_traversal_depth(tree, dataset, geom: Optional[GpuGeom] = None) -> float:
+    """eval_serial.cpp:99-110: mean of traversal_depths; an empty dataset
+    raises ArgumentError, as in the reference."""
+    dataset = _as_data(dataset)
+    if dataset.count() == 0:
+        raise ArgumentError("mean traversal depth of an empty dataset")
+    d = traversal_depths(tree, dataset, geom)
+    return float(d.sum(dtype=np.uint64)) / len(d)
+
+
 def eval_gpu(tree, dataset, geom: Optional[GpuGeom] = None, stats: Optional["SpeculativeStats"] = None,
              layout: str = "aos", out: Optional[np.ndarray] = None) -> np.ndarray:
     """Host-buffer evaluation through ``st_eval`` (H2D + kernel + D2H).
@@ -126,10 +190,7 @@ def eval_gpu(tree, dataset, geom: Optional[GpuGeom] = None, stats: Optional["Spe
     dataset = _as_data(dataset)
     check_attribute_range(tree, dataset)
     m = dataset.count()
-    if out is None:
-        out = np.empty(m, dtype=np.uint32)
-    if out.dtype != np.uint32 or out.size != m or not out.flags.c_contiguous:
-        raise ArgumentError("out must be a contiguous uint32 array of one label per record")
+    out = _u32_out(out, m)
     g = (geom or GpuGeom()).to_c()
     x = dataset.values()
     if layout == "soa":
@@ -321,36 +382,86 @@ def _stream_handle(stream):
     return C.c_void_p(stream.cuda_stream)
 
 
-def eval_device(tree, x, labels, geom: Optional[GpuGeom] = None, layout: str = "aos",
-                stream=None, stats=None) -> None:
-    """Enqueue one evaluation of device tensor ``x`` into device tensor
-    ``labels`` (uint32/int32, m elements) on ``stream``.  AoS x is (m, a);
-    SoA x is (a, m).  Asynchronous."""
-    tree = _as_tree(tree)
-    if not x.is_cuda or not labels.is_cuda:
-        raise ArgumentError("eval_device expects CUDA tensors")
+def _device_records(x, layout: str):
+    """(m, a, ld, st_layout) of a float32 CUDA tensor on the current device
+    (AoS x is (m, a), SoA x is (a, m)); raises ArgumentError otherwise."""
+    import torch
+
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise ArgumentError("expected a CUDA tensor of records")
+    if x.dtype != torch.float32:
+        raise ArgumentError(f"records must be float32, got {x.dtype}")
+    if x.dim() != 2:
+        raise ArgumentError(f"records must be a 2-D tensor, got shape {tuple(x.shape)}")
+    if x.device.index != torch.cuda.current_device():
+        raise ArgumentError(f"records live on {x.device}, the current device is "
+                            f"cuda:{torch.cuda.current_device()}")
     # strides of size-1 dimensions carry no information (torch reports 1)
     if layout == "aos":
         m, a = x.shape
         ld = x.stride(0) if m > 1 else a
-        lay = _lib.ST_LAYOUT_AOS
         if x.stride(1) != 1 and a > 1:
             raise ArgumentError("AoS tensor must have unit attribute stride")
-    else:
+        return m, a, ld, _lib.ST_LAYOUT_AOS
+    if layout == "soa":
         a, m = x.shape
         ld = x.stride(0) if a > 1 else m
-        lay = _lib.ST_LAYOUT_SOA
         if x.stride(1) != 1 and m > 1:
             raise ArgumentError("SoA tensor must have unit record stride")
+        return m, a, ld, _lib.ST_LAYOUT_SOA
+    raise ArgumentError(f"unknown layout '{layout}'")
+
+
+def _device_u32(t, m: int, what: str, device) -> C.c_void_p:
+    """Pointer of a CUDA tensor of >= m contiguous 4-byte integers on `device`."""
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ArgumentError(f"{what} must be a CUDA tensor")
+    if t.dtype not in (torch.int32, torch.uint32):
+        raise ArgumentError(f"{what} must be int32 or uint32, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ArgumentError(f"{what} must be contiguous")
+    if t.numel() < m:
+        raise ArgumentError(f"{what} holds {t.numel()} elements, need {m}")
+    if t.device != device:
+        raise ArgumentError(f"{what} lives on {t.device}, the records on {device}")
+    return C.c_void_p(t.data_ptr())
+
+
+def eval_device(tree, x, labels, geom: Optional[GpuGeom] = None, layout: str = "aos",
+                stream=None, stats=None) -> None:
+    """Enqueue one evaluation of device tensor ``x`` into device tensor
+    ``labels`` (uint32/int32, m elements) on ``stream``.  AoS x is (m, a);
+    SoA x is (a, m); both float32 on the current device.  ``stats`` =
+    (iterations, doubling_steps) tensors for the speculative counters.
+    Asynchronous."""
+    tree = _as_tree(tree)
+    m, a, ld, lay = _device_records(x, layout)
+    lp = _device_u32(labels, m, "labels", x.device)
     g = (geom or GpuGeom()).to_c()
     sp = None
     if stats is not None:
-        sp = st_stats(C.c_void_p(stats[0].data_ptr()), C.c_void_p(stats[1].data_ptr()))
+        sp = st_stats(_device_u32(stats[0], m, "stats[0] (iterations)", x.device),
+                      _device_u32(stats[1], m, "stats[1] (doubling_steps)", x.device))
     L = _lib.load()
     h = tree.handle()
-    _check(L.st_eval_device(h.h, C.c_void_p(x.data_ptr()), m, a, ld, lay, C.byref(g),
-                            C.c_void_p(labels.data_ptr()), C.byref(sp) if sp is not None else None,
-                            _stream_handle(stream)))
+    _check(L.st_eval_device(h.h, C.c_void_p(x.data_ptr()), m, a, ld, lay, C.byref(g), lp,
+                            C.byref(sp) if sp is not None else None, _stream_handle(stream)))
+
+
+def eval_depths_device(tree, x, labels, depths, geom: Optional[GpuGeom] = None, layout: str = "aos",
+                       stream=None) -> None:
+    """Device-resident labels + traversal depths (``st_eval_depths_device``)."""
+    tree = _as_tree(tree)
+    m, a, ld, lay = _device_records(x, layout)
+    lp = _device_u32(labels, m, "labels", x.device)
+    dp = _device_u32(depths, m, "depths", x.device)
+    g = (geom or GpuGeom()).to_c()
+    L = _lib.load()
+    h = tree.handle()
+    _check(L.st_eval_depths_device(h.h, C.c_void_p(x.data_ptr()), m, a, ld, lay, C.byref(g), lp, dp,
+                                   _stream_handle(stream)))
 
 
 def eval_sharded(tree, dataset, devices: Sequence[int], geom: Optional[GpuGeom] = None) -> np.ndarray:
@@ -405,23 +516,27 @@ class Forest:
             pass
 
 
-def eval_forest(forest: Forest, dataset) -> np.ndarray:
+def eval_forest(forest: Forest, dataset, geom: Optional[GpuGeom] = None,
+                out: Optional[np.ndarray] = None) -> np.ndarray:
     dataset = _as_data(dataset)
     if forest.max_attribute >= dataset.arity():
         raise ArgumentError(f"tree reads attribute {forest.max_attribute} but records have arity "
                             f"{dataset.arity()}")
     m = dataset.count()
-    out = np.empty(m, dtype=np.uint32)
+    out = _u32_out(out, m)
+    g = (geom or GpuGeom()).to_c()
     x = dataset.values()
     _check(forest.L.st_forest_eval(forest.h, x.ctypes.data_as(C.c_void_p) if m else None, m,
-                                   dataset.arity(), 0, _lib.ST_LAYOUT_AOS,
+                                   dataset.arity(), 0, _lib.ST_LAYOUT_AOS, C.byref(g),
                                    out.ctypes.data_as(C.c_void_p) if m else None))
     return out
 
 
-def eval_forest_device(forest: Forest, x, labels, stream=None) -> None:
-    m, a = x.shape
-    _check(forest.L.st_forest_eval_device(forest.h, C.c_void_p(x.data_ptr()), m, a,
-                                          x.stride(0) if m > 1 else a,
-                                          _lib.ST_LAYOUT_AOS, C.c_void_p(labels.data_ptr()),
-                                          _stream_handle(stream)))
+def eval_forest_device(forest: Forest, x, labels, geom: Optional[GpuGeom] = None, stream=None) -> None:
+    """Enqueue the forest vote of AoS float32 device tensor ``x`` (m, a) into
+    ``labels`` (m int32/uint32) on ``stream``."""
+    m, a, ld, lay = _device_records(x, "aos")
+    lp = _device_u32(labels, m, "labels", x.device)
+    g = (geom or GpuGeom()).to_c()
+    _check(forest.L.st_forest_eval_device(forest.h, C.c_void_p(x.data_ptr()), m, a, ld, lay, C.byref(g),
+                                          lp, _stream_handle(stream)))

@@ -287,27 +287,32 @@ def test_dag_shaped_input(cuda, co):
         assert np.array_equal(st.eval_gpu(nodes, x, g), want)
 
 
-@pytest.mark.parametrize("no_fold", ["0", "1"])
-def test_forest_variants(cuda, co, no_fold, monkeypatch):
+@pytest.mark.parametrize("no_fold", [False, True])
+def test_forest_variants(cuda, co, no_fold):
     """Shared-memory ring (<= 8 classes, <= 255 trees) and the L1 fallback,
     aligned (TMA) and unaligned / SoA-less record views, trees folded (leaf
-    pairs in terminal nodes) or not, against the oracle vote."""
-    monkeypatch.setenv("ST_FOREST_NO_FOLD", no_fold)
+    pairs in terminal nodes) or not (ST_VAR_NO_FOLD), ring geometries,
+    against the oracle vote."""
+    geoms = [st.GpuGeom(variant=("no_fold",) if no_fold else ()),
+             st.GpuGeom(variant=("no_fold",) if no_fold else (), forest_chains=1, forest_slots=2),
+             st.GpuGeom(variant=("no_fold",) if no_fold else (), forest_chains=4, warps_per_cta=4)]
     x = co.gen_dataset(7001, 12, 9)
     for t_count, classes in ((1, 3), (7, 8), (300, 5), (9, 40)):
         trees = [co.gen_tree(7, 40, 12, classes, 50 + t) for t in range(t_count)]
         want = co.eval_forest(trees, x, classes)
         f = st.Forest(trees, classes)
-        assert np.array_equal(st.eval_forest(f, x), want), (t_count, classes)
+        for g in geoms:
+            assert np.array_equal(st.eval_forest(f, x, g), want), (t_count, classes, g)
         xd = torch.from_numpy(x[1:]).cuda()  # odd base address: no TMA, warp-stored tiles
         out = torch.empty(len(x) - 1, dtype=torch.int32, device="cuda")
-        st.eval_forest_device(f, xd, out)
+        st.eval_forest_device(f, xd, out, geoms[0])
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want[1:]), (t_count, classes)
     for a in (8, 16, 64):  # compile-time arities of the transposed-tile walk
         trees = [co.gen_tree(9, 100, a, 8, 900 + t) for t in range(11)]
         xa = co.gen_dataset(3001, a, 77)
-        assert np.array_equal(st.eval_forest(st.Forest(trees, 8), xa), co.eval_forest(trees, xa, 8)), a
+        for g in geoms:
+            assert np.array_equal(st.eval_forest(st.Forest(trees, 8), xa, g), co.eval_forest(trees, xa, 8)), a
     with pytest.raises(st.ArgumentError):
         st.Forest([co.gen_tree(7, 40, 12, 9, 1)], 4)  # class >= n_classes
 
@@ -372,21 +377,20 @@ def test_reference_acceptance_through_cpp_dropin(cuda):
     p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     print(p.stdout)
     assert p.returncode == 0, p.stdout + p.stderr
-    assert p.stdout.count("PASS") >= 5
+    assert p.stdout.count("PASS") >= 6
 
 
-@pytest.mark.parametrize("fold_min", ["1", "1000000"])
-def test_folded_tree_walks(cuda, co, fold_min, monkeypatch):
+@pytest.mark.parametrize("fold_min", [1, 1000000])
+def test_folded_tree_walks(cuda, co, fold_min):
     """Folded shared trees (leaf pairs inside terminal nodes) for 8/16/32-
     attribute records: all 626 exhaustive shapes (terminal roots, mixed
     pairs, ties on grid records) and 300 synthetic trees, through the
     register walk and the shared-tile walk, against the oracles -- with the
-    fold forced on for every tree size (ST_DATA_FOLD_MIN=1) and off."""
-    monkeypatch.setenv("ST_DATA_FOLD_MIN", fold_min)
-    geoms = [st.GpuGeom(algo="data"), st.GpuGeom(algo="data", record_regs=2),
-             st.GpuGeom(algo="data", record_regs=1, samples_per_thread=1),
-             st.GpuGeom(algo="data", record_regs=3),                          # transposed tiles
-             st.GpuGeom(algo="data", record_regs=3, samples_per_thread=2, stages=1)]
+    fold forced on for every tree size (fold_min = 1) and off."""
+    geoms = [st.GpuGeom(algo="data", fold_min=fold_min), st.GpuGeom(algo="data", record_regs=2, fold_min=fold_min),
+             st.GpuGeom(algo="data", record_regs=1, samples_per_thread=1, fold_min=fold_min),
+             st.GpuGeom(algo="data", record_regs=3, fold_min=fold_min),          # transposed tiles
+             st.GpuGeom(algo="data", record_regs=3, samples_per_thread=2, stages=1, fold_min=fold_min)]
     for leaves in range(1, 9):
         for shape in support.all_shapes(leaves):
             internal = support.assign_labels(shape)
@@ -413,18 +417,17 @@ def test_folded_tree_walks(cuda, co, fold_min, monkeypatch):
 
 
 @pytest.mark.parametrize("mode", ["ballot", "jump", "general"])
-def test_single_window_speculation(cuda, co, mode, monkeypatch):
+def test_single_window_speculation(cuda, co, mode):
     """Trees with <= 32 internal nodes speculate as one window (the paper's
     Proc. 5 geometry): the one-window ring path with the ballot + leaf
-    path-mask reduction (default), with pointer jumping
-    (ST_SPEC_ONEWIN_JUMP=1), and the general window loop
-    (ST_SPEC_NO_ONEWIN=1), against the oracles -- all exhaustive shapes up to
-    8 leaves, and random small trees over row-local, odd and wide arities
-    with ragged record counts."""
-    monkeypatch.setenv("ST_SPEC_NO_ONEWIN", "1" if mode == "general" else "0")
-    monkeypatch.setenv("ST_SPEC_ONEWIN_JUMP", "1" if mode == "jump" else "0")
-    geoms = [st.GpuGeom(algo="speculative"), st.GpuGeom(algo="speculative", group_lanes=32),
-             st.GpuGeom(algo="speculative", group_lanes=16)]
+    path-mask reduction (default), with pointer jumping (ST_VAR_SPEC_JUMP),
+    and the general window loop (ST_VAR_SPEC_GENERAL), against the oracles --
+    all exhaustive shapes up to 8 leaves, and random small trees over
+    row-local, odd and wide arities with ragged record counts."""
+    var = {"ballot": (), "jump": ("spec_jump",), "general": ("spec_general",)}[mode]
+    geoms = [st.GpuGeom(algo="speculative", variant=var),
+             st.GpuGeom(algo="speculative", group_lanes=32, variant=var),
+             st.GpuGeom(algo="speculative", group_lanes=16, variant=var)]
     for leaves in range(1, 9):
         for shape in support.all_shapes(leaves):
             internal = support.assign_labels(shape)
@@ -447,14 +450,14 @@ def test_single_window_speculation(cuda, co, mode, monkeypatch):
             assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, m, g)
 
 
-@pytest.mark.parametrize("wide", ["0", "1"])
-def test_spec_window_formats(cuda, co, wide, monkeypatch):
+@pytest.mark.parametrize("wide", [False, True])
+def test_spec_window_formats(cuda, co, wide):
     """The ring kernel's 8-byte window entries (default when the tree's
-    fields fit) and the 16-byte format (ST_SPEC_WIDE_WIN=1): random trees
+    fields fit) and the 16-byte format (ST_VAR_SPEC_WIDE): random trees
     with many windows, group widths 2..16, one and two record streams,
     row-local and other arities, ragged counts, large leaf payloads
     (class ids >= 2^31 -> ordinals), against the oracle."""
-    monkeypatch.setenv("ST_SPEC_WIDE_WIN", wide)
+    var = ("spec_wide",) if wide else ()
     for seed in range(1, 161):
         a = (8, 16, 32, 19, 64, 3, 128, 300)[seed % 8]
         depth = 4 + seed % 17
@@ -466,20 +469,20 @@ def test_spec_window_formats(cuda, co, wide, monkeypatch):
         m = (1, 33, 1000, 4097, 20011)[seed % 5]
         x = co.gen_dataset(m, a, seed + 4000, gaussian=(seed % 2 == 0))
         want = co.eval_serial(nodes, x)
-        for g in (st.GpuGeom(algo="speculative"),
+        for g in (st.GpuGeom(algo="speculative", variant=var),
                   st.GpuGeom(algo="speculative", group_lanes=(2, 4, 8, 16)[seed % 4],
-                             samples_per_thread=1 + seed % 2)):
+                             samples_per_thread=1 + seed % 2, variant=var)):
             assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, m, g)
 
 
-@pytest.mark.parametrize("pdl", ["0", "1", "2"])
-def test_programmatic_dependent_launch_ordering(cuda, co, pdl, monkeypatch):
+@pytest.mark.parametrize("pdl", [0, 1, 2, 3])
+def test_programmatic_dependent_launch_ordering(cuda, co, pdl):
     """Data launches are programmatic dependents of the previous kernel in
     the stream: records written by that kernel (an elementwise torch kernel
     here, no host sync in between) must be read only after it completed, and
     labels must not be overwritten early.  Small inputs with room for a
-    dependent CTA (early trigger), large ones (trigger at exit), forced off."""
-    monkeypatch.setenv("ST_PDL", pdl)
+    dependent CTA (early trigger), large ones (trigger at exit), forced off
+    (st_geom.pdl 0 auto, 1 early, 2 at exit, 3 off)."""
     for depth, leaves, a, m in ((10, 1024, 16, 300_000), (12, 2048, 8, 200_000), (24, 256, 32, 2_000_000)):
         nodes = co.gen_tree(depth, leaves, a, 8, 900 + depth)
         tree = st.EncodedTree(nodes)
@@ -489,22 +492,23 @@ def test_programmatic_dependent_launch_ordering(cuda, co, pdl, monkeypatch):
         outs = [torch.empty(m, dtype=torch.int32, device=cuda) for _ in srcs]
         for s, o in zip(srcs, outs):
             torch.add(s, 0.0, out=xd)  # producer kernel immediately before the launch
-            st.eval_device(tree, xd, o, st.GpuGeom(algo="data"))
+            st.eval_device(tree, xd, o, st.GpuGeom(algo="data", pdl=pdl))
         torch.cuda.synchronize()
         for o, want in zip(outs, wants):
             assert np.array_equal(o.cpu().numpy().view(np.uint32), want), (depth, pdl)
 
 
-@pytest.mark.parametrize("bulk", ["0", "1"])
-def test_tree_staging_paths(cuda, co, bulk, monkeypatch):
+@pytest.mark.parametrize("bulk", [False, True])
+def test_tree_staging_paths(cuda, co, bulk):
     """Shared trees / window tables staged by one cp.async.bulk (default) or
-    by the per-thread copy loop (ST_TREE_BULK=0): identical labels for the
+    by the per-thread copy loop (ST_VAR_TREE_LOOP): identical labels for the
     record-major, attribute-major and register walks, folded and plain trees,
     and the speculative ring (8- and 16-byte window tables, one window)."""
-    monkeypatch.setenv("ST_TREE_BULK", bulk)
-    geoms = [st.GpuGeom(algo="data"), st.GpuGeom(algo="data", record_regs=1),
-             st.GpuGeom(algo="data", record_regs=3), st.GpuGeom(algo="data", record_regs=2),
-             st.GpuGeom(algo="speculative"), st.GpuGeom(algo="speculative", samples_per_thread=1)]
+    v = () if bulk else ("tree_loop",)
+    geoms = [st.GpuGeom(algo="data", variant=v), st.GpuGeom(algo="data", record_regs=1, variant=v),
+             st.GpuGeom(algo="data", record_regs=3, variant=v), st.GpuGeom(algo="data", record_regs=2, variant=v),
+             st.GpuGeom(algo="speculative", variant=v),
+             st.GpuGeom(algo="speculative", samples_per_thread=1, variant=v)]
     for depth, leaves, a, seed in ((10, 1024, 16, 31), (12, 2048, 8, 32), (24, 256, 32, 33), (11, 16, 19, 1)):
         nodes = co.gen_tree(depth, leaves, a, 8, seed)
         x = co.gen_dataset(50_001, a, seed + 100)
@@ -514,13 +518,12 @@ def test_tree_staging_paths(cuda, co, bulk, monkeypatch):
             assert np.array_equal(_dev_eval(nodes, xd, g, len(x)), want), (depth, a, g, bulk)
 
 
-@pytest.mark.parametrize("tile", ["1", "2"])
-def test_spec_ring_slot_sizes(cuda, co, tile, monkeypatch):
-    """Speculative ring slots of 32 or 64 records (ST_SPEC_TILE) for the
-    two-stream 8-byte-window loop: skewed and complete trees, 8/16/32
+@pytest.mark.parametrize("tile", [1, 2])
+def test_spec_ring_slot_sizes(cuda, co, tile):
+    """Speculative ring slots of 32 or 64 records (st_geom.slot_records) for
+    the two-stream 8-byte-window loop: skewed and complete trees, 8/16/32
     attributes, ragged record counts (partial last slot, fewer records than
     one slot), single-leaf tree."""
-    monkeypatch.setenv("ST_SPEC_TILE", tile)
     cases = ((24, 256, 32, 41), (16, 4096, 16, 42), (12, 2048, 8, 43), (0, 1, 16, 44))
     for depth, leaves, a, seed in cases:
         nodes = co.gen_tree(depth, leaves, a, 8, seed)
@@ -528,5 +531,6 @@ def test_spec_ring_slot_sizes(cuda, co, tile, monkeypatch):
             x = co.gen_dataset(m, a, seed + m)
             want = co.eval_serial(nodes, x)
             xd = torch.from_numpy(x).to(cuda)
-            for g in (st.GpuGeom(algo="speculative"), st.GpuGeom(algo="speculative", group_lanes=8)):
+            for g in (st.GpuGeom(algo="speculative", slot_records=tile),
+                      st.GpuGeom(algo="speculative", group_lanes=8, slot_records=tile)):
                 assert np.array_equal(_dev_eval(nodes, xd, g, m), want), (depth, a, m, g, tile)

@@ -111,7 +111,7 @@ def test_cli_verify_bench_classify(cuda, co, cli, tmp_path):
 
 
 @pytest.mark.parametrize("slots", [1, 3, 7])
-def test_spec_ring_shallow_ring_stress(cuda, co, slots, monkeypatch):
+def test_spec_ring_shallow_ring_stress(cuda, co, slots):
     """k_spec_ring with a ring shallower than the warp count: tickets run up to
     several generations ahead of a slow warp on a deep record (skewed depth-24
     tree), which a parity-only slot wait would mistake for a completed refill.
@@ -122,10 +122,10 @@ def test_spec_ring_shallow_ring_stress(cuda, co, slots, monkeypatch):
     x = co.gen_dataset(400_000, 32, 202)
     want = co.eval_serial(nodes, x)
     xd = torch.from_numpy(x).cuda()
-    monkeypatch.setenv("ST_SPEC_RING_SLOTS", str(slots))
     for sr in (1, 2, 1):
         out = torch.empty(len(x), dtype=torch.int32, device="cuda")
-        st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative", pipeline=2, samples_per_thread=sr))
+        st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative", pipeline=2, samples_per_thread=sr,
+                                                  ring_slots=slots))
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint32), want)
 

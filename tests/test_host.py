@@ -49,7 +49,7 @@ def test_library_is_sm100a():
 def test_abi_struct_sizes():
     import ctypes as C
 
-    assert C.sizeof(_lib.st_geom) == 48
+    assert C.sizeof(_lib.st_geom) == 96
     assert st.NODE_DTYPE.itemsize == 16
     assert [st.NODE_DTYPE.fields[f][1] for f in ("attribute", "threshold", "child", "class_id")] == [0, 4, 8, 12]
 

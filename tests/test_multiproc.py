@@ -62,3 +62,48 @@ def test_gloo_label_gather(world, m):
     for rank, buf, tmax in res:
         assert np.array_equal(np.frombuffer(buf, dtype=np.int32), want)
         assert tmax == float(world)
+
+
+def test_bench_self_spawn_two_ranks():
+    """`bench.py --gpus 2` without torchrun re-launches itself as two ranks
+    under torch.distributed.run (127.0.0.1 rendezvous): exercised here on CPU
+    through the reference arm, which rank 0 alone runs and prints -- exactly
+    one JSON line with n_gpus 2, every rank exits 0."""
+    import json
+    import subprocess
+    import sys
+
+    import oracle
+
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--workload", "C1",
+                        "--steps", "1", "--warmup", "3", "--ref-sample", "20000"],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_bench_rank_parity_hashes_cover_eight_ranks():
+    """bench.py checks every rank's labels against the reference hash of its
+    own batch: the committed golden file holds C2 / C4 hashes for ranks 0-7
+    and all 64 C5 shards at every depth (rank 0 / shard 0 = Appendix A)."""
+    import bench
+
+    g = bench.golden()
+    assert len(g["c2_ranks"]["labels_fnv"]) == 8 and len(g["c4_ranks"]["vote_fnv"]) == 8
+    assert bench.golden_labels(bench.WORKLOADS["C2"], 0) == 0x9e7e87e9cc15c4e0
+    assert int(g["c4_ranks"]["vote_fnv"][0], 16) == 0x1b2543c41e436ce0
+    assert sorted(int(d) for d in g["c5"]["depths"]) == [8, 10, 12, 14, 16, 18, 20]
+    for d, want in ((8, 0xa41b18f5886a3516), (12, 0x8a36c71851f61114), (16, 0x4bbe70e47d70a501),
+                    (20, 0x894ffd1cd01ac0a5)):
+        row = g["c5"]["depths"][str(d)]
+        assert len(row["labels_fnv"]) == 64 and int(row["labels_fnv"][0], 16) == want
+        assert bench.golden_labels(bench.WORKLOADS[f"C5d{d}"], 0) == want
+    # Appendix A d_mu of shard 0
+    assert abs(g["c5"]["depths"]["16"]["depth_sum"][0] / 15_625_000 - 7.7637) < 5e-5
+    assert abs(g["c5"]["depths"]["20"]["depth_sum"][0] / 15_625_000 - 7.3201) < 5e-5

@@ -1,6 +1,11 @@
-"""A/B data-kernel geometries on canonical workloads (development aid):
-    python tools/ab_geoms.py W1,W2 'dict(record_regs=3, samples_per_thread=2, stages=1)' ... [--flush] [--tile=N]
-Alternates the geometries for 5 rounds on one box; prints per-geometry ms."""
+"""A/B kernel geometries / variants on canonical workloads (development aid):
+    python tools/ab_geoms.py W1,W2 'dict(record_regs=3, samples_per_thread=2, stages=1)' ... \
+        [--algo=data|speculative] [--flush] [--tile=N]
+    e.g. ... C2 'dict(variant=("spec_wide",))' 'dict(slot_records=1)' --algo=speculative
+W may be PAPER: the paper's tree(11,16,19,7,1) on 256 copies of its
+data(16384,19,2) (16.8M records).  Every st_geom field (including the
+ST_VAR_* variants) is reachable per call.  Alternates the geometries for 5
+rounds on one box; prints per-geometry us."""
 import os
 import sys
 
@@ -15,16 +20,23 @@ import workloads  # noqa: E402
 
 flush = "--flush" in sys.argv
 tile = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--tile=")), 1))
-args = [a for a in sys.argv[1:] if a != "--flush" and not a.startswith("--tile=")]
+algo = next((a.split("=")[1] for a in sys.argv if a.startswith("--algo=")), "data")
+args = [a for a in sys.argv[1:] if a != "--flush" and not a.startswith("--tile=") and not a.startswith("--algo=")]
 names, specs = args[0].split(","), ["dict()"] + args[1:]
 fl = workloads.make_flush() if flush else None
 for name in names:
-    w = bench.WORKLOADS[name]
-    tree = st.generate_synthetic_tree(*w["tree"])
-    x = st.generate_synthetic_dataset(w["m"], w["a"], w["seed"])
+    if name == "PAPER":
+        import numpy as np
+        tree = st.generate_synthetic_tree(11, 16, 19, 7, 1)
+        x = np.tile(st.generate_synthetic_dataset(16384, 19, 2), (256, 1))
+        w = {"m": len(x), "labels_fnv": st.fnv1a64(st.eval_gpu(tree, x, st.GpuGeom(algo="data")))}
+    else:
+        w = bench.WORKLOADS[name]
+        tree = st.generate_synthetic_tree(*w["tree"])
+        x = st.generate_synthetic_dataset(w["m"], w["a"], w["seed"])
     xd = torch.from_numpy(x).cuda().repeat(tile, 1)
     out = torch.empty(len(xd), dtype=torch.int32, device="cuda")
-    geoms = [st.GpuGeom(algo="data", **eval(s)) for s in specs]
+    geoms = [st.GpuGeom(algo=algo, **eval(s)) for s in specs]
     res = {s: [] for s in specs}
     for g, s in zip(geoms, specs):
         st.eval_device(tree, xd, out, g)

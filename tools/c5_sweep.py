@@ -8,8 +8,10 @@ SURVEY §8d/§8e) at full size.
     GPU over its contiguous shard block, all GPUs launched together, time =
     max over GPUs of the CUDA-event time (median of --reps).  No collective:
     the only exchange is the label gather, timed separately (D2H of every
-    GPU's labels into one pinned host buffer).  Parity: shard 0's labels
-    against the reference hashes of SURVEY Appendix A (D = 8, 12, 16, 20).
+    GPU's labels into one pinned host buffer).  Parity: every shard's
+    labels at every depth, both algorithms, against the reference hashes in
+    tests/golden/shard_hashes.json (generated from oracle/_ref by
+    tests/golden/make_shard_golden.py; shard 0 = SURVEY Appendix A).
 
 Records are generated on the host with the reference generator (one thread
 per shard, st_synthetic_dataset releases the GIL) straight into pinned
@@ -37,8 +39,7 @@ import paper_1111_1373_b200 as st  # noqa: E402
 
 SHARD = 15_625_000
 A = 16
-SHARD0_FNV = {8: 0xa41b18f5886a3516, 12: 0x8a36c71851f61114, 16: 0x4bbe70e47d70a501,
-              20: 0x894ffd1cd01ac0a5}
+GOLD = bench.golden().get("c5", {}).get("depths", {})
 
 
 def main():
@@ -113,14 +114,23 @@ def main():
                 return max(a.elapsed_time(b) for a, b in evs) / 1e3
 
             launch_all()  # warm (device tree / window tables)
+            # every shard against the reference hash of that shard and depth
+            want = GOLD.get(str(D), {}).get("labels_fnv", [])
+            parts = []
+            for g, (lo, hi) in enumerate(own):
+                host = labs[g].cpu().numpy()
+                parts += [(s, host[(s - lo) * SHARD:(s - lo + 1) * SHARD]) for s in range(lo, hi)]
+            with cf.ThreadPoolExecutor(max_workers=16) as pool:
+                hashes = list(pool.map(lambda p: st.fnv1a64(p[1]), parts))
+            ok = [h == int(want[s], 16) if s < len(want) else None for (s, _), h in zip(parts, hashes)]
+            del parts
             ts = [launch_all() for _ in range(args.reps)]
             t = statistics.median(ts)
-            ok = None
-            if D in SHARD0_FNV:
-                ok = st.fnv1a64(labs[0][:SHARD].cpu().numpy()) == SHARD0_FNV[D]
             gbs = S * SHARD * A * 4 / t / 1e9
             row[algo] = {"s": t, "samples_per_s": S * SHARD / t, "GBs": gbs,
-                         "frac_of_G_x_peak": gbs / (G * peak), "shard0_labels_match_reference": ok}
+                         "frac_of_G_x_peak": gbs / (G * peak),
+                         "shards_match_reference": f"{sum(v is True for v in ok)}/{len(ok)}",
+                         "all_shards_match_reference": all(v is True for v in ok)}
         # label gather: every GPU's labels into one pinned host buffer
         g0 = time.perf_counter()
         off = 0

@@ -1,6 +1,6 @@
 """C4 forest geometry sweep (development aid): U trees per lane step, tree-ring
-depth NT, CTA width W via the ST_FOREST_* knobs; CUDA-event timing, vote hash
-checked against Appendix A.
+depth NT, CTA width W via st_geom (forest_chains, forest_slots,
+warps_per_cta); CUDA-event timing, vote hash checked against Appendix A.
 
     python tools/forest_sweep.py [records]
 """
@@ -27,11 +27,10 @@ if len(sys.argv) > 2 and sys.argv[2] == "deep":  # deeper rings at fewer consume
 if len(sys.argv) > 2 and sys.argv[2] == "fine":  # around the folded-tree optimum
     grid = [(0, 0, 0)] + [(u, nt, w) for u in (2, 3, 4) for nt in range(u + 2, u + 5) for w in (0, 24, 20, 16)]
 for u, nt, w in grid:
-    env = {"ST_FOREST_U": u, "ST_FOREST_NT": nt, "ST_FOREST_W": w}
-    for k, v in env.items():
-        os.environ[k] = str(v)
+    env = {"forest_chains": u, "forest_slots": nt, "warps_per_cta": w}
+    geom = st.GpuGeom(**env)
     try:
-        st.eval_forest_device(f, x, lab)
+        st.eval_forest_device(f, x, lab, geom)
         torch.cuda.synchronize()
     except Exception as e:  # geometry does not fit
         print("skip", env, e, flush=True)
@@ -40,7 +39,7 @@ for u, nt, w in grid:
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(3):
-        st.eval_forest_device(f, x, lab)
+        st.eval_forest_device(f, x, lab, geom)
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / 3

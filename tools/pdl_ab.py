@@ -1,6 +1,6 @@
 """Back-to-back launches on distinct record buffers (a frame stream larger
 than L2), captured in one CUDA graph, with and without programmatic dependent
-launch (ST_PDL): per-launch device time (development aid).
+launch (st_geom.pdl): per-launch device time (development aid).
     python tools/pdl_ab.py [W ...] [--frames=16] [--algo=data]"""
 import os
 import sys
@@ -21,13 +21,9 @@ for name in names:
     x = torch.from_numpy(st.generate_synthetic_dataset(w["m"], w["a"], w["seed"])).cuda()
     xs = [x.clone() for _ in range(frames)]
     outs = [torch.empty(w["m"], dtype=torch.int32, device="cuda") for _ in range(frames)]
-    g = st.GpuGeom(algo=algo)
     res = {}
-    for pdl in ("0", "1", "2", "auto", "0", "1", "2", "auto"):
-        if pdl == "auto":
-            os.environ.pop("ST_PDL", None)
-        else:
-            os.environ["ST_PDL"] = pdl
+    for pdl in ("off", "1", "2", "auto", "off", "1", "2", "auto"):
+        g = st.GpuGeom(algo=algo, pdl={"off": 3, "1": 1, "2": 2, "auto": 0}[pdl])
         s = torch.cuda.Stream()
         with torch.cuda.stream(s):
             for xi, oi in zip(xs, outs):
@@ -52,6 +48,5 @@ for name in names:
             b.record()
             torch.cuda.synchronize()
             best = min(best, a.elapsed_time(b) * 1e3 / frames)
-        res.setdefault(f"ST_PDL={pdl}", []).append(round(best, 2))
+        res.setdefault(f"pdl={pdl}", []).append(round(best, 2))
     print(name, algo, f"{frames} launches on distinct buffers, us per launch (best of 5 replays):", res, flush=True)
-os.environ.pop("ST_PDL", None)

@@ -42,11 +42,9 @@ for targs, a in cases:
             bad += 1
             print("MISMATCH", targs, g)
     # one-window trees: the pointer-jumping variant of the one-window path too
-    os.environ["ST_SPEC_ONEWIN_JUMP"] = "1"
     out = torch.empty(len(x), dtype=torch.int32, device="cuda")
-    st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative"))
+    st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative", variant=("spec_jump",)))
     torch.cuda.synchronize()
-    del os.environ["ST_SPEC_ONEWIN_JUMP"]
     if not np.array_equal(out.cpu().numpy().view(np.uint32), want):
         bad += 1
         print("MISMATCH one-window jump", targs)

@@ -63,8 +63,7 @@ def run():
 
     # The reference model walks node by node; a folded tree (leaf pairs inside
     # terminal nodes) skips the last level's node load by
-    # construction, so the cross-check runs the unfolded walk.
-    os.environ["ST_DATA_NO_FOLD"] = "1"
+    # construction, so the cross-check runs the unfolded walk (ST_VAR_NO_FOLD).
     import paper_1111_1373_b200 as st
 
     order = []
@@ -72,7 +71,8 @@ def run():
         nodes, x = inputs(name, st.generate_synthetic_tree, st.generate_synthetic_dataset)
         xd = torch.from_numpy(x).cuda()
         out = torch.empty(len(x), dtype=torch.int32, device="cuda")
-        st.eval_device(nodes, xd, out, st.GpuGeom(algo="data", samples_per_thread=1, tree_loc="shared"))
+        st.eval_device(nodes, xd, out, st.GpuGeom(algo="data", samples_per_thread=1, tree_loc="shared",
+                                                  variant=("no_fold",)))
         order.append(("data", name, 0))
     nodes, x = inputs("paper", st.generate_synthetic_tree, st.generate_synthetic_dataset)
     xd = torch.from_numpy(x).cuda()
