@@ -109,7 +109,11 @@ enum st_variant {
   ST_VAR_SPEC_GENERAL = 4u, /* speculative, one-window trees: the general window loop */
   ST_VAR_SPEC_JUMP = 8u,    /* speculative, one-window trees: shfl pointer jumping instead of
                                the ballot + leaf path-mask reduction */
-  ST_VAR_SPEC_WIDE = 16u    /* speculative: 16-byte window entries instead of 8-byte ones */
+  ST_VAR_SPEC_WIDE = 16u,   /* speculative: 16-byte window entries instead of 8-byte ones */
+  ST_VAR_SPEC_SELECT = 32u, /* speculative: a select per pointer-jumping step (round-1 codes) instead
+                               of self-loop terminal codes */
+  ST_VAR_SPEC_PRED = 64u,   /* speculative, self-loop two-stream loop: predicated stream advance */
+  ST_VAR_SPEC_BRANCH = 128u /* ... the stream advance in a divergent branch (default: by tree shape) */
 };
 
 /* Optional per-record speculative counters (SpeculativeStats,

@@ -60,6 +60,9 @@ ST_VAR_TREE_LOOP = 2
 ST_VAR_SPEC_GENERAL = 4
 ST_VAR_SPEC_JUMP = 8
 ST_VAR_SPEC_WIDE = 16
+ST_VAR_SPEC_SELECT = 32
+ST_VAR_SPEC_PRED = 64
+ST_VAR_SPEC_BRANCH = 128
 
 
 class st_stats(C.Structure):

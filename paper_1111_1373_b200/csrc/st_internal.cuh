@@ -140,6 +140,21 @@ struct WinTable {
   // (cw_units of them; 0 = none): entry (w, j) at 8 * (G * w + j) bytes,
   // word = attr4 | left << cw_abits | right << (cw_abits + cw_cbits).
   uint32_t cw_off = 0, cw_units = 0, cw_abits = 0, cw_cbits = 0;
+  // Self-loop 8-byte windows (k_spec_ring SL), appended at sl_off (sl_units
+  // SEntry units; 0 = none): entry (w, j) at 8 * (G * w + j), word = attr4 |
+  // left << sl_abits | right << (sl_abits + sl_cbits).  A code is a lane
+  // target t < G, or payload << log2(G) | j for a terminal -- payload = the
+  // next window (>= 1; nothing exits to the root window) or sl_nw + leaf
+  // code -- so a terminal's low bits name its own lane and a width-G shfl
+  // pointer-jumping step returns it unchanged (no select per step), and
+  // (payload << log2 G) * 8 is the next window's byte offset.  Windows
+  // sl_nw.. hold copies of window 0: after a leaf the stream restarts at the
+  // root without a select.
+  uint32_t sl_off = 0, sl_units = 0, sl_abits = 0, sl_cbits = 0, sl_nw = 0;
+  // One-window trees: entries[sl1_off + j] = {thr, 4*attr, left, right} with
+  // self-loop leaf codes kLeafBit | leaf code << 5 | j (0 = none).
+  uint32_t sl1_off = 0;
+  uint32_t base_units = 0;  // entries of the 16-byte table incl. path masks (cw / sl tables follow)
 };
 
 }  // namespace sti
@@ -206,6 +221,7 @@ struct st_tree {
     if (is_leaf(0)) {
       wt.root_code = kLeafBit | leaf_code[0];
       wt.entries.assign(32, SEntry{0.0f, 0u, 0u, 0u});
+      wt.base_units = 32;
       return wt;
     }
     std::vector<int32_t> win_of_root(n, -1);
@@ -309,10 +325,37 @@ struct st_tree {
               tb, (4u * nd.attribute) | (ccode(nd.child) << abits) | (ccode(nd.child + 1) << (abits + cbits)));
         }
       }
+      // unused lanes of the window read the window root's attribute (code 0:
+      // they point at lane 0, never on a path): the same shared-memory word
+      // as lane 0 -- a broadcast, not an extra bank conflict
+      if (cw)
+        for (uint32_t j = (uint32_t)mem.size(); j < G; ++j)
+          cwt[(size_t)w * G + j] = make_uint2(0u, 4u * nodes[mem[0]].attribute);
       for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = -1;
     }
     wt.root_code = kExitBit | 0u;
     wt.windows = nw;
+    if (nw == 1) {
+      add_path_masks(wt, members[0], G);
+      // one-window self-loop entries: leaf codes kLeafBit | code << 5 | j
+      if (max_code < (1u << 26)) {
+        const auto& mem = members[0];
+        std::vector<SEntry> s1(32, SEntry{0.0f, 0u, 0u, 0u});
+        for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = (int32_t)j;
+        for (uint32_t j = 0; j < mem.size(); ++j) {
+          auto code = [&](uint32_t c) -> uint32_t {
+            if (is_leaf(c)) return kLeafBit | (leaf_code[c] << 5) | j;
+            return (uint32_t)lane_of[c];
+          };
+          const st_node& nd = nodes[mem[j]];
+          s1[j] = SEntry{nd.threshold, 4u * nd.attribute, code(nd.child), code(nd.child + 1)};
+        }
+        wt.sl1_off = (uint32_t)wt.entries.size();
+        wt.entries.insert(wt.entries.end(), s1.begin(), s1.end());
+      }
+    }
+    // the 16-byte-entry kernels stage [0, base_units): windows, path masks
+    wt.base_units = (uint32_t)wt.entries.size();
     if (cw) {
       if (cwt.size() & 1) cwt.push_back(make_uint2(0u, 0u));
       wt.cw_off = (uint32_t)wt.entries.size();
@@ -323,7 +366,47 @@ struct st_tree {
       wt.entries.resize(base_units + wt.cw_units, SEntry{0.0f, 0u, 0u, 0u});
       std::memcpy(wt.entries.data() + base_units, cwt.data(), cwt.size() * sizeof(uint2));
     }
-    if (nw == 1) add_path_masks(wt, members[0], G);
+    // self-loop 8-byte windows (see WinTable): codes of cbits2 bits
+    {
+      uint32_t lg = 0;
+      while ((1u << lg) < G) ++lg;
+      const uint64_t ncodes = (uint64_t)max_code + 1;  // leaf payloads sl_nw + code
+      const uint64_t units = (uint64_t)nw + ncodes;      // windows + root copies
+      uint32_t cbits2 = 1;
+      while (cbits2 < 40 && ((units * G - 1) >> cbits2) != 0) ++cbits2;
+      if (G <= 32 && (1u << lg) == G && ncodes <= 64 && abits + 2 * cbits2 <= 32 && units * G < (1u << 24)) {
+        std::vector<uint2> slt((size_t)units * G + 64, make_uint2(0u, 0u));
+        for (uint32_t w = 0; w < nw; ++w) {
+          const auto& mem = members[w];
+          for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = (int32_t)j;
+          for (uint32_t j = 0; j < mem.size(); ++j) {
+            auto scode = [&](uint32_t c) -> uint32_t {
+              if (is_leaf(c)) return ((nw + leaf_code[c]) << lg) | j;
+              if (lane_of[c] >= 0) return (uint32_t)lane_of[c];
+              return ((uint32_t)win_of_root[c] << lg) | j;
+            };
+            const st_node& nd = nodes[mem[j]];
+            uint32_t tb;
+            std::memcpy(&tb, &nd.threshold, 4);
+            slt[(size_t)w * G + j] = make_uint2(
+                tb, (4u * nd.attribute) | (scode(nd.child) << abits) | (scode(nd.child + 1) << (abits + cbits2)));
+          }
+          for (uint32_t j = (uint32_t)mem.size(); j < G; ++j)  // unused lanes: the root's word (broadcast)
+            slt[(size_t)w * G + j] = make_uint2(0u, 4u * nodes[mem[0]].attribute);
+          for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = -1;
+        }
+        for (uint64_t w = nw; w < units; ++w)  // root copies (leaf payloads)
+          std::copy(slt.begin(), slt.begin() + G, slt.begin() + (size_t)w * G);
+        if (slt.size() & 1) slt.push_back(make_uint2(0u, 0u));
+        wt.sl_off = (uint32_t)wt.entries.size();
+        wt.sl_units = (uint32_t)(slt.size() / 2);
+        wt.sl_abits = abits;
+        wt.sl_cbits = cbits2;
+        wt.sl_nw = nw;
+        wt.entries.resize(wt.entries.size() + wt.sl_units, SEntry{0.0f, 0u, 0u, 0u});
+        std::memcpy(wt.entries.data() + wt.sl_off, slt.data(), slt.size() * sizeof(uint2));
+      }
+    }
     return wt;
   }
 

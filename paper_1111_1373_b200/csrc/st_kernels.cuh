@@ -815,6 +815,13 @@ struct SpecArgs {
   // reads them straight from the constant bank: attr4 mask, left / right
   // code shifts, code mask, leaf bit, exit payload mask, window stride (8 G)
   uint32_t cw_amask, cw_lsh, cw_rsh, cw_cmask, cw_leaf, cw_emask, cw_wstride;
+  // k_spec_ring SL (self-loop codes): terminal-code mask (code bits above
+  // log2 G), first leaf code, a stream's advance to its next record (bytes
+  // added to / XOR applied to its swizzled record address)
+  uint32_t sl_xmask, sl_leafmin, sl_adv, sl_xor;
+  // ring label rows hold raw terminal codes: class = ((code & lab_mask) >>
+  // lab_shift) - lab_sub (then the leaf-class table, if any)
+  uint32_t lab_mask, lab_shift, lab_sub;
 };
 
 // Window codes: lane index (< 32; a width-G shuffle uses its low log2(G)
@@ -997,10 +1004,18 @@ struct SpecRingArgs {
 // RT: records per ring slot / 32.  Two-stream groups over 64-record slots
 // (RT = 2) walk 4 records per stream instead of 2, which evens out the
 // streams' window counts on skewed trees and halves the per-slot overhead.
-template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false, int RT = 1>
+// SL: self-loop terminal codes (WinTable::sl_*): a pointer-jumping step is
+// one shfl with no select.  With SR == 2: SL == 1 advances a resolved
+// stream by a constant address step under predication (skewed trees, where
+// some stream of the warp resolves in almost every window step), SL == 2 in
+// a divergent branch taken only when one does (complete trees, whose
+// streams resolve in lockstep every depth / h steps).
+template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false, int RT = 1, int SL = 0>
 __global__ void __launch_bounds__(kMaxThreads)
     k_spec_ring(const SpecRingArgs ra, const __grid_constant__ CUtensorMap tmap) {
   static_assert(!CW || (WIN_SHARED && SR >= 1), "8-byte windows: shared table, window-loop paths");
+  static_assert(!SL || SR == 0 || (SR == 2 && CW), "self-loop codes: one window, or two 8-byte-window streams");
+  static_assert(SL != 2 || SR == 2, "branchy stream advance: two-stream loop");
   static_assert(RT == 1 || SR == 2, "multi-chunk slots: two-stream loop only");
   extern __shared__ __align__(1024) unsigned char smem[];
   const SpecArgs& args = ra.s;
@@ -1124,8 +1139,9 @@ __global__ void __launch_bounds__(kMaxThreads)
   uint4 e1 = make_uint4(0u, 0u, 0u, 0u), pm1 = make_uint4(0u, 0u, 0u, 0u);
   if constexpr (SR == 0) {
     static_assert(SR != 0 || WIN_SHARED, "one-window path stages its table in shared memory");
-    e1 = lds_u4(jaddr);
-    if (args.pm_off) pm1 = lds_u4(sbase + 16u * (args.pm_off + j));
+    // SL: the self-loop copy of the window (host offset in pm_off)
+    e1 = SL ? lds_u4(sbase + 16u * (args.pm_off + j)) : lds_u4(jaddr);
+    if (args.pm_off && !SL) pm1 = lds_u4(sbase + 16u * (args.pm_off + j));
   }
 
   while (true) {
@@ -1179,7 +1195,38 @@ __global__ void __launch_bounds__(kMaxThreads)
           return rec.get(attr4);
         }
       };
-      if (args.pm_off) {
+      if constexpr (SL) {
+        // Pointer jumping with self-loop leaf codes: a leaf code's low bits
+        // name its own lane, so each doubling is one shfl with no select
+        // (snapshot semantics of path_double_step, eval_speculative.cpp:
+        // 38-51); group lane 0 then holds the leaf.  Full tiles advance the
+        // feature / label addresses by constants (no row clamp).
+        if (rows == 32u * RT) {
+          const uint32_t a4 = 4u * (A > 0 ? (uint32_t)A : args.p.a);
+          const uint32_t df = NG * a4, dl = 4u * NG;
+          uint32_t f = tile + g * a4 + attr4, la = lbuf + 4u * g;
+#pragma unroll 4
+          for (uint32_t r = g; r < 32u * RT; r += NG, f += df, la += dl) {
+            const float v = lds_f32(f ^ ((f >> 3) & 0x70u));  // swizzled (tile 1024-aligned)
+            uint32_t c = (v > __uint_as_float(thr)) ? e1.w : e1.z;
+#pragma unroll
+            for (int st = 0; st < (STEPS > 0 ? STEPS : 0); ++st) c = __shfl_sync(0xffffffffu, c, c, G);
+            const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
+            if (j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(la), "r"(root) : "memory");
+          }
+        } else {
+#pragma unroll 4
+          for (uint32_t r = g; r < 32u * RT; r += NG) {
+            const float v = feature(r);
+            uint32_t c = (v > __uint_as_float(thr)) ? e1.w : e1.z;
+#pragma unroll
+            for (int st = 0; st < (STEPS > 0 ? STEPS : 0); ++st) c = __shfl_sync(0xffffffffu, c, c, G);
+            const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
+            if (j == 0 && r < rows)
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(root) : "memory");
+          }
+        }
+      } else if (args.pm_off) {
         // Ballot reduction: one vote gathers every lane's predicate (the
         // same speculation), and the lane whose leaf path mask matches --
         // exactly one per group in a tree -- stores its class.  No shuffles.
@@ -1285,6 +1332,131 @@ __global__ void __launch_bounds__(kMaxThreads)
           woff = exit_off(root);
         }
       } while (__any_sync(0xffffffffu, active));
+    } else if constexpr (SR == 2 && SL == 2) {
+      // Two record streams, self-loop codes, the stream advance in a
+      // divergent branch (taken by the warp only in steps where some stream
+      // resolves).
+      static_assert(Rec<A, kTma>::kRowLocal, "self-loop streams: records inside one 128-byte row");
+      const uint32_t a4 = 4u * (uint32_t)A;
+      auto base_of = [&](uint32_t rr) {
+        const uint32_t ra4 = rr * a4, rowb = ra4 & ~127u;
+        return (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
+      };
+      uint32_t rA = g, rB = g + NG;
+      bool aA = rA < rows, aB = rB < rows;
+      uint32_t wA = 0, wB = 0;
+      uint32_t bA = base_of(aA ? rA : 0u), bB = base_of(aB ? rB : 0u);
+      do {
+        const uint2 eA = lds_u2(jaddr + wA), eB = lds_u2(jaddr + wB);
+        const float vA = lds_f32((eA.y & args.cw_amask) ^ bA), vB = lds_f32((eB.y & args.cw_amask) ^ bB);
+        uint32_t cA = eA.y >> (vA > __uint_as_float(eA.x) ? args.cw_rsh : args.cw_lsh);
+        uint32_t cB = eB.y >> (vB > __uint_as_float(eB.x) ? args.cw_rsh : args.cw_lsh);
+        if constexpr (STEPS >= 0) {
+#pragma unroll
+          for (int st = 0; st < STEPS; ++st) {
+            cA = __shfl_sync(0xffffffffu, cA, cA, G);
+            cB = __shfl_sync(0xffffffffu, cB, cB, G);
+          }
+        } else {
+          for (uint32_t st = 0; st < args.smax; ++st) {
+            cA = __shfl_sync(0xffffffffu, cA, cA, G);
+            cB = __shfl_sync(0xffffffffu, cB, cB, G);
+          }
+        }
+        const uint32_t xA = __shfl_sync(0xffffffffu, cA, 0, G) & args.sl_xmask;
+        const uint32_t xB = __shfl_sync(0xffffffffu, cB, 0, G) & args.sl_xmask;
+        if (xA >= args.sl_leafmin) {
+          if (aA && j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rA), "r"(xA) : "memory");
+          rA += 2 * NG;
+          aA = rA < rows;
+          wA = 0;
+          if (aA) bA = base_of(rA);
+        } else {
+          wA = xA << 3;
+        }
+        if (xB >= args.sl_leafmin) {
+          if (aB && j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rB), "r"(xB) : "memory");
+          rB += 2 * NG;
+          aB = rB < rows;
+          wB = 0;
+          if (aB) bB = base_of(rB);
+        } else {
+          wB = xB << 3;
+        }
+      } while (__any_sync(0xffffffffu, aA || aB));
+    } else if constexpr (SR == 2 && SL == 1) {
+      // Two record streams per group, self-loop codes (WinTable::sl_*).  Per
+      // window step and stream: entry, feature, compare, one shift selecting
+      // the successor code, ceil(log2 h) select-free shfl doublings, the
+      // root broadcast and one mask; then (sl_step) the stream either moves
+      // to the exit window (LEA) or, on a leaf, stores the code, steps to its
+      // next record by a constant address increment and restarts at the root
+      // window -- all predicated, no divergent branch.  An exhausted stream
+      // re-walks its last record (re-storing the same code) until every
+      // stream of the warp is done.
+      static_assert(Rec<A, kTma>::kRowLocal, "self-loop streams: records inside one 128-byte row");
+      const uint32_t a4 = 4u * (uint32_t)A;
+      auto base_of = [&](uint32_t rr) {
+        const uint32_t ra4 = rr * a4, rowb = ra4 & ~127u;
+        return (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
+      };
+      const uint32_t ng2 = 2u * NG, dl = 4u * ng2;
+      const uint32_t rA = g, rB = g + NG;
+      // label address of each stream's last record (a stream without
+      // records is done from the start and stores beyond `rows` only)
+      const uint32_t kA = rA < rows ? (rows - rA - 1u) / ng2 : 0u, kB = rB < rows ? (rows - rB - 1u) / ng2 : 0u;
+      uint32_t lA = lbuf + 4u * rA, lB = lbuf + 4u * rB;
+      const uint32_t eLA = lA + dl * kA, eLB = lB + dl * kB;
+      uint32_t dA = rA >= rows ? 1u : 0u, dB = rB >= rows ? 1u : 0u;
+      uint32_t bA = base_of(rA < rows ? rA : 0u), bB = base_of(rB < rows ? rB : 0u);
+      uint32_t aA = jaddr, aB = jaddr;
+      const uint32_t j0 = j == 0 ? 1u : 0u;
+      // one stream's terminal step (x = masked root code)
+      auto sl_step = [&](uint32_t x, uint32_t& a, uint32_t& b, uint32_t& l, uint32_t& d, uint32_t el) {
+        asm volatile(
+            "{\n\t"
+            ".reg .pred lf, sto, adv, fin;\n\t"
+            ".reg .u32 t;\n\t"
+            "setp.ge.u32 lf, %4, %6;\n\t"
+            "setp.ne.and.u32 sto, %7, 0, lf;\n\t"
+            "@sto st.shared.u32 [%2], %4;\n\t"
+            "setp.ne.and.u32 adv, %2, %5, lf;\n\t"
+            "setp.eq.and.u32 fin, %2, %5, lf;\n\t"
+            "@adv add.u32 %2, %2, %8;\n\t"
+            "@adv add.u32 %1, %1, %9;\n\t"
+            "@adv xor.b32 %1, %1, %10;\n\t"
+            "@fin mov.u32 %3, 1;\n\t"
+            "shl.b32 t, %4, 3;\n\t"
+            "add.u32 t, t, %11;\n\t"
+            "selp.u32 %0, %11, t, lf;\n\t"
+            "}"
+            : "=r"(a), "+r"(b), "+r"(l), "+r"(d)
+            : "r"(x), "r"(el), "r"(args.sl_leafmin), "r"(j0), "r"(dl), "r"(args.sl_adv), "r"(args.sl_xor),
+              "r"(jaddr)
+            : "memory");
+      };
+      do {
+        const uint2 eA = lds_u2(aA), eB = lds_u2(aB);
+        const float vA = lds_f32((eA.y & args.cw_amask) ^ bA), vB = lds_f32((eB.y & args.cw_amask) ^ bB);
+        uint32_t cA = eA.y >> (vA > __uint_as_float(eA.x) ? args.cw_rsh : args.cw_lsh);
+        uint32_t cB = eB.y >> (vB > __uint_as_float(eB.x) ? args.cw_rsh : args.cw_lsh);
+        if constexpr (STEPS >= 0) {
+#pragma unroll
+          for (int st = 0; st < STEPS; ++st) {
+            cA = __shfl_sync(0xffffffffu, cA, cA, G);
+            cB = __shfl_sync(0xffffffffu, cB, cB, G);
+          }
+        } else {
+          for (uint32_t st = 0; st < args.smax; ++st) {
+            cA = __shfl_sync(0xffffffffu, cA, cA, G);
+            cB = __shfl_sync(0xffffffffu, cB, cB, G);
+          }
+        }
+        const uint32_t xA = __shfl_sync(0xffffffffu, cA, 0, G) & args.sl_xmask;
+        const uint32_t xB = __shfl_sync(0xffffffffu, cB, 0, G) & args.sl_xmask;
+        sl_step(xA, aA, bA, lA, dA, eLA);
+        sl_step(xB, aB, bB, lB, dB, eLB);
+      } while (__any_sync(0xffffffffu, (dA & dB) == 0u));
     } else if constexpr (SR == 2 && WIN_SHARED && Rec<A, kTma>::kRowLocal) {
       // Two record streams per group in the lean style (no predication; an
       // exhausted stream re-walks its last record): two independent window
@@ -1352,7 +1524,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       if (rr < rows) {
         uint32_t code;
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(code) : "r"(lbuf + 4u * rr));
-        const uint32_t cls = code & (leafbit - 1u);
+        const uint32_t cls = ((code & args.lab_mask) >> args.lab_shift) - args.lab_sub;
         args.labels[r0 + rr] = args.leaf_class ? __ldg(args.leaf_class + cls) : cls;
       }
     }

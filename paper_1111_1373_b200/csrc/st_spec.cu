@@ -31,10 +31,10 @@ void launch_spec_steps(const SpecArgs& sa, const Staging& stg, size_t smem, int 
   }
 }
 
-template <int A, bool WS, int STEPS, int SR, bool CW = false, int RT = 1>
+template <int A, bool WS, int STEPS, int SR, bool CW = false, int RT = 1, int SL = 0>
 void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
                         uint32_t warps, cudaStream_t s) {
-  auto fn = k_spec_ring<A, WS, STEPS, SR, CW, RT>;
+  auto fn = k_spec_ring<A, WS, STEPS, SR, CW, RT, SL>;
   const uint64_t n_tiles = (ra.s.p.m + 32 * RT - 1) / (32 * RT);
   const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles * warps, warps);
   clear_stale_error();
@@ -44,10 +44,18 @@ void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem,
 
 template <int A, bool WS, int STEPS, bool CW = false>
 void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
-                         uint32_t warps, cudaStream_t s) {
+                         uint32_t warps, cudaStream_t s, int sl = 0) {
   // two record streams: shared window table and records inside one 128-byte row
   if constexpr (WS && (A == 8 || A == 16 || A == 32)) {
     if constexpr (CW) {
+      if (sl == 1 && sr >= 2) {  // self-loop codes (WinTable::sl_*), predicated advance
+        if (ra.tile_mult == 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 2, 1>(ra, stg, smem, dev, warps, s);
+        return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 1>(ra, stg, smem, dev, warps, s);
+      }
+      if (sl == 2 && sr >= 2) {  // self-loop codes, branchy advance
+        if (ra.tile_mult == 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 2, 2>(ra, stg, smem, dev, warps, s);
+        return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 2>(ra, stg, smem, dev, warps, s);
+      }
       if (sr >= 2 && ra.tile_mult == 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 2>(ra, stg, smem, dev, warps, s);
     }
     if (sr >= 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW>(ra, stg, smem, dev, warps, s);
@@ -56,16 +64,27 @@ void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg
 }
 
 template <int A>
-void launch_spec_ring(bool ws, uint32_t sr, bool cw, const SpecRingArgs& ra, const Staging& stg,
+void launch_spec_ring(bool ws, uint32_t sr, bool cw, int sl, const SpecRingArgs& ra, const Staging& stg,
                       size_t smem, int dev, uint32_t warps, cudaStream_t s) {
   // 8-byte window entries (shared table, window loop)
   if (cw && sr != 0) {
     switch (ra.s.smax) {
-      case 0: return launch_spec_ring_sr<A, true, 0, true>(sr, ra, stg, smem, dev, warps, s);
-      case 1: return launch_spec_ring_sr<A, true, 1, true>(sr, ra, stg, smem, dev, warps, s);
-      case 2: return launch_spec_ring_sr<A, true, 2, true>(sr, ra, stg, smem, dev, warps, s);
-      case 3: return launch_spec_ring_sr<A, true, 3, true>(sr, ra, stg, smem, dev, warps, s);
-      default: return launch_spec_ring_sr<A, true, -1, true>(sr, ra, stg, smem, dev, warps, s);
+      case 0: return launch_spec_ring_sr<A, true, 0, true>(sr, ra, stg, smem, dev, warps, s, sl);
+      case 1: return launch_spec_ring_sr<A, true, 1, true>(sr, ra, stg, smem, dev, warps, s, sl);
+      case 2: return launch_spec_ring_sr<A, true, 2, true>(sr, ra, stg, smem, dev, warps, s, sl);
+      case 3: return launch_spec_ring_sr<A, true, 3, true>(sr, ra, stg, smem, dev, warps, s, sl);
+      default: return launch_spec_ring_sr<A, true, -1, true>(sr, ra, stg, smem, dev, warps, s, sl);
+    }
+  }
+  // one window, pointer jumping with self-loop leaf codes
+  if (sr == 0 && ws && sl && ra.s.smax <= 5) {
+    switch (ra.s.smax) {
+      case 0: return launch_spec_ring_k<A, true, 0, 0, false, 1, 1>(ra, stg, smem, dev, warps, s);
+      case 1: return launch_spec_ring_k<A, true, 1, 0, false, 1, 1>(ra, stg, smem, dev, warps, s);
+      case 2: return launch_spec_ring_k<A, true, 2, 0, false, 1, 1>(ra, stg, smem, dev, warps, s);
+      case 3: return launch_spec_ring_k<A, true, 3, 0, false, 1, 1>(ra, stg, smem, dev, warps, s);
+      case 4: return launch_spec_ring_k<A, true, 4, 0, false, 1, 1>(ra, stg, smem, dev, warps, s);
+      default: return launch_spec_ring_k<A, true, 5, 0, false, 1, 1>(ra, stg, smem, dev, warps, s);
     }
   }
   // the whole tree in one window (sr == 0): hoisted entry, independent
@@ -211,13 +230,14 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   SpecArgs sa{};
   sa.p = pipe_args(x, m, a, ld, layout);
   sa.win = wdev;
-  sa.n_entries = (uint32_t)wt->entries.size();
+  sa.n_entries = wt->base_units;
   sa.root_code = wt->root_code;
   sa.G = G;
   sa.smax = wt->max_steps;
   sa.k = g.reductions;
   sa.leaf_class = dv.leaf_tbl;
   sa.labels = labels;
+  sa.lab_mask = kLeafBit - 1u;  // ring label rows: kLeafBit | class (per-format overrides below)
   if (stats) {
     sa.iters = stats->iterations;
     sa.steps = stats->doubling_steps;
@@ -227,7 +247,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     // k without counters: same labels; the fixed-step path is used
     sa.k = 0;
   }
-  const uint32_t win_bytes = round1024(wt->entries.size() * sizeof(SEntry));
+  const uint32_t win_bytes = round1024((size_t)wt->base_units * sizeof(SEntry));
   bool win_shared = win_bytes <= 96 * 1024;
   Staging stg = plan_staging(x, m, a, ld, layout, 1, g.stages, win_shared ? win_bytes : 0, pr);
   if (win_shared && win_bytes + 1024 + stg.tile_smem() > pr.smem_optin) {
@@ -267,6 +287,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
         rs.cw_leaf = 1u << (cb2 - 1u);
         rs.cw_emask = (1u << (cb2 - 2u)) - 1u;
         rs.cw_wstride = 8u * G;
+        rs.lab_mask = rs.cw_leaf - 1u;
       }
     }
     // record streams per group (samples_per_thread): two independent window
@@ -277,6 +298,57 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     // profiles/r1_sweep_*_spec2d.json, *_spec2e.json)
     uint32_t sr = g.samples_per_thread ? g.samples_per_thread : ((cw || t->info.internal > 511) ? 2u : 1u);
     if (onewin) sr = 0;  // whole tree in one window
+    // Self-loop codes (WinTable::sl_*): a terminal code's low bits name its
+    // own lane, so every pointer-jumping step is one shfl with no select,
+    // and the two-stream loop advances a resolved stream by a constant
+    // record-address step under predication.  Needs the stream step to keep
+    // the tile's 128B-swizzle phase (row step = 0 or 4 mod 8).
+    // ST_VAR_SPEC_SELECT keeps the select-per-step loop.
+    int sl = 0;
+    uint32_t lg = 0;
+    while ((1u << lg) < G) ++lg;
+    // Complete trees (leaves == 2^depth) keep the select loop: their streams
+    // resolve in lockstep and it measured 1-2 % ahead there (C5 d8 / d12).
+    const bool complete = t->info.depth < 32 && t->info.leaves == (1u << t->info.depth);
+    const bool want_sl = !(g.variant & ST_VAR_SPEC_SELECT) &&
+                         (!complete || (g.variant & (ST_VAR_SPEC_PRED | ST_VAR_SPEC_BRANCH)));
+    if (!(g.variant & ST_VAR_SPEC_SELECT)) {
+      const uint32_t ng = 32u / G;
+      const uint32_t adv = 2u * ng * 4u * a, rows_step = adv / 128u;
+      if (want_sl && cw && sr >= 2 && wt->sl_units && (a == 8 || a == 16 || a == 32) && adv % 128u == 0 &&
+          (rows_step % 8u == 0 || rows_step % 8u == 4) &&
+          round1024((size_t)wt->sl_units * sizeof(SEntry)) <= 96 * 1024) {
+        // Stream advance: predicated on skewed trees (depth >= log2(leaves)
+        // + 3: records resolve after scattered window counts, so some stream
+        // of the warp resolves in nearly every step -- C5 d16 / d20 -9 / -10
+        // %), a divergent branch on (near-)complete ones (streams resolve in
+        // lockstep: C5 d8 / d12 -6 / -7 %, C1 -7 %, C3 -6 %; C2 even;
+        // profiles/r2_spec_sl_ab.txt).  ST_VAR_SPEC_PRED / _BRANCH force one.
+        uint32_t lgl = 0;
+        while ((1u << lgl) < t->info.leaves) ++lgl;
+        sl = (g.variant & ST_VAR_SPEC_PRED) ? 1
+             : (g.variant & ST_VAR_SPEC_BRANCH) ? 2
+             : t->info.depth >= lgl + 3 ? 1 : 2;
+        rs.win = wdev + wt->sl_off;
+        rs.n_entries = wt->sl_units;
+        rs.win_bytes = round1024((size_t)wt->sl_units * sizeof(SEntry));
+        rs.cw_amask = (1u << wt->sl_abits) - 1u;
+        rs.cw_lsh = wt->sl_abits;
+        rs.cw_rsh = wt->sl_abits + wt->sl_cbits;
+        rs.sl_xmask = ((1u << wt->sl_cbits) - 1u) & ~(G - 1u);
+        rs.sl_leafmin = wt->sl_nw << lg;
+        rs.sl_adv = adv;
+        rs.sl_xor = rows_step % 8u == 4 ? 0x40u : 0u;
+        rs.lab_mask = 0xFFFFFFFFu;
+        rs.lab_shift = lg;
+        rs.lab_sub = wt->sl_nw;
+      }
+      if (onewin && (g.variant & ST_VAR_SPEC_JUMP) && wt->sl1_off) {
+        sl = 1;  // one window: pointer jumping with self-loop leaf codes
+        rs.lab_mask = ~kLeafBit;
+        rs.lab_shift = 5;
+      }
+    }
     // 64-record ring slots for the two-stream 8-byte-window loop: the slot's
     // records are shared by 16 streams, 4 each instead of 2, which evens out
     // the streams' window counts and halves the per-slot overhead -- taken
@@ -306,14 +378,15 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       ra.s.stage_bytes = rstg.stage_bytes;
       const size_t rsmem = 1024 + rs.win_bytes + (size_t)ra.n_slots * (rstg.stage_bytes + 8u) +
                            (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128 * rt;
-      // one window: ballot + leaf path masks unless pointer jumping is asked for
-      if (onewin) ra.s.pm_off = (g.variant & ST_VAR_SPEC_JUMP) ? 0u : wt->pm_off;
+      // one window: ballot + leaf path masks unless pointer jumping is asked
+      // for (pm_off then names the self-loop entries, or 0: select per step)
+      if (onewin) ra.s.pm_off = (g.variant & ST_VAR_SPEC_JUMP) ? (sl ? wt->sl1_off : 0u) : wt->pm_off;
       switch (ct_arity(a) ? a : 0) {
-        case 8: return launch_spec_ring<8>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
-        case 16: return launch_spec_ring<16>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
-        case 32: return launch_spec_ring<32>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
-        case 64: return launch_spec_ring<64>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
-        default: return launch_spec_ring<0>(ws, sr, cw, ra, rstg, rsmem, dev, warps, s);
+        case 8: return launch_spec_ring<8>(ws, sr, cw, sl, ra, rstg, rsmem, dev, warps, s);
+        case 16: return launch_spec_ring<16>(ws, sr, cw, sl, ra, rstg, rsmem, dev, warps, s);
+        case 32: return launch_spec_ring<32>(ws, sr, cw, sl, ra, rstg, rsmem, dev, warps, s);
+        case 64: return launch_spec_ring<64>(ws, sr, cw, sl, ra, rstg, rsmem, dev, warps, s);
+        default: return launch_spec_ring<0>(ws, sr, cw, sl, ra, rstg, rsmem, dev, warps, s);
       }
     }
   }

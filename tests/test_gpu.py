@@ -416,7 +416,7 @@ def test_folded_tree_walks(cuda, co, fold_min):
             assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, g)
 
 
-@pytest.mark.parametrize("mode", ["ballot", "jump", "general"])
+@pytest.mark.parametrize("mode", ["ballot", "jump", "jump_select", "general"])
 def test_single_window_speculation(cuda, co, mode):
     """Trees with <= 32 internal nodes speculate as one window (the paper's
     Proc. 5 geometry): the one-window ring path with the ballot + leaf
@@ -424,7 +424,8 @@ def test_single_window_speculation(cuda, co, mode):
     and the general window loop (ST_VAR_SPEC_GENERAL), against the oracles --
     all exhaustive shapes up to 8 leaves, and random small trees over
     row-local, odd and wide arities with ragged record counts."""
-    var = {"ballot": (), "jump": ("spec_jump",), "general": ("spec_general",)}[mode]
+    var = {"ballot": (), "jump": ("spec_jump",), "jump_select": ("spec_jump", "spec_select"),
+           "general": ("spec_general",)}[mode]
     geoms = [st.GpuGeom(algo="speculative", variant=var),
              st.GpuGeom(algo="speculative", group_lanes=32, variant=var),
              st.GpuGeom(algo="speculative", group_lanes=16, variant=var)]
@@ -450,14 +451,16 @@ def test_single_window_speculation(cuda, co, mode):
             assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, m, g)
 
 
-@pytest.mark.parametrize("wide", [False, True])
+@pytest.mark.parametrize("wide", [(), ("spec_wide",), ("spec_select",), ("spec_pred",), ("spec_branch",)])
 def test_spec_window_formats(cuda, co, wide):
-    """The ring kernel's 8-byte window entries (default when the tree's
-    fields fit) and the 16-byte format (ST_VAR_SPEC_WIDE): random trees
+    """The ring kernel's window formats: 8-byte entries with self-loop codes
+    (default; stream advance predicated or branchy by tree shape, and both
+    forced), 8-byte entries with a select per doubling (ST_VAR_SPEC_SELECT)
+    and the 16-byte format (ST_VAR_SPEC_WIDE): random trees
     with many windows, group widths 2..16, one and two record streams,
     row-local and other arities, ragged counts, large leaf payloads
     (class ids >= 2^31 -> ordinals), against the oracle."""
-    var = ("spec_wide",) if wide else ()
+    var = wide
     for seed in range(1, 161):
         a = (8, 16, 32, 19, 64, 3, 128, 300)[seed % 8]
         depth = 4 + seed % 17
@@ -532,5 +535,7 @@ def test_spec_ring_slot_sizes(cuda, co, tile):
             want = co.eval_serial(nodes, x)
             xd = torch.from_numpy(x).to(cuda)
             for g in (st.GpuGeom(algo="speculative", slot_records=tile),
+                      st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_pred",)),
+                      st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_branch",)),
                       st.GpuGeom(algo="speculative", group_lanes=8, slot_records=tile)):
                 assert np.array_equal(_dev_eval(nodes, xd, g, m), want), (depth, a, m, g, tile)
