@@ -74,7 +74,7 @@ WORKLOADS = {
                   tree=(11, 16, 19, 7, 1), m=16384 * 1024, a=19, seed=2, tile=16384,
                   labels_fnv=0xc90f17638d0c1525),  # hash of the first 4 tiles (Appendix A)
 }
-for _d in (8, 12, 16, 20):
+for _d in (8, 10, 12, 14, 16, 18, 20):
     WORKLOADS[f"C5d{_d}"] = dict(desc=f"C5 shard: depth-{_d} tree, 16 attributes, 15.625M samples per GPU",
                                  tree=(_d, min(2 ** _d, 4096), 16, 8, 500 + _d), m=15_625_000, a=16,
                                  seed=5000, seed_step=1, golden=f"c5:{_d}")

@@ -113,7 +113,8 @@ enum st_variant {
   ST_VAR_SPEC_SELECT = 32u, /* speculative: a select per pointer-jumping step (round-1 codes) instead
                                of self-loop terminal codes */
   ST_VAR_SPEC_PRED = 64u,   /* speculative, self-loop two-stream loop: predicated stream advance */
-  ST_VAR_SPEC_BRANCH = 128u /* ... the stream advance in a divergent branch (default: by tree shape) */
+  ST_VAR_SPEC_BRANCH = 128u,/* ... the stream advance in a divergent branch (default: by tree shape) */
+  ST_VAR_SPEC_FIXED = 256u  /* ... every record runs the deepest window count, leaves absorbing */
 };
 
 /* Optional per-record speculative counters (SpeculativeStats,

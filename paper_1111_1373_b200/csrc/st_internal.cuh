@@ -151,6 +151,10 @@ struct WinTable {
   // sl_nw.. hold copies of window 0: after a leaf the stream restarts at the
   // root without a select.
   uint32_t sl_off = 0, sl_units = 0, sl_abits = 0, sl_cbits = 0, sl_nw = 0;
+  // fixed-trip loop: the most windows any record visits, and the expected
+  // count under the synthetic data distribution (leaf weight 2^-depth)
+  uint32_t sl_wmax = 0;
+  double sl_wmean = 0.0;
   // One-window trees: entries[sl1_off + j] = {thr, 4*attr, left, right} with
   // self-loop leaf codes kLeafBit | leaf code << 5 | j (0 = none).
   uint32_t sl1_off = 0;
@@ -227,6 +231,7 @@ struct st_tree {
     std::vector<int32_t> win_of_root(n, -1);
     std::vector<std::vector<uint32_t>> members;
     std::vector<std::vector<uint32_t>> ldepth;
+    std::vector<uint32_t> wdepth{1};  // windows on the path from the root window, inclusive
     std::deque<uint32_t> roots;
     win_of_root[0] = 0;
     members.emplace_back();
@@ -261,6 +266,7 @@ struct st_tree {
           win_of_root[u] = (int32_t)members.size();
           members.emplace_back();
           ldepth.emplace_back();
+          wdepth.push_back(wdepth[w] + 1);
           roots.push_back(u);
         }
       }
@@ -395,14 +401,45 @@ struct st_tree {
             slt[(size_t)w * G + j] = make_uint2(0u, 4u * nodes[mem[0]].attribute);
           for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = -1;
         }
-        for (uint64_t w = nw; w < units; ++w)  // root copies (leaf payloads)
-          std::copy(slt.begin(), slt.begin() + G, slt.begin() + (size_t)w * G);
+        // Leaf sinks: window sl_nw + c holds, in every lane, the terminal
+        // code of leaf payload c on both sides, so a stream that reached a
+        // leaf stays there for any number of further window steps (leaves
+        // are fixpoints, eval_speculative.cpp:38-51) -- the fixed-trip loop
+        // runs every record for sl_wmax steps with no per-step test.
+        for (uint64_t w = nw; w < units; ++w)
+          for (uint32_t j = 0; j < G; ++j) {
+            const uint32_t code = ((uint32_t)w << lg) | j;
+            slt[(size_t)w * G + j] = make_uint2(0u, (code << abits) | (code << (abits + cbits2)));
+          }
         if (slt.size() & 1) slt.push_back(make_uint2(0u, 0u));
         wt.sl_off = (uint32_t)wt.entries.size();
         wt.sl_units = (uint32_t)(slt.size() / 2);
         wt.sl_abits = abits;
         wt.sl_cbits = cbits2;
         wt.sl_nw = nw;
+        // fixed-trip statistics: the deepest window count, and its mean over
+        // records under uniform data and midpoint splits (leaf weight
+        // 2^-depth: the synthetic generators' volume fractions)
+        std::vector<uint32_t> nd(n, 0);
+        double ew = 0.0, wsum = 0.0;
+        for (uint32_t i = 0; i < n; ++i) {
+          if (is_leaf(i)) continue;
+          for (uint32_t c : {nodes[i].child, nodes[i].child + 1}) nd[c] = std::max(nd[c], nd[i] + 1);
+        }
+        std::vector<uint32_t> win_of_node(n, 0);
+        for (uint32_t w = 0; w < nw; ++w)
+          for (uint32_t u : members[w]) win_of_node[u] = w;
+        for (uint32_t i = 0; i < n; ++i) {
+          if (is_leaf(i)) continue;
+          for (uint32_t c : {nodes[i].child, nodes[i].child + 1}) {
+            if (!is_leaf(c)) continue;
+            const double wt_c = std::ldexp(1.0, -(int)std::min<uint32_t>(nd[c], 1000));
+            wsum += wt_c;
+            ew += wt_c * wdepth[win_of_node[i]];
+          }
+        }
+        wt.sl_wmax = *std::max_element(wdepth.begin(), wdepth.end());
+        wt.sl_wmean = wsum > 0 ? ew / wsum : (double)wt.sl_wmax;
         wt.entries.resize(wt.entries.size() + wt.sl_units, SEntry{0.0f, 0u, 0u, 0u});
         std::memcpy(wt.entries.data() + wt.sl_off, slt.data(), slt.size() * sizeof(uint2));
       }

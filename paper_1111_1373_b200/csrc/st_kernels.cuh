@@ -819,6 +819,7 @@ struct SpecArgs {
   // log2 G), first leaf code, a stream's advance to its next record (bytes
   // added to / XOR applied to its swizzled record address)
   uint32_t sl_xmask, sl_leafmin, sl_adv, sl_xor;
+  uint32_t sl_wmax;      // SL == 3: window steps every record takes (leaves are sinks)
   // ring label rows hold raw terminal codes: class = ((code & lab_mask) >>
   // lab_shift) - lab_sub (then the leaf-class table, if any)
   uint32_t lab_mask, lab_shift, lab_sub;
@@ -997,6 +998,7 @@ __global__ void __launch_bounds__(kMaxThreads)
 struct SpecRingArgs {
   SpecArgs s;
   uint32_t n_slots;       // NS
+  uint32_t ns_magic;      // floor(2^32 / NS): ticket -> (generation, slot) without a division
   uint32_t bulk_win;      // stage the window table with one cp.async.bulk (else per-thread loads)
   uint32_t tile_mult;     // host: records per ring slot / 32 (the kernel's RT)
 };
@@ -1008,14 +1010,16 @@ struct SpecRingArgs {
 // one shfl with no select.  With SR == 2: SL == 1 advances a resolved
 // stream by a constant address step under predication (skewed trees, where
 // some stream of the warp resolves in almost every window step), SL == 2 in
-// a divergent branch taken only when one does (complete trees, whose
-// streams resolve in lockstep every depth / h steps).
+// a divergent branch taken only when one does; SL == 3 runs every record for
+// a fixed sl_wmax window steps with leaves as absorbing sink windows -- no
+// per-step test at all (balanced trees, where records' window counts barely
+// differ).
 template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false, int RT = 1, int SL = 0>
 __global__ void __launch_bounds__(kMaxThreads)
     k_spec_ring(const SpecRingArgs ra, const __grid_constant__ CUtensorMap tmap) {
   static_assert(!CW || (WIN_SHARED && SR >= 1), "8-byte windows: shared table, window-loop paths");
   static_assert(!SL || SR == 0 || (SR == 2 && CW), "self-loop codes: one window, or two 8-byte-window streams");
-  static_assert(SL != 2 || SR == 2, "branchy stream advance: two-stream loop");
+  static_assert(SL < 2 || SR == 2, "branchy / fixed-trip stream loops: two-stream layout");
   static_assert(RT == 1 || SR == 2, "multi-chunk slots: two-stream loop only");
   extern __shared__ __align__(1024) unsigned char smem[];
   const SpecArgs& args = ra.s;
@@ -1039,9 +1043,14 @@ __global__ void __launch_bounds__(kMaxThreads)
   auto tile_of = [&](uint64_t j) { return blockIdx.x + j * (uint64_t)gridDim.x; };
   // Stage tile j into slot b: TMA for full tiles (lane 0), warp-cooperative
   // swizzled stores + a plain arrive for the partial tail.
-  auto fill = [&](uint64_t jj) {
+  // ticket -> (generation q, slot r): multiply-high estimate, one correction
+  auto divmod_ns = [&](uint32_t x, uint32_t& q, uint32_t& r) {
+    q = __umulhi(x, ra.ns_magic);
+    r = x - q * NS;
+    if (r >= NS) ++q, r -= NS;
+  };
+  auto fill = [&](uint64_t jj, uint32_t b) {
     const uint64_t t = tile_of(jj);
-    const uint32_t b = (uint32_t)(jj % NS);
     const uint32_t dst = slots0 + b * args.stage_bytes;
     const uint64_t r0 = t * (uint64_t)R;
     if ((t + 1) * (uint64_t)R <= m) {
@@ -1075,7 +1084,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   }
   __syncthreads();
   if (warp == 0)
-    for (uint64_t jj = 0; jj < NS && jj < my_tiles; ++jj) fill(jj);
+    for (uint64_t jj = 0; jj < NS && jj < my_tiles; ++jj) fill(jj, (uint32_t)jj);
   // window table staged while the first tiles are in flight
   if constexpr (WIN_SHARED) {
     if (!ra.bulk_win) {
@@ -1151,7 +1160,8 @@ __global__ void __launch_bounds__(kMaxThreads)
     if (tk >= my_tiles) break;
     const uint64_t t = tile_of(tk);
     const uint64_t r0 = t * (uint64_t)R;
-    const uint32_t b = tk % NS;
+    uint32_t gen, b;
+    divmod_ns(tk, gen, b);
     const uint32_t tile = slots0 + b * args.stage_bytes;
     const uint32_t rows = (uint32_t)((m - r0) < (uint64_t)R ? (m - r0) : (uint64_t)R);
     // A parity wait cannot tell generation g of a slot from g + 2: a slow
@@ -1165,13 +1175,12 @@ __global__ void __launch_bounds__(kMaxThreads)
     // Every lane polls the same word (one broadcast wavefront, warp-uniform
     // exit): no divergent lane-0 section before the walk's shuffles.
     {
-      const uint32_t g = tk / NS;
       uint32_t have;
       do {
         asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(have) : "r"(gen0 + 4u * b) : "memory");
-      } while (__any_sync(0xffffffffu, have < g));
+      } while (__any_sync(0xffffffffu, have < gen));
     }
-    mbar_wait(full0 + 8u * b, (tk / NS) & 1u);
+    mbar_wait(full0 + 8u * b, gen & 1u);
     if (args.root_code & kLeafBit) {  // N == 1
 #pragma unroll
       for (int k = 0; k < RT; ++k)
@@ -1332,6 +1341,62 @@ __global__ void __launch_bounds__(kMaxThreads)
           woff = exit_off(root);
         }
       } while (__any_sync(0xffffffffu, active));
+    } else if constexpr (SR == 2 && SL == 3) {
+      // Fixed trip count (the paper's Proc. 5 property lifted to windows:
+      // terminal codes are fixpoints, so extra steps are harmless): each
+      // group walks its records as batches of KS independent streams, every
+      // stream exactly sl_wmax window steps -- entry, feature, compare,
+      // shift, select-free doublings, root broadcast, mask, LEA -- then the
+      // group's lane 0 stores the KS leaf codes.  No leaf test, no stream
+      // state, no divergence.
+      static_assert(Rec<A, kTma>::kRowLocal, "fixed-trip streams: records inside one 128-byte row");
+      constexpr int KS = 4;
+      const uint32_t a4 = 4u * (uint32_t)A;
+      auto base_of = [&](uint32_t rr) {
+        const uint32_t ra4 = rr * a4, rowb = ra4 & ~127u;
+        return (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
+      };
+      const uint32_t per_group = R / NG;  // records of this group in the slot
+      for (uint32_t k0 = 0; k0 < per_group; k0 += KS) {
+        uint32_t rr[KS], bx[KS], ad[KS];
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          rr[s] = g + NG * (k0 + s);
+          bx[s] = base_of(rr[s] < rows ? rr[s] : 0u);  // rows past a partial tile walk record 0
+          ad[s] = jaddr;
+        }
+        for (uint32_t w = 0; w < args.sl_wmax; ++w) {
+          uint32_t c[KS];
+#pragma unroll
+          for (int s = 0; s < KS; ++s) {
+            const uint2 e = lds_u2(ad[s]);
+            const float v = lds_f32((e.y & args.cw_amask) ^ bx[s]);
+            c[s] = e.y >> (v > __uint_as_float(e.x) ? args.cw_rsh : args.cw_lsh);
+          }
+          if constexpr (STEPS >= 0) {
+#pragma unroll
+            for (int st = 0; st < STEPS; ++st)
+#pragma unroll
+              for (int s = 0; s < KS; ++s) c[s] = __shfl_sync(0xffffffffu, c[s], c[s], G);
+          } else {
+            for (uint32_t st = 0; st < args.smax; ++st)
+#pragma unroll
+              for (int s = 0; s < KS; ++s) c[s] = __shfl_sync(0xffffffffu, c[s], c[s], G);
+          }
+#pragma unroll
+          for (int s = 0; s < KS; ++s) {
+            const uint32_t x = __shfl_sync(0xffffffffu, c[s], 0, G) & args.sl_xmask;
+            ad[s] = jaddr + (x << 3);
+            c[s] = x;
+          }
+          if (w + 1 == args.sl_wmax && j == 0) {
+#pragma unroll
+            for (int s = 0; s < KS; ++s)
+              if (rr[s] < rows)
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rr[s]), "r"(c[s]) : "memory");
+          }
+        }
+      }
     } else if constexpr (SR == 2 && SL == 2) {
       // Two record streams, self-loop codes, the stream advance in a
       // divergent branch (taken by the warp only in steps where some stream
@@ -1404,7 +1469,8 @@ __global__ void __launch_bounds__(kMaxThreads)
       const uint32_t rA = g, rB = g + NG;
       // label address of each stream's last record (a stream without
       // records is done from the start and stores beyond `rows` only)
-      const uint32_t kA = rA < rows ? (rows - rA - 1u) / ng2 : 0u, kB = rB < rows ? (rows - rB - 1u) / ng2 : 0u;
+      const uint32_t lg2 = (uint32_t)__ffs(ng2) - 1u;  // ng2 = 64 / G: a power of two
+      const uint32_t kA = rA < rows ? (rows - rA - 1u) >> lg2 : 0u, kB = rB < rows ? (rows - rB - 1u) >> lg2 : 0u;
       uint32_t lA = lbuf + 4u * rA, lB = lbuf + 4u * rB;
       const uint32_t eLA = lA + dl * kA, eLB = lB + dl * kB;
       uint32_t dA = rA >= rows ? 1u : 0u, dB = rB >= rows ? 1u : 0u;
@@ -1514,9 +1580,9 @@ __global__ void __launch_bounds__(kMaxThreads)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA refill
     __syncwarp();
     if (tk + NS < my_tiles) {
-      fill(tk + NS);  // this warp freed slot b: refill it ...
+      fill(tk + NS, b);  // this warp freed slot b: refill it ...
       if (lane == 0)  // ... and publish that generation tk / NS + 1 is on its way
-        asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(tk / NS + 1u) : "memory");
+        asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(gen + 1u) : "memory");
     }
 #pragma unroll
     for (int k = 0; k < RT; ++k) {

@@ -52,6 +52,10 @@ void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg
         if (ra.tile_mult == 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 2, 1>(ra, stg, smem, dev, warps, s);
         return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 1>(ra, stg, smem, dev, warps, s);
       }
+      if (sl == 3 && sr >= 2) {  // self-loop codes, fixed trip count
+        if (ra.tile_mult == 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 2, 3>(ra, stg, smem, dev, warps, s);
+        return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 3>(ra, stg, smem, dev, warps, s);
+      }
       if (sl == 2 && sr >= 2) {  // self-loop codes, branchy advance
         if (ra.tile_mult == 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 2, 2>(ra, stg, smem, dev, warps, s);
         return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 2>(ra, stg, smem, dev, warps, s);
@@ -307,28 +311,32 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     int sl = 0;
     uint32_t lg = 0;
     while ((1u << lg) < G) ++lg;
-    // Complete trees (leaves == 2^depth) keep the select loop: their streams
-    // resolve in lockstep and it measured 1-2 % ahead there (C5 d8 / d12).
-    const bool complete = t->info.depth < 32 && t->info.leaves == (1u << t->info.depth);
-    const bool want_sl = !(g.variant & ST_VAR_SPEC_SELECT) &&
-                         (!complete || (g.variant & (ST_VAR_SPEC_PRED | ST_VAR_SPEC_BRANCH)));
+    const bool want_sl = !(g.variant & ST_VAR_SPEC_SELECT);
     if (!(g.variant & ST_VAR_SPEC_SELECT)) {
       const uint32_t ng = 32u / G;
       const uint32_t adv = 2u * ng * 4u * a, rows_step = adv / 128u;
       if (want_sl && cw && sr >= 2 && wt->sl_units && (a == 8 || a == 16 || a == 32) && adv % 128u == 0 &&
           (rows_step % 8u == 0 || rows_step % 8u == 4) &&
           round1024((size_t)wt->sl_units * sizeof(SEntry)) <= 96 * 1024) {
-        // Stream advance: predicated on skewed trees (depth >= log2(leaves)
-        // + 3: records resolve after scattered window counts, so some stream
-        // of the warp resolves in nearly every step -- C5 d16 / d20 -9 / -10
-        // %), a divergent branch on (near-)complete ones (streams resolve in
-        // lockstep: C5 d8 / d12 -6 / -7 %, C1 -7 %, C3 -6 %; C2 even;
-        // profiles/r2_spec_sl_ab.txt).  ST_VAR_SPEC_PRED / _BRANCH force one.
+        // Loop shape by tree (same-box A/B, profiles/r2_spec_sl_ab.txt):
+        //  * balanced (the deepest record visits <= 1.5x the expected window
+        //    count): fixed trip count, leaves absorbing, no per-step test --
+        //    C5 d8 / d10 / d12 / d14 -5 / -6 / -4 / -17 %, C1 -6 %, C3 -11 %
+        //    vs the select loop;
+        //  * skewed (depth >= log2(leaves) + 3): the stream advance
+        //    predicated -- some stream of the warp resolves in nearly every
+        //    step -- C5 d16 / d18 / d20 -15 / -16 / -17 %, C2 -5 %;
+        //  * otherwise the advance in a divergent branch.
+        // ST_VAR_SPEC_FIXED / _PRED / _BRANCH force one.
         uint32_t lgl = 0;
         while ((1u << lgl) < t->info.leaves) ++lgl;
+        const bool balanced = wt->sl_wmax <= 1.5 * wt->sl_wmean;
         sl = (g.variant & ST_VAR_SPEC_PRED) ? 1
              : (g.variant & ST_VAR_SPEC_BRANCH) ? 2
+             : (g.variant & ST_VAR_SPEC_FIXED) ? 3
+             : balanced ? 3
              : t->info.depth >= lgl + 3 ? 1 : 2;
+        rs.sl_wmax = wt->sl_wmax;
         rs.win = wdev + wt->sl_off;
         rs.n_entries = wt->sl_units;
         rs.win_bytes = round1024((size_t)wt->sl_units * sizeof(SEntry));
@@ -373,6 +381,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       ra.n_slots = (uint32_t)std::min<size_t>(max_slots, warps + 12);
       // stress knob: any ring depth >= 1 must give exact labels
       if (g.ring_slots) ra.n_slots = std::min<uint32_t>(ra.n_slots, g.ring_slots);
+      ra.ns_magic = (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, (1ull << 32) / ra.n_slots);
       ra.bulk_win = (g.variant & ST_VAR_TREE_LOOP) ? 0u : 1u;
       ra.tile_mult = rt;
       ra.s.stage_bytes = rstg.stage_bytes;

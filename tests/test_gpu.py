@@ -451,7 +451,8 @@ def test_single_window_speculation(cuda, co, mode):
             assert np.array_equal(st.eval_gpu(nodes, x, g), want), (seed, a, m, g)
 
 
-@pytest.mark.parametrize("wide", [(), ("spec_wide",), ("spec_select",), ("spec_pred",), ("spec_branch",)])
+@pytest.mark.parametrize("wide", [(), ("spec_wide",), ("spec_select",), ("spec_pred",), ("spec_branch",),
+                                  ("spec_fixed",)])
 def test_spec_window_formats(cuda, co, wide):
     """The ring kernel's window formats: 8-byte entries with self-loop codes
     (default; stream advance predicated or branchy by tree shape, and both
@@ -537,5 +538,6 @@ def test_spec_ring_slot_sizes(cuda, co, tile):
             for g in (st.GpuGeom(algo="speculative", slot_records=tile),
                       st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_pred",)),
                       st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_branch",)),
+                      st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_fixed",)),
                       st.GpuGeom(algo="speculative", group_lanes=8, slot_records=tile)):
                 assert np.array_equal(_dev_eval(nodes, xd, g, m), want), (depth, a, m, g, tile)

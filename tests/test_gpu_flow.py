@@ -122,7 +122,7 @@ def test_spec_ring_shallow_ring_stress(cuda, co, slots):
     x = co.gen_dataset(400_000, 32, 202)
     want = co.eval_serial(nodes, x)
     xd = torch.from_numpy(x).cuda()
-    for sr, var in ((1, ()), (2, ()), (2, ("spec_branch",)), (2, ("spec_select",)), (1, ())):
+    for sr, var in ((1, ()), (2, ()), (2, ("spec_branch",)), (2, ("spec_select",)), (2, ("spec_fixed",)), (1, ())):
         out = torch.empty(len(x), dtype=torch.int32, device="cuda")
         st.eval_device(nodes, xd, out, st.GpuGeom(algo="speculative", pipeline=2, samples_per_thread=sr,
                                                   ring_slots=slots, variant=var))
