@@ -249,6 +249,10 @@ class Dist:
             backend = "nccl" if torch.cuda.device_count() >= self.world else "gloo"
         self.backend = backend
         if self.world > 1:
+            # NCCL's communicator-init lines (rank count per communicator) on
+            # stderr, unless the launcher chose its own NCCL_DEBUG
+            if "NCCL_DEBUG" not in os.environ:
+                os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT", NCCL_DEBUG_FILE="/dev/stderr")
             if backend == "nccl":
                 dist.init_process_group("nccl", device_id=dev)
             else:

@@ -155,6 +155,7 @@ struct WinTable {
   // count under the synthetic data distribution (leaf weight 2^-depth)
   uint32_t sl_wmax = 0;
   double sl_wmean = 0.0;
+  uint32_t sl_ws = 0;  // entries per window in the self-loop table
   // One-window trees: entries[sl1_off + j] = {thr, 4*attr, left, right} with
   // self-loop leaf codes kLeafBit | leaf code << 5 | j (0 = none).
   uint32_t sl1_off = 0;
@@ -380,8 +381,13 @@ struct st_tree {
       const uint64_t units = (uint64_t)nw + ncodes;      // windows + root copies
       uint32_t cbits2 = 1;
       while (cbits2 < 40 && ((units * G - 1) >> cbits2) != 0) ++cbits2;
+      // ws entries per window (the largest window; lanes >= ws read lane
+      // 0's entry): G = 4 two-level windows pack their 3 nodes in 24 B
+      uint32_t ws = 1;
+      for (uint32_t w = 0; w < nw; ++w) ws = std::max<uint32_t>(ws, (uint32_t)members[w].size());
+      if ((8u * ws) % G != 0) ws = G;
       if (G <= 32 && (1u << lg) == G && ncodes <= 64 && abits + 2 * cbits2 <= 32 && units * G < (1u << 24)) {
-        std::vector<uint2> slt((size_t)units * G + 64, make_uint2(0u, 0u));
+        std::vector<uint2> slt((size_t)units * ws + 64, make_uint2(0u, 0u));
         for (uint32_t w = 0; w < nw; ++w) {
           const auto& mem = members[w];
           for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = (int32_t)j;
@@ -394,11 +400,11 @@ struct st_tree {
             const st_node& nd = nodes[mem[j]];
             uint32_t tb;
             std::memcpy(&tb, &nd.threshold, 4);
-            slt[(size_t)w * G + j] = make_uint2(
+            slt[(size_t)w * ws + j] = make_uint2(
                 tb, (4u * nd.attribute) | (scode(nd.child) << abits) | (scode(nd.child + 1) << (abits + cbits2)));
           }
-          for (uint32_t j = (uint32_t)mem.size(); j < G; ++j)  // unused lanes: the root's word (broadcast)
-            slt[(size_t)w * G + j] = make_uint2(0u, 4u * nodes[mem[0]].attribute);
+          for (uint32_t j = (uint32_t)mem.size(); j < ws; ++j)  // unused lanes: the root's word (broadcast)
+            slt[(size_t)w * ws + j] = make_uint2(0u, 4u * nodes[mem[0]].attribute);
           for (uint32_t j = 0; j < mem.size(); ++j) lane_of[mem[j]] = -1;
         }
         // Leaf sinks: window sl_nw + c holds, in every lane, the terminal
@@ -407,9 +413,9 @@ struct st_tree {
         // are fixpoints, eval_speculative.cpp:38-51) -- the fixed-trip loop
         // runs every record for sl_wmax steps with no per-step test.
         for (uint64_t w = nw; w < units; ++w)
-          for (uint32_t j = 0; j < G; ++j) {
+          for (uint32_t j = 0; j < ws; ++j) {
             const uint32_t code = ((uint32_t)w << lg) | j;
-            slt[(size_t)w * G + j] = make_uint2(0u, (code << abits) | (code << (abits + cbits2)));
+            slt[(size_t)w * ws + j] = make_uint2(0u, (code << abits) | (code << (abits + cbits2)));
           }
         if (slt.size() & 1) slt.push_back(make_uint2(0u, 0u));
         wt.sl_off = (uint32_t)wt.entries.size();
@@ -417,6 +423,7 @@ struct st_tree {
         wt.sl_abits = abits;
         wt.sl_cbits = cbits2;
         wt.sl_nw = nw;
+        wt.sl_ws = ws;
         // fixed-trip statistics: the deepest window count, and its mean over
         // records under uniform data and midpoint splits (leaf weight
         // 2^-depth: the synthetic generators' volume fractions)

@@ -820,6 +820,7 @@ struct SpecArgs {
   // added to / XOR applied to its swizzled record address)
   uint32_t sl_xmask, sl_leafmin, sl_adv, sl_xor;
   uint32_t sl_wmax;      // SL == 3: window steps every record takes (leaves are sinks)
+  uint32_t sl_ws, sl_wmul;  // entries per window (lanes >= sl_ws read lane 0's); bytes per code unit
   // ring label rows hold raw terminal codes: class = ((code & lab_mask) >>
   // lab_shift) - lab_sub (then the leaf-class table, if any)
   uint32_t lab_mask, lab_shift, lab_sub;
@@ -1102,7 +1103,11 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t NG = 32u / G;
   const uint32_t g = lane / G;
   const uint32_t j = lane & (G - 1);
-  const uint32_t jaddr = (WIN_SHARED ? sbase : 0u) + (CW ? 8u : 16u) * j;
+  // self-loop tables pack sl_ws entries per window (G = 4: the 3 nodes of a
+  // two-level window, 24 B); lanes beyond them read lane 0's entry (a
+  // broadcast, never on a path)
+  const uint32_t jaddr =
+      (WIN_SHARED ? sbase : 0u) + (CW ? 8u : 16u) * ((CW && SL >= 1) ? (j < args.sl_ws ? j : 0u) : j);
   const char* wglob = reinterpret_cast<const char*>(args.win) + 16u * j;
   if constexpr (WIN_SHARED) {  // window table staged
     if (ra.bulk_win) mbar_wait(ticket + 8u, 0);
@@ -1386,14 +1391,17 @@ __global__ void __launch_bounds__(kMaxThreads)
 #pragma unroll
           for (int s = 0; s < KS; ++s) {
             const uint32_t x = __shfl_sync(0xffffffffu, c[s], 0, G) & args.sl_xmask;
-            ad[s] = jaddr + (x << 3);
+            ad[s] = jaddr + x * args.sl_wmul;
             c[s] = x;
           }
-          if (w + 1 == args.sl_wmax && j == 0) {
+          if (w + 1 == args.sl_wmax) {
+            // lane j of the group stores stream j's code: one store per lane
+            uint32_t mine = c[0], mr = rr[0];
 #pragma unroll
-            for (int s = 0; s < KS; ++s)
-              if (rr[s] < rows)
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rr[s]), "r"(c[s]) : "memory");
+            for (int s = 1; s < KS; ++s)
+              if (j == (uint32_t)s) mine = c[s], mr = rr[s];
+            if (j < (uint32_t)KS && mr < rows)
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * mr), "r"(mine) : "memory");
           }
         }
       }
@@ -1411,6 +1419,10 @@ __global__ void __launch_bounds__(kMaxThreads)
       bool aA = rA < rows, aB = rB < rows;
       uint32_t wA = 0, wB = 0;
       uint32_t bA = base_of(aA ? rA : 0u), bB = base_of(aB ? rB : 0u);
+      // lane j of the group collects the code of its stream's j-th record in
+      // a register (no shared-memory store per resolution); stored at the end
+      const uint32_t mA = g + 2u * NG * j, mB = mA + NG;
+      uint32_t kA = 0u, kB = 0u;
       do {
         const uint2 eA = lds_u2(jaddr + wA), eB = lds_u2(jaddr + wB);
         const float vA = lds_f32((eA.y & args.cw_amask) ^ bA), vB = lds_f32((eB.y & args.cw_amask) ^ bB);
@@ -1431,24 +1443,26 @@ __global__ void __launch_bounds__(kMaxThreads)
         const uint32_t xA = __shfl_sync(0xffffffffu, cA, 0, G) & args.sl_xmask;
         const uint32_t xB = __shfl_sync(0xffffffffu, cB, 0, G) & args.sl_xmask;
         if (xA >= args.sl_leafmin) {
-          if (aA && j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rA), "r"(xA) : "memory");
+          if (rA == mA) kA = xA;
           rA += 2 * NG;
           aA = rA < rows;
           wA = 0;
           if (aA) bA = base_of(rA);
         } else {
-          wA = xA << 3;
+          wA = xA * args.sl_wmul;
         }
         if (xB >= args.sl_leafmin) {
-          if (aB && j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rB), "r"(xB) : "memory");
+          if (rB == mB) kB = xB;
           rB += 2 * NG;
           aB = rB < rows;
           wB = 0;
           if (aB) bB = base_of(rB);
         } else {
-          wB = xB << 3;
+          wB = xB * args.sl_wmul;
         }
       } while (__any_sync(0xffffffffu, aA || aB));
+      if (mA < rows) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * mA), "r"(kA) : "memory");
+      if (mB < rows) asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * mB), "r"(kB) : "memory");
     } else if constexpr (SR == 2 && SL == 1) {
       // Two record streams per group, self-loop codes (WinTable::sl_*).  Per
       // window step and stream: entry, feature, compare, one shift selecting
@@ -1476,30 +1490,33 @@ __global__ void __launch_bounds__(kMaxThreads)
       uint32_t dA = rA >= rows ? 1u : 0u, dB = rB >= rows ? 1u : 0u;
       uint32_t bA = base_of(rA < rows ? rA : 0u), bB = base_of(rB < rows ? rB : 0u);
       uint32_t aA = jaddr, aB = jaddr;
-      const uint32_t j0 = j == 0 ? 1u : 0u;
+      // lane j of the group collects the code of its stream's j-th record in
+      // a register (label address myA / myB): no shared-memory store per
+      // resolution; one store per lane at the end of the slot
+      const uint32_t myA = lbuf + 4u * (rA + ng2 * j), myB = myA + 4u * NG;
+      uint32_t kcA = 0u, kcB = 0u;
       // one stream's terminal step (x = masked root code)
-      auto sl_step = [&](uint32_t x, uint32_t& a, uint32_t& b, uint32_t& l, uint32_t& d, uint32_t el) {
+      auto sl_step = [&](uint32_t x, uint32_t& a, uint32_t& b, uint32_t& l, uint32_t& d, uint32_t& kc,
+                         uint32_t el, uint32_t my) {
         asm volatile(
             "{\n\t"
-            ".reg .pred lf, sto, adv, fin;\n\t"
+            ".reg .pred lf, cap, adv, fin;\n\t"
             ".reg .u32 t;\n\t"
-            "setp.ge.u32 lf, %4, %6;\n\t"
-            "setp.ne.and.u32 sto, %7, 0, lf;\n\t"
-            "@sto st.shared.u32 [%2], %4;\n\t"
-            "setp.ne.and.u32 adv, %2, %5, lf;\n\t"
-            "setp.eq.and.u32 fin, %2, %5, lf;\n\t"
-            "@adv add.u32 %2, %2, %8;\n\t"
-            "@adv add.u32 %1, %1, %9;\n\t"
-            "@adv xor.b32 %1, %1, %10;\n\t"
+            "setp.ge.u32 lf, %5, %7;\n\t"
+            "setp.eq.and.u32 cap, %2, %8, lf;\n\t"
+            "@cap mov.u32 %4, %5;\n\t"
+            "setp.ne.and.u32 adv, %2, %6, lf;\n\t"
+            "setp.eq.and.u32 fin, %2, %6, lf;\n\t"
+            "@adv add.u32 %2, %2, %9;\n\t"
+            "@adv add.u32 %1, %1, %10;\n\t"
+            "@adv xor.b32 %1, %1, %11;\n\t"
             "@fin mov.u32 %3, 1;\n\t"
-            "shl.b32 t, %4, 3;\n\t"
-            "add.u32 t, t, %11;\n\t"
-            "selp.u32 %0, %11, t, lf;\n\t"
+            "mad.lo.u32 t, %5, %12, %13;\n\t"
+            "selp.u32 %0, %13, t, lf;\n\t"
             "}"
-            : "=r"(a), "+r"(b), "+r"(l), "+r"(d)
-            : "r"(x), "r"(el), "r"(args.sl_leafmin), "r"(j0), "r"(dl), "r"(args.sl_adv), "r"(args.sl_xor),
-              "r"(jaddr)
-            : "memory");
+            : "=r"(a), "+r"(b), "+r"(l), "+r"(d), "+r"(kc)
+            : "r"(x), "r"(el), "r"(args.sl_leafmin), "r"(my), "r"(dl), "r"(args.sl_adv), "r"(args.sl_xor),
+              "r"(args.sl_wmul), "r"(jaddr));
       };
       do {
         const uint2 eA = lds_u2(aA), eB = lds_u2(aB);
@@ -1520,9 +1537,11 @@ __global__ void __launch_bounds__(kMaxThreads)
         }
         const uint32_t xA = __shfl_sync(0xffffffffu, cA, 0, G) & args.sl_xmask;
         const uint32_t xB = __shfl_sync(0xffffffffu, cB, 0, G) & args.sl_xmask;
-        sl_step(xA, aA, bA, lA, dA, eLA);
-        sl_step(xB, aB, bB, lB, dB, eLB);
+        sl_step(xA, aA, bA, lA, dA, kcA, eLA, myA);
+        sl_step(xB, aB, bB, lB, dB, kcB, eLB, myB);
       } while (__any_sync(0xffffffffu, (dA & dB) == 0u));
+      if (rA + ng2 * j < rows) asm volatile("st.shared.u32 [%0], %1;" ::"r"(myA), "r"(kcA) : "memory");
+      if (rB + ng2 * j < rows) asm volatile("st.shared.u32 [%0], %1;" ::"r"(myB), "r"(kcB) : "memory");
     } else if constexpr (SR == 2 && WIN_SHARED && Rec<A, kTma>::kRowLocal) {
       // Two record streams per group in the lean style (no predication; an
       // exhausted stream re-walks its last record): two independent window

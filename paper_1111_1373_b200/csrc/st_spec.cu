@@ -337,6 +337,8 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
              : balanced ? 3
              : t->info.depth >= lgl + 3 ? 1 : 2;
         rs.sl_wmax = wt->sl_wmax;
+        rs.sl_ws = wt->sl_ws;
+        rs.sl_wmul = 8u * wt->sl_ws / G;  // code units (w << log2 G) -> byte offset of window w
         rs.win = wdev + wt->sl_off;
         rs.n_entries = wt->sl_units;
         rs.win_bytes = round1024((size_t)wt->sl_units * sizeof(SEntry));
