@@ -99,6 +99,18 @@ inline int current_device() {
   return d;
 }
 
+// Table uploads (tree nodes, window tables, forests).  They are read by
+// kernels on the caller's streams, which may be non-blocking: a cudaMemcpy
+// from pageable memory may return before its DMA has landed, and a
+// non-blocking stream does not order behind the legacy stream -- so every
+// upload is enqueued on the legacy stream and that stream is drained
+// (publish) before the device pointer is handed out.
+inline void upload(void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cudaStreamLegacy));
+}
+inline void zero_fill(void* dst, size_t bytes) { CK(cudaMemsetAsync(dst, 0, bytes, cudaStreamLegacy)); }
+inline void publish() { CK(cudaStreamSynchronize(cudaStreamLegacy)); }
+
 struct DevProps {
   int sms = 0;
   size_t smem_optin = 0;
@@ -491,33 +503,30 @@ struct st_tree {
     if (it != dev.end()) return it->second;
     Dev dv;
     CK(cudaMalloc(&dv.wide, nodes.size() * sizeof(st_node)));
-    CK(cudaMemcpy(dv.wide, nodes.data(), nodes.size() * sizeof(st_node), cudaMemcpyHostToDevice));
+    upload(dv.wide, nodes.data(), nodes.size() * sizeof(st_node));
     if (compact_ok) {
       const size_t bytes = ((compact.size() * sizeof(CNode) + 15) & ~size_t(15)) + 16;
       CK(cudaMalloc(&dv.compact, bytes));
-      CK(cudaMemset(dv.compact, 0, bytes));
-      CK(cudaMemcpy(dv.compact, compact.data(), compact.size() * sizeof(CNode),
-                    cudaMemcpyHostToDevice));
+      zero_fill(dv.compact, bytes);
+      upload(dv.compact, compact.data(), compact.size() * sizeof(CNode));
     }
     if (fold_ok) {
       const size_t bytes = ((folded.size() * sizeof(CNode) + 15) & ~size_t(15)) + 16;
       CK(cudaMalloc(&dv.folded, bytes));
-      CK(cudaMemset(dv.folded, 0, bytes));
-      CK(cudaMemcpy(dv.folded, folded.data(), folded.size() * sizeof(CNode), cudaMemcpyHostToDevice));
+      zero_fill(dv.folded, bytes);
+      upload(dv.folded, folded.data(), folded.size() * sizeof(CNode));
     }
-    {
-      std::vector<uint32_t> map;
-      for (uint32_t i = 0; i < nodes.size(); ++i)
-        if (!is_leaf(i)) map.push_back(i);
-      map.push_back(0);  // keep the allocation non-empty
-      CK(cudaMalloc(&dv.internal_map, map.size() * 4));
-      CK(cudaMemcpy(dv.internal_map, map.data(), map.size() * 4, cudaMemcpyHostToDevice));
-    }
+    std::vector<uint32_t> map;  // lives until publish()
+    for (uint32_t i = 0; i < nodes.size(); ++i)
+      if (!is_leaf(i)) map.push_back(i);
+    map.push_back(0);  // keep the allocation non-empty
+    CK(cudaMalloc(&dv.internal_map, map.size() * 4));
+    upload(dv.internal_map, map.data(), map.size() * 4);
     if (leaf_table) {
       CK(cudaMalloc(&dv.leaf_tbl, leaf_classes.size() * 4));
-      CK(cudaMemcpy(dv.leaf_tbl, leaf_classes.data(), leaf_classes.size() * 4,
-                    cudaMemcpyHostToDevice));
+      upload(dv.leaf_tbl, leaf_classes.data(), leaf_classes.size() * 4);
     }
+    publish();
     return dev.emplace(d, dv).first->second;
   }
 
@@ -529,7 +538,8 @@ struct st_tree {
     if (it != dv.wins.end()) return it->second;
     SEntry* p = nullptr;
     CK(cudaMalloc(&p, wt.entries.size() * sizeof(SEntry)));
-    CK(cudaMemcpy(p, wt.entries.data(), wt.entries.size() * sizeof(SEntry), cudaMemcpyHostToDevice));
+    upload(p, wt.entries.data(), wt.entries.size() * sizeof(SEntry));
+    publish();
     dv.wins[key] = p;
     return p;
   }
@@ -571,11 +581,12 @@ struct st_forest {
     const Layout& L = lay[l];
     Dev dv;
     CK(cudaMalloc(&dv.nodes, L.compact.size() * sizeof(CNode) + 16));
-    CK(cudaMemcpy(dv.nodes, L.compact.data(), L.compact.size() * sizeof(CNode), cudaMemcpyHostToDevice));
+    upload(dv.nodes, L.compact.data(), L.compact.size() * sizeof(CNode));
     CK(cudaMalloc(&dv.offsets, L.offsets.size() * 4));
-    CK(cudaMemcpy(dv.offsets, L.offsets.data(), L.offsets.size() * 4, cudaMemcpyHostToDevice));
+    upload(dv.offsets, L.offsets.data(), L.offsets.size() * 4);
     CK(cudaMalloc(&dv.tree_bytes, L.tree_bytes.size() * 4));
-    CK(cudaMemcpy(dv.tree_bytes, L.tree_bytes.data(), L.tree_bytes.size() * 4, cudaMemcpyHostToDevice));
+    upload(dv.tree_bytes, L.tree_bytes.data(), L.tree_bytes.size() * 4);
+    publish();
     return dev.emplace(std::make_pair(d, l), dv).first->second;
   }
 };

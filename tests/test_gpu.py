@@ -340,6 +340,27 @@ def test_host_pipeline_multi_chunk(cuda, co):
         assert st.last_launch_count() >= 2
 
 
+def test_fresh_tree_on_nonblocking_stream(cuda, co):
+    """Tables of a tree used for the first time are complete before the
+    first kernel reads them, on a non-blocking stream (a pageable cudaMemcpy
+    returns before its DMA lands; the fixed-trip window table of the C3 tree
+    is ~100 KB).  Round 2 regression: the first host-pipeline chunk read a
+    half-uploaded table."""
+    nodes = co.gen_tree(12, 2048, 8, 8, 301)
+    x = co.gen_dataset(200_000, 8, 302)
+    want = co.eval_serial(nodes, x)
+    xd = torch.from_numpy(x).cuda()
+    s = torch.cuda.Stream()
+    for i in range(6):
+        for g in (st.GpuGeom(algo="speculative", variant=("spec_fixed",)), st.GpuGeom(algo="data")):
+            tree = st.EncodedTree(nodes)  # fresh device tables every time
+            out = torch.zeros(len(x), dtype=torch.int32, device="cuda")
+            torch.cuda.synchronize()
+            st.eval_device(tree, xd, out, g, stream=s)
+            s.synchronize()
+            assert np.array_equal(out.cpu().numpy().view(np.uint32), want), (i, g.algo)
+
+
 def test_concurrent_callers(cuda, co):
     """Pure-function contract: concurrent host threads
     sharing one tree."""
