@@ -331,7 +331,7 @@ def test_sharded_driver(cuda, co):
 
 
 def test_host_pipeline_multi_chunk(cuda, co):
-    """Host-buffer path with several H2D/kernel/D2H chunks over two streams."""
+    """Host-buffer path with several H2D/kernel/D2H chunks over three streams."""
     nodes = co.gen_tree(12, 2048, 8, 8, 301)
     x = co.gen_dataset(9_000_000, 8, 302)  # 288 MB > one 256 MB chunk
     want = co.eval_serial(nodes, x)
