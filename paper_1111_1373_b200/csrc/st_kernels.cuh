@@ -1225,8 +1225,8 @@ __global__ void __launch_bounds__(kMaxThreads)
             uint32_t c = (v > __uint_as_float(thr)) ? e1.w : e1.z;
 #pragma unroll
             for (int st = 0; st < (STEPS > 0 ? STEPS : 0); ++st) c = __shfl_sync(0xffffffffu, c, c, G);
-            const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
-            if (j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(la), "r"(root) : "memory");
+            // group lane 0 holds the root's contracted code: no broadcast
+            if (j == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(la), "r"(c) : "memory");
           }
         } else {
 #pragma unroll 4
@@ -1235,9 +1235,8 @@ __global__ void __launch_bounds__(kMaxThreads)
             uint32_t c = (v > __uint_as_float(thr)) ? e1.w : e1.z;
 #pragma unroll
             for (int st = 0; st < (STEPS > 0 ? STEPS : 0); ++st) c = __shfl_sync(0xffffffffu, c, c, G);
-            const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
             if (j == 0 && r < rows)
-              asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(root) : "memory");
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(c) : "memory");
           }
         }
       } else if (args.pm_off) {
@@ -1288,9 +1287,8 @@ __global__ void __launch_bounds__(kMaxThreads)
               c = (c < 32u) ? u : c;
             }
           }
-          const uint32_t root = __shfl_sync(0xffffffffu, c, 0, G);
-          if (j == 0 && r < rows)
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(root) : "memory");
+          if (j == 0 && r < rows)  // group lane 0 holds the root's code
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * r), "r"(c) : "memory");
         }
       }
     } else if constexpr (SR == 1) {

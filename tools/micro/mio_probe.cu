@@ -67,6 +67,17 @@ __global__ void __launch_bounds__(1024) probe(uint32_t* out, uint32_t salt, uint
         else
           asm volatile("redux.sync.or.b32 %0, %1, 0xffffffff;" : "=r"(v) : "r"((acc & 1u) << lane) : "memory");
         acc ^= a + v;
+      } else if (MODE == 12 || MODE == 13 || MODE == 14 || MODE == 15) {
+        uint32_t v;
+        if (MODE == 12)  // full-width idx, computed source lane
+          asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(v) : "r"(acc + u), "r"((lane & ~3u) | ((lane + u + addr) & 3u)) : "memory");
+        else if (MODE == 13)
+          asm volatile("shfl.sync.bfly.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(v) : "r"(acc + u), "r"((u + addr) & 31u) : "memory");
+        else if (MODE == 14)  // width 4 but uniform source index
+          asm volatile("shfl.sync.idx.b32 %0, %1, 0, 0x1c1f, 0xffffffff;" : "=r"(v) : "r"(acc + u + addr) : "memory");
+        else  // full-width idx, all lanes read lane 0
+          asm volatile("shfl.sync.idx.b32 %0, %1, 0, 0x1f, 0xffffffff;" : "=r"(v) : "r"(acc + u + addr) : "memory");
+        acc ^= v;
       } else if (MODE == 5) {
         { uint32_t v; asm volatile("{.reg .pred p; setp.ne.u32 p, %1, 0; vote.sync.ballot.b32 %0, p, 0xffffffff;}" : "=r"(v) : "r"(acc & (1u << u)) : "memory"); acc += v; }
       }
@@ -103,9 +114,11 @@ int main() {
   const char* names[] = {"LDS.128 bcast 8 chunks", "LDS.64 256B contiguous", "LDS.32 128B contiguous",
                          "LDS.32 bcast 8 words", "SHFL.IDX w4", "VOTE.BALLOT", "LDS.128 bcast 2-way quad",
                          "LDS.64 (same as 1)", "LDS.64 bcast 8 words", "LDS.32 + VOTE (pair)", "LDS.32 + SHFL (pair)",
-                         "LDS.32 + REDUX.OR (pair)"};
-  float r[12] = {run<0>(sms), run<1>(sms), run<2>(sms), run<3>(sms), run<4>(sms), run<5>(sms),
-                 run<6>(sms), run<7>(sms), run<8>(sms), run<9>(sms), run<10>(sms), run<11>(sms)};
-  for (int i = 0; i < 12; ++i) printf("%-28s %.3f SM-cycles per warp-instruction (at max clock)\n", names[i], r[i]);
+                         "LDS.32 + REDUX.OR (pair)", "SHFL.IDX w32 computed src", "SHFL.BFLY", "SHFL.IDX w4 src 0",
+                         "SHFL.IDX w32 src 0"};
+  float r[16] = {run<0>(sms), run<1>(sms), run<2>(sms), run<3>(sms), run<4>(sms), run<5>(sms),
+                 run<6>(sms), run<7>(sms), run<8>(sms), run<9>(sms), run<10>(sms), run<11>(sms),
+                 run<12>(sms), run<13>(sms), run<14>(sms), run<15>(sms)};
+  for (int i = 0; i < 16; ++i) printf("%-28s %.3f SM-cycles per warp-instruction (at max clock)\n", names[i], r[i]);
   return 0;
 }
