@@ -44,6 +44,29 @@ __global__ void __launch_bounds__(512) k_read_label(const float4* __restrict__ x
   }
 }
 
+// the read of k_read_v4 plus the label stream of a tree walk: 4 bytes written
+// per 64-byte record (thread i of a warp covers float4 i; every 4th lane
+// stores), writes coalesced per warp
+__global__ void __launch_bounds__(512) k_read_v4_labels(const float4* __restrict__ x, size_t n4, uint32_t* out) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n4; i += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(v[k].x), "=f"(v[k].y), "=f"(v[k].z), "=f"(v[k].w)
+                   : "l"(x + i + k * stride));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t a = __float_as_uint(v[k].x) ^ __float_as_uint(v[k].w);
+      a ^= __shfl_xor_sync(0xffffffffu, a, 1);
+      a ^= __shfl_xor_sync(0xffffffffu, a, 2);
+      if ((threadIdx.x & 3) == 0) out[(i + k * stride) >> 2] = a;
+    }
+  }
+}
+
 extern "C" int read_floor(const void* x, size_t bytes, uint32_t* out, int mode, int blocks_per_sm, void* stream) {
   int sms = 0, dev = 0;
   cudaGetDevice(&dev);
@@ -51,6 +74,7 @@ extern "C" int read_floor(const void* x, size_t bytes, uint32_t* out, int mode, 
   const size_t n4 = bytes / 16;
   auto s = static_cast<cudaStream_t>(stream);
   if (mode == 0) k_read_v4<<<sms * blocks_per_sm, 512, 0, s>>>(static_cast<const float4*>(x), n4, out);
+  else if (mode == 2) k_read_v4_labels<<<sms * blocks_per_sm, 512, 0, s>>>(static_cast<const float4*>(x), n4, out);
   else k_read_label<<<sms * blocks_per_sm, 512, 0, s>>>(static_cast<const float4*>(x), n4, out);
   return (int)cudaGetLastError();
 }

@@ -24,6 +24,19 @@ METRICS = {
     "launch__occupancy_limit_shared_mem": "occupancy_limit_smem_blocks",
     "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
     "lts__t_bytes.sum": "l2_bytes",
+    # shared-memory (MIO) pipe: the binding resource of the tree walks
+    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed": "l1tex_lsu_wavefronts_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_wavefronts_pct",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum": "smem_ld_wavefronts",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum": "smem_ld_bank_conflicts",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active": "lsu_pipe_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio": "stall_short_scoreboard",
+    "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio": "stall_long_scoreboard",
+    "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio": "stall_wait",
+    "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio": "stall_mio_throttle",
+    "sm__cycles_elapsed.avg": "sm_cycles",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "nsecond": 1e-9,
         "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1, "second": 1,
@@ -53,6 +66,12 @@ def main():
                 d["algorithmic_bytes"] = algo_bytes
                 d["traffic_over_algorithmic"] = d["dram_bytes_per_launch"] / algo_bytes
                 d["achieved_GBs_under_ncu"] = algo_bytes / d["duration"] / 1e9
+        if "smem_wavefronts" in d and d.get("sm_cycles"):
+            # shared-memory wavefronts per SM-cycle (the pipe retires <= 1 per cycle)
+            sms = 148.0
+            d["shared_wavefronts_per_clk_per_sm"] = d["smem_wavefronts"] / (d["sm_cycles"] * sms)
+            if "smem_ld_bank_conflicts" in d and d.get("smem_ld_wavefronts"):
+                d["shared_conflict_fraction"] = d["smem_ld_bank_conflicts"] / d["smem_ld_wavefronts"]
         res["kernels"].append(d)
     k0 = res["kernels"][0]
     res.update({k: k0[k] for k in ("dram_bytes_per_launch", "duration") if k in k0})

@@ -46,6 +46,7 @@ def main():
             "read_v4_2b": rfl(0, 2),
             "read_v4_8b": rfl(0, 8),
             "read_label_4b": rfl(1, 4),
+            "read_v4_labels_4b": rfl(2, 4),
             "data_stump": lambda: st.eval_device(stump, x, out, st.GpuGeom(algo="data")),
             "data": lambda: st.eval_device(tree, x, out, st.GpuGeom(algo="data")),
             "speculative": lambda: st.eval_device(tree, x, out, st.GpuGeom(algo="speculative")),
