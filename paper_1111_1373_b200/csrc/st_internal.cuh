@@ -398,7 +398,9 @@ struct st_tree {
       uint32_t ws = 1;
       for (uint32_t w = 0; w < nw; ++w) ws = std::max<uint32_t>(ws, (uint32_t)members[w].size());
       if ((8u * ws) % G != 0) ws = G;
-      if (G <= 32 && (1u << lg) == G && ncodes <= 64 && abits + 2 * cbits2 <= 32 && units * G < (1u << 24)) {
+      // (codes fit 16 bits: the kernels broadcast two streams' codes in one word)
+      if (G <= 32 && (1u << lg) == G && ncodes <= 64 && abits + 2 * cbits2 <= 32 && cbits2 <= 16 &&
+          units * G < (1u << 24)) {
         std::vector<uint2> slt((size_t)units * ws + 64, make_uint2(0u, 0u));
         for (uint32_t w = 0; w < nw; ++w) {
           const auto& mem = members[w];

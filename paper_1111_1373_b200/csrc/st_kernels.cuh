@@ -146,6 +146,16 @@ __device__ __forceinline__ uint32_t swz(uint32_t byte_off) {
   return byte_off ^ ((byte_off >> 3) & 0x70u);
 }
 
+// Low halves of two codes in one word (PRMT): self-loop codes are < 2^16
+// (WinTable::sl_cbits <= 15), so one root broadcast serves two record
+// streams -- a shuffle costs ~1.8 shared-pipe cycles per warp instruction
+// (profiles/r2_mio_probe.txt), two integer ops cost none of it.
+__device__ __forceinline__ uint32_t pack_lo16(uint32_t lo, uint32_t hi) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // Per-record feature accessor over a staged tile (or global for kDirect).
 // get(attr4) takes the attribute as a byte offset (4 * attribute).
@@ -1387,10 +1397,13 @@ __global__ void __launch_bounds__(kMaxThreads)
               for (int s = 0; s < KS; ++s) c[s] = __shfl_sync(0xffffffffu, c[s], c[s], G);
           }
 #pragma unroll
-          for (int s = 0; s < KS; ++s) {
-            const uint32_t x = __shfl_sync(0xffffffffu, c[s], 0, G) & args.sl_xmask;
-            ad[s] = jaddr + x * args.sl_wmul;
-            c[s] = x;
+          for (int s = 0; s < KS; s += 2) {  // one root broadcast per two streams
+            const uint32_t v = __shfl_sync(0xffffffffu, pack_lo16(c[s], c[s + 1]), 0, G);
+            const uint32_t x0 = v & args.sl_xmask, x1 = (v >> 16) & args.sl_xmask;
+            ad[s] = jaddr + x0 * args.sl_wmul;
+            ad[s + 1] = jaddr + x1 * args.sl_wmul;
+            c[s] = x0;
+            c[s + 1] = x1;
           }
           if (w + 1 == args.sl_wmax) {
             // lane j of the group stores stream j's code: one store per lane
@@ -1438,8 +1451,8 @@ __global__ void __launch_bounds__(kMaxThreads)
             cB = __shfl_sync(0xffffffffu, cB, cB, G);
           }
         }
-        const uint32_t xA = __shfl_sync(0xffffffffu, cA, 0, G) & args.sl_xmask;
-        const uint32_t xB = __shfl_sync(0xffffffffu, cB, 0, G) & args.sl_xmask;
+        const uint32_t vAB = __shfl_sync(0xffffffffu, pack_lo16(cA, cB), 0, G);  // both roots, one shuffle
+        const uint32_t xA = vAB & args.sl_xmask, xB = (vAB >> 16) & args.sl_xmask;
         if (xA >= args.sl_leafmin) {
           if (rA == mA) kA = xA;
           rA += 2 * NG;
@@ -1533,8 +1546,8 @@ __global__ void __launch_bounds__(kMaxThreads)
             cB = __shfl_sync(0xffffffffu, cB, cB, G);
           }
         }
-        const uint32_t xA = __shfl_sync(0xffffffffu, cA, 0, G) & args.sl_xmask;
-        const uint32_t xB = __shfl_sync(0xffffffffu, cB, 0, G) & args.sl_xmask;
+        const uint32_t vAB = __shfl_sync(0xffffffffu, pack_lo16(cA, cB), 0, G);  // both roots, one shuffle
+        const uint32_t xA = vAB & args.sl_xmask, xB = (vAB >> 16) & args.sl_xmask;
         sl_step(xA, aA, bA, lA, dA, kcA, eLA, myA);
         sl_step(xB, aB, bB, lB, dB, kcB, eLB, myB);
       } while (__any_sync(0xffffffffu, (dA & dB) == 0u));
