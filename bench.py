@@ -234,6 +234,31 @@ def ncu_traffic(workload, algo):
     return None, None
 
 
+def ncu_pipes(workload, algo):
+    """Shared-memory (MIO) pipe and issue utilisation of this kernel and
+    workload from the newest committed ncu summary: the tree walks that do
+    not reach the HBM roofline are bound there."""
+    import glob
+    import re
+
+    files = glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_{workload}_{algo}.json"))
+    files.sort(key=lambda f: int(re.search(r"/r(\d+)_ncu_", f).group(1)))
+    for p in reversed(files):
+        try:
+            k = json.load(open(p))["kernels"][0]
+            if "l1tex_lsu_wavefronts_pct" not in k:
+                continue
+            return {"bound": "smem pipe (l1tex LSU wavefronts) / issue",
+                    "l1tex_lsu_wavefronts_pct": k["l1tex_lsu_wavefronts_pct"],
+                    "shared_wavefronts_per_clk_per_sm": k.get("shared_wavefronts_per_clk_per_sm"),
+                    "shared_conflict_fraction": k.get("shared_conflict_fraction"),
+                    "alu_pipe_pct": k.get("alu_pipe_pct"), "issue_active_pct": k.get("issue_active_pct"),
+                    "source": os.path.relpath(p, ROOT) + " (ncu --set full of the same kernel and workload)"}
+        except Exception:
+            continue
+    return None
+
+
 class Dist:
     """Process-group plumbing for N > 1 (barrier, max over ranks, gather);
     every call is a no-op at N = 1."""
@@ -402,6 +427,10 @@ def run_ours(args):
         "ballot + leaf path masks over one window (every internal node's predicate in one vote)"
         if one_window else "warp-shuffle pointer jumping inside G-lane windows")
     by_algo["speculative_over_data_time"] = by_algo["speculative"]["ms_per_step"] / by_algo["data"]["ms_per_step"]
+    for name in ("data", "speculative"):
+        pipes = ncu_pipes(args.workload, name)
+        if pipes:
+            by_algo[name]["pipes"] = pipes
 
     # e2e through the public host API on every rank at once: pinned host
     # records -> labels on host
@@ -627,6 +656,10 @@ def run_c5(args):
         row["d_mu"] = float(sum(sums)) / m
         del dep, dv
         row["speculative_over_data_time"] = row["speculative"]["ms_per_step"] / row["data"]["ms_per_step"]
+        for algo in ("data", "speculative"):  # ncu of one shard at this depth, where captured
+            pipes = ncu_pipes(f"C5d{D}", algo)
+            if pipes:
+                row[algo]["pipes"] = pipes
         by_depth[f"d{D}"] = row
     tm, tl, launches, steps, (c0, c1), algo, D = main
     clocks = sampler.summary(c0, c1)

@@ -77,7 +77,8 @@ uint32_t choose_S(uint32_t a, uint32_t want, bool small) {
   // where a tile is small -- C3 (a = 8): S = 4 0.63 ms vs S = 2 0.67 ms for 32
   // frames; C2 (a = 32): S = 2 0.307 vs S = 1 0.321 ms (profiles/r1_sweep_*);
   // C5 (a = 16, one stage per warp): S = 4 vs 1: d12 -7 %, d16 -16 %, d20
-  // -10 %, d8 even (profiles/r1_ab_stages.txt).  Small inputs (C1) keep S = 1.
+  // -10 %, d8 even (profiles/r1_ab_stages.txt).  Small inputs keep S = 1
+  // (C1 with a shared tree: S = 2, eval_data_device).
   if (want == 0) want = a <= 8 ? 4 : a == 32 ? 2 : (a == 16 && !small) ? 4 : 1;
   uint32_t S = 1;
   while (S * 2 <= std::min(want, maxS)) S *= 2;
@@ -172,7 +173,14 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // shared trees are rebased to absolute shared addresses inside the compact
   // child field: the largest address must fit below the leaf bit
   if (tloc == ST_TREE_SHARED && ((uint64_t)pr.smem_optin << t->abits) >= (1ull << 31)) tloc = ST_TREE_GLOBAL;
-  const uint32_t S0 = ct_arity(a) ? choose_S(a, g.samples_per_thread, small) : 1;
+  uint32_t S0 = ct_arity(a) ? choose_S(a, g.samples_per_thread, small) : 1;
+  // small 16-attribute inputs walking a shared tree (C1): S = 2 with one
+  // stage per warp, 15.6 vs 15.9-16.6 us for S = 1 with one or two stages
+  // (profiles/r2_small_sweep_C1.json)
+  const bool small16 = !g.samples_per_thread && a == 16 && small && tloc == ST_TREE_SHARED &&
+                       g.tree_loc != ST_TREE_GLOBAL && g.tree_loc != ST_TREE_CONSTANT &&
+                       tma_ok(x, m, a, ld, layout, 2);
+  if (small16) S0 = 2;
   // Records walked from registers release their tile before the walk, so one
   // stage per warp already double-buffers (next TMA in flight during the
   // walk) and the saved shared memory buys twice the warps (C3 x 32 frames:
@@ -181,9 +189,9 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
   // smem it frees holds S-record tiles for as many warps, and the S chains
   // per lane hide the tree latency better than a second tile in flight
   // (same-box A/B, profiles/r1_ab_stages.txt: C2 -1.9 %, C5 d16 -16 %).
-  // Small inputs are ramp-up bound and keep two (C1: 17.3 vs 17.8 us).
+  // Small inputs keep two, except 16-attribute records at S = 2 (above).
   const uint32_t want_ns =
-      g.stages ? g.stages : ((d.record_regs == 1 || !small) && tloc == ST_TREE_SHARED ? 1u : 0u);
+      g.stages ? g.stages : ((d.record_regs == 1 || !small || small16) && tloc == ST_TREE_SHARED ? 1u : 0u);
   Staging stg = plan_staging(x, m, a, ld, layout, S0, want_ns,
                              tloc == ST_TREE_SHARED ? tree_bytes : 0, pr);
   if (tloc == ST_TREE_SHARED && tree_bytes + 1024 + stg.tile_smem() > pr.smem_optin) {
