@@ -114,7 +114,9 @@ enum st_variant {
                                of self-loop terminal codes */
   ST_VAR_SPEC_PRED = 64u,   /* speculative, self-loop two-stream loop: predicated stream advance */
   ST_VAR_SPEC_BRANCH = 128u,/* ... the stream advance in a divergent branch (default: by tree shape) */
-  ST_VAR_SPEC_FIXED = 256u  /* ... every record runs the deepest window count, leaves absorbing */
+  ST_VAR_SPEC_FIXED = 256u, /* ... every record runs the deepest window count, leaves absorbing */
+  ST_VAR_SPEC_QUAD = 512u   /* ... fixed-trip loop on 4-lane groups (8 records per warp step) instead of
+                               interleaved lane triples (10) */
 };
 
 /* Optional per-record speculative counters (SpeculativeStats,

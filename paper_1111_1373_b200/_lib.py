@@ -64,6 +64,7 @@ ST_VAR_SPEC_SELECT = 32
 ST_VAR_SPEC_PRED = 64
 ST_VAR_SPEC_BRANCH = 128
 ST_VAR_SPEC_FIXED = 256
+ST_VAR_SPEC_QUAD = 512
 
 
 class st_stats(C.Structure):

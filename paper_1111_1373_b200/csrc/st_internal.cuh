@@ -810,10 +810,11 @@ inline bool tma_ok(const float* x, uint64_t m, uint32_t a, uint64_t ld, int layo
   return encode_tiled() != nullptr;
 }
 
-inline void make_tmap(Staging& st, const float* x, uint64_t m, uint32_t a) {
+// box rows = one tile of 32*S records, or `records` (a multiple of 32 / a)
+inline void make_tmap(Staging& st, const float* x, uint64_t m, uint32_t a, uint32_t records = 0) {
   const cuuint64_t dims[2] = {32, (cuuint64_t)(m * (uint64_t)a / 32)};
   const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {32, 32u * st.S * a / 32u};
+  const cuuint32_t box[2] = {32, (records ? records : 32u * st.S) * a / 32u};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_tiled()(&st.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(x),
                               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

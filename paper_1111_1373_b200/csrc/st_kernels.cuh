@@ -39,6 +39,7 @@ constexpr uint32_t kPairBit = 0x40000000u;
 constexpr uint32_t kNoClass = 0xFFFFFFFFu;
 constexpr int kWarpsPerCta = 8;    // default CTA width (warps); launches may use up to 32
 constexpr int kMaxThreads = 1024;
+constexpr int kTripleSlot = 80;   // records per ring slot of the lane-triple speculative loop
 
 // Compact 8-byte device node.  internal: meta = (8*child) << abits | 4*attr
 // (bit 31 clear; byte offsets so the walk does no scaling); leaf: meta =
@@ -1011,7 +1012,7 @@ struct SpecRingArgs {
   uint32_t n_slots;       // NS
   uint32_t ns_magic;      // floor(2^32 / NS): ticket -> (generation, slot) without a division
   uint32_t bulk_win;      // stage the window table with one cp.async.bulk (else per-thread loads)
-  uint32_t tile_mult;     // host: records per ring slot / 32 (the kernel's RT)
+  uint32_t tile_mult;     // host: records per ring slot / 32 (the kernel's RT); 0 = lane triples (kTripleSlot)
 };
 
 // RT: records per ring slot / 32.  Two-stream groups over 64-record slots
@@ -1025,16 +1026,24 @@ struct SpecRingArgs {
 // a fixed sl_wmax window steps with leaves as absorbing sink windows -- no
 // per-step test at all (balanced trees, where records' window counts barely
 // differ).
-template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false, int RT = 1, int SL = 0>
+// L3: interleaved lane triples (fixed-trip loop, G = 4 self-loop tables of
+// three-node windows): lanes 3g .. 3g + 2 hold window lanes 0..2 of record
+// group g < 10, so a warp instruction carries 10 records instead of 8 (the
+// fourth lane of a 4-lane group only ever mirrors lane 0); a doubling step's
+// source lane is 3g + (code & 3).  Lanes 30 / 31 mirror lanes 27 / 28 (same
+// addresses: broadcasts, no extra wavefronts).  80-record ring slots (8 per
+// group).
+template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false, int RT = 1, int SL = 0, int L3 = 0>
 __global__ void __launch_bounds__(kMaxThreads)
     k_spec_ring(const SpecRingArgs ra, const __grid_constant__ CUtensorMap tmap) {
   static_assert(!CW || (WIN_SHARED && SR >= 1), "8-byte windows: shared table, window-loop paths");
   static_assert(!SL || SR == 0 || (SR == 2 && CW), "self-loop codes: one window, or two 8-byte-window streams");
   static_assert(SL < 2 || SR == 2, "branchy / fixed-trip stream loops: two-stream layout");
   static_assert(RT == 1 || SR == 2, "multi-chunk slots: two-stream loop only");
+  static_assert(!L3 || (SL == 3 && RT == 1), "lane triples: fixed-trip loop, 80-record slots");
   extern __shared__ __align__(1024) unsigned char smem[];
   const SpecArgs& args = ra.s;
-  constexpr int R = 32 * RT;
+  constexpr int R = L3 ? kTripleSlot : 32 * RT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t NS = ra.n_slots;
   const uint32_t sbase = align1024(smem_u32(smem));
@@ -1110,9 +1119,9 @@ __global__ void __launch_bounds__(kMaxThreads)
   }
 
   const uint32_t G = args.G;
-  const uint32_t NG = 32u / G;
-  const uint32_t g = lane / G;
-  const uint32_t j = lane & (G - 1);
+  const uint32_t NG = L3 ? 10u : 32u / G;
+  const uint32_t g = L3 ? (lane < 30 ? (uint32_t)lane / 3u : 9u) : lane / G;
+  const uint32_t j = L3 ? (lane < 30 ? (uint32_t)lane - 3u * g : (uint32_t)lane - 30u) : lane & (G - 1);
   // self-loop tables pack sl_ws entries per window (G = 4: the 3 nodes of a
   // two-level window, 24 B); lanes beyond them read lane 0's entry (a
   // broadcast, never on a path)
@@ -1198,7 +1207,7 @@ __global__ void __launch_bounds__(kMaxThreads)
     mbar_wait(full0 + 8u * b, gen & 1u);
     if (args.root_code & kLeafBit) {  // N == 1
 #pragma unroll
-      for (int k = 0; k < RT; ++k)
+      for (int k = 0; k < (R + 31) / 32; ++k)
         if (lane + 32u * k < rows)
           asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * (lane + 32u * k)), "r"(args.root_code)
                        : "memory");
@@ -1370,50 +1379,64 @@ __global__ void __launch_bounds__(kMaxThreads)
         return (tile + rowb) | (((rowb >> 3) & 0x70u) ^ (ra4 & 127u));
       };
       const uint32_t per_group = R / NG;  // records of this group in the slot
+      const uint32_t g3 = 3u * g;         // L3: the group's lane 0
+      // every stream starts in the root window: its entry lives in registers
+      const uint2 e_root = lds_u2(jaddr);
       for (uint32_t k0 = 0; k0 < per_group; k0 += KS) {
-        uint32_t rr[KS], bx[KS], ad[KS];
+        uint32_t rr[KS], bx[KS], ad[KS], c[KS];
 #pragma unroll
         for (int s = 0; s < KS; ++s) {
           rr[s] = g + NG * (k0 + s);
           bx[s] = base_of(rr[s] < rows ? rr[s] : 0u);  // rows past a partial tile walk record 0
-          ad[s] = jaddr;
         }
-        for (uint32_t w = 0; w < args.sl_wmax; ++w) {
-          uint32_t c[KS];
+        auto step = [&](const bool first) {
 #pragma unroll
           for (int s = 0; s < KS; ++s) {
-            const uint2 e = lds_u2(ad[s]);
+            const uint2 e = first ? e_root : lds_u2(ad[s]);
             const float v = lds_f32((e.y & args.cw_amask) ^ bx[s]);
             c[s] = e.y >> (v > __uint_as_float(e.x) ? args.cw_rsh : args.cw_lsh);
           }
+          // one pointer-jumping step: width-G segments, or (L3) source lane
+          // 3g + the code's lane bits
+          auto jump = [&](uint32_t cc) -> uint32_t {
+            if constexpr (L3) return __shfl_sync(0xffffffffu, cc, g3 + (cc & 3u));
+            else return __shfl_sync(0xffffffffu, cc, cc, G);
+          };
           if constexpr (STEPS >= 0) {
 #pragma unroll
             for (int st = 0; st < STEPS; ++st)
 #pragma unroll
-              for (int s = 0; s < KS; ++s) c[s] = __shfl_sync(0xffffffffu, c[s], c[s], G);
+              for (int s = 0; s < KS; ++s) c[s] = jump(c[s]);
           } else {
             for (uint32_t st = 0; st < args.smax; ++st)
 #pragma unroll
-              for (int s = 0; s < KS; ++s) c[s] = __shfl_sync(0xffffffffu, c[s], c[s], G);
+              for (int s = 0; s < KS; ++s) c[s] = jump(c[s]);
           }
 #pragma unroll
           for (int s = 0; s < KS; s += 2) {  // one root broadcast per two streams
-            const uint32_t v = __shfl_sync(0xffffffffu, pack_lo16(c[s], c[s + 1]), 0, G);
+            const uint32_t v = L3 ? __shfl_sync(0xffffffffu, pack_lo16(c[s], c[s + 1]), g3)
+                                  : __shfl_sync(0xffffffffu, pack_lo16(c[s], c[s + 1]), 0, G);
             const uint32_t x0 = v & args.sl_xmask, x1 = (v >> 16) & args.sl_xmask;
             ad[s] = jaddr + x0 * args.sl_wmul;
             ad[s + 1] = jaddr + x1 * args.sl_wmul;
             c[s] = x0;
             c[s + 1] = x1;
           }
-          if (w + 1 == args.sl_wmax) {
-            // lane j of the group stores stream j's code: one store per lane
-            uint32_t mine = c[0], mr = rr[0];
+        };
+        step(true);
+        for (uint32_t w = 1; w < args.sl_wmax; ++w) step(false);
+        // lane j of the group stores stream j's code: one store per lane
+        // (L3: three lanes, lane 0 also stores stream 3; mirror lanes none)
+        uint32_t mine = c[0], mr = rr[0];
 #pragma unroll
-            for (int s = 1; s < KS; ++s)
-              if (j == (uint32_t)s) mine = c[s], mr = rr[s];
-            if (j < (uint32_t)KS && mr < rows)
-              asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * mr), "r"(mine) : "memory");
-          }
+        for (int s = 1; s < KS; ++s)
+          if (j == (uint32_t)s) mine = c[s], mr = rr[s];
+        const bool st_ok = L3 ? lane < 30 : j < (uint32_t)KS;
+        if (st_ok && mr < rows)
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * mr), "r"(mine) : "memory");
+        if constexpr (L3) {
+          if (lane < 30 && j == 0u && rr[3] < rows)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rr[3]), "r"(c[3]) : "memory");
         }
       }
     } else if constexpr (SR == 2 && SL == 2) {
@@ -1615,7 +1638,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(gen + 1u) : "memory");
     }
 #pragma unroll
-    for (int k = 0; k < RT; ++k) {
+    for (int k = 0; k < (R + 31) / 32; ++k) {
       const uint32_t rr = lane + 32u * k;
       if (rr < rows) {
         uint32_t code;

@@ -31,11 +31,12 @@ void launch_spec_steps(const SpecArgs& sa, const Staging& stg, size_t smem, int 
   }
 }
 
-template <int A, bool WS, int STEPS, int SR, bool CW = false, int RT = 1, int SL = 0>
+template <int A, bool WS, int STEPS, int SR, bool CW = false, int RT = 1, int SL = 0, int L3 = 0>
 void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
                         uint32_t warps, cudaStream_t s) {
-  auto fn = k_spec_ring<A, WS, STEPS, SR, CW, RT, SL>;
-  const uint64_t n_tiles = (ra.s.p.m + 32 * RT - 1) / (32 * RT);
+  auto fn = k_spec_ring<A, WS, STEPS, SR, CW, RT, SL, L3>;
+  constexpr uint64_t R = L3 ? kTripleSlot : 32 * RT;
+  const uint64_t n_tiles = (ra.s.p.m + R - 1) / R;
   const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles * warps, warps);
   clear_stale_error();
   fn<<<blocks, warps * 32, smem, s>>>(ra, stg.tmap);
@@ -53,6 +54,8 @@ void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg
         return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 1>(ra, stg, smem, dev, warps, s);
       }
       if (sl == 3 && sr >= 2) {  // self-loop codes, fixed trip count
+        if (ra.tile_mult == 0)  // lane triples, 80-record slots
+          return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 3, 1>(ra, stg, smem, dev, warps, s);
         if (ra.tile_mult == 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 2, 3>(ra, stg, smem, dev, warps, s);
         return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 3>(ra, stg, smem, dev, warps, s);
       }
@@ -373,7 +376,21 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       Staging s2 = plan_staging(x, m, a, ld, layout, 2, g.stages, rs.win_bytes, pr);
       if (s2.loader == kTma && s2.S == 2) rt = 2, rstg = s2;
     }
-    const size_t lb = 32 + 32 * 128 * rt;  // generation padding + ticket + per-warp label rows (<= 32 warps)
+    // Lane triples (fixed-trip loop over G = 4 three-node windows): 10
+    // record groups per warp instead of 8, 80-record slots -- C1 / C3 / C5
+    // d8..d14 -8 / -10 / -9 % (same-box A/B); ST_VAR_SPEC_QUAD keeps the
+    // 4-lane groups.
+    if (sl == 3 && !(g.variant & ST_VAR_SPEC_QUAD) && G == 4 && wt->sl_ws == 3 && m >= kTripleSlot &&
+        (a == 8 || a == 16 || a == 32) && tma_ok(x, m, a, ld, layout, 1)) {
+      Staging s3 = stg;
+      s3.S = 1;
+      s3.stage_bytes = round1024((uint64_t)kTripleSlot * a * 4);
+      make_tmap(s3, x, m, a, kTripleSlot);
+      rstg = s3;
+      rt = 0;
+    }
+    const size_t slot_recs = rt ? 32u * rt : (size_t)kTripleSlot;
+    const size_t lb = 32 + 32 * 4 * slot_recs;  // generation padding + ticket + per-warp label rows (<= 32 warps)
     const size_t budget = pr.smem_optin - 1024 - rs.win_bytes - lb;
     const size_t max_slots = budget / (rstg.stage_bytes + 16u);
     const uint32_t warps = (uint32_t)std::min<size_t>(32, max_slots > 12 ? max_slots - 12 : 0);
@@ -388,7 +405,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       ra.tile_mult = rt;
       ra.s.stage_bytes = rstg.stage_bytes;
       const size_t rsmem = 1024 + rs.win_bytes + (size_t)ra.n_slots * (rstg.stage_bytes + 8u) +
-                           (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 128 * rt;
+                           (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 4 * slot_recs;
       // one window: ballot + leaf path masks unless pointer jumping is asked
       // for (pm_off then names the self-loop entries, or 0: select per step)
       if (onewin) ra.s.pm_off = (g.variant & ST_VAR_SPEC_JUMP) ? (sl ? wt->sl1_off : 0u) : wt->pm_off;

@@ -41,7 +41,7 @@ VARIANTS = {"no_fold": _lib.ST_VAR_NO_FOLD, "tree_loop": _lib.ST_VAR_TREE_LOOP,
             "spec_general": _lib.ST_VAR_SPEC_GENERAL, "spec_jump": _lib.ST_VAR_SPEC_JUMP,
             "spec_wide": _lib.ST_VAR_SPEC_WIDE, "spec_select": _lib.ST_VAR_SPEC_SELECT,
             "spec_pred": _lib.ST_VAR_SPEC_PRED, "spec_branch": _lib.ST_VAR_SPEC_BRANCH,
-            "spec_fixed": _lib.ST_VAR_SPEC_FIXED}
+            "spec_fixed": _lib.ST_VAR_SPEC_FIXED, "spec_quad": _lib.ST_VAR_SPEC_QUAD}
 
 
 def _check(rc: int) -> None:

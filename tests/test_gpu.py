@@ -49,6 +49,7 @@ def test_appendix_a_labels(cuda, co, name):
     tree = st.EncodedTree(nodes)
     xd = torch.from_numpy(x).to(cuda)
     geoms = ALL_GEOMS if name in ("paper", "C1", "C2", "C3") else [DATA_GEOMS[0], SPEC_GEOMS[0]]
+    geoms = geoms + [st.GpuGeom(algo="speculative", variant=("spec_fixed", "spec_quad"))]
     for g in geoms:
         got = _dev_eval(tree, xd, g, len(x))
         assert co.fnv1a(got) == lab_fnv, f"{name} {g}"
@@ -473,7 +474,7 @@ def test_single_window_speculation(cuda, co, mode):
 
 
 @pytest.mark.parametrize("wide", [(), ("spec_wide",), ("spec_select",), ("spec_pred",), ("spec_branch",),
-                                  ("spec_fixed",)])
+                                  ("spec_fixed",), ("spec_fixed", "spec_quad")])
 def test_spec_window_formats(cuda, co, wide):
     """The ring kernel's window formats: 8-byte entries with self-loop codes
     (default; stream advance predicated or branchy by tree shape, and both
@@ -560,5 +561,6 @@ def test_spec_ring_slot_sizes(cuda, co, tile):
                       st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_pred",)),
                       st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_branch",)),
                       st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_fixed",)),
+                      st.GpuGeom(algo="speculative", variant=("spec_fixed", "spec_quad")),
                       st.GpuGeom(algo="speculative", group_lanes=8, slot_records=tile)):
                 assert np.array_equal(_dev_eval(nodes, xd, g, m), want), (depth, a, m, g, tile)
