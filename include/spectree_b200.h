@@ -208,6 +208,40 @@ int st_eval_depths_device(const st_tree* tree, const float* x, uint64_t m, uint3
                           uint64_t ld, int layout, const st_geom* geom, uint32_t* labels,
                           uint32_t* depths, void* stream);
 
+/* ---- resident frame stream (C3: video-rate per-pixel classification) ----
+ * One data-decomposition grid stays resident and classifies frame 0, 1, 2,
+ * ... as they are published into a device ring of `ring` frame slots of
+ * `records` records x `a` attributes (AoS float32; a = 8, 16 or 32; records a
+ * multiple of the walk's tile, 32..128 records): the tree is staged once, no
+ * launch per frame.  Frame seq lives in slot seq % ring (st_frames_slot gives
+ * its device pointers).  Stream-ordered protocol for device producers:
+ *   st_frames_acquire(seq, s)  s waits until frame seq - ring is done (slot free)
+ *   ... producer work on s writes the slot's records ...
+ *   st_frames_publish(seq, s)  after s's prior work, frames up to seq are ready
+ *   st_frames_wait(seq, s2)    s2 waits until frame seq's labels are written
+ * Frames complete in order, so one acquire of the last frame of a batch
+ * (seq + k) frees the slots of frames seq .. seq + k, and one publish of it
+ * publishes the batch; a frame must be acquired before it is published.
+ * (cuStreamWriteValue32 / cuStreamWaitValue64: no SM time).  Host convenience:
+ * st_frames_push copies host records into the next slot and publishes them;
+ * st_frames_pop waits for a frame and copies its labels out (pop frame seq
+ * before publishing frame seq + ring).  The resident grid owns the SMs it
+ * occupies (max_ctas caps it, 0 = the planned persistent grid); device-wide
+ * synchronisation (cudaDeviceSynchronize, cudaFree) waits for it until
+ * st_frames_close.  A grid idle for idle_timeout_ms (0 = 10 s) stops itself
+ * (st_frames_status reports it).  Labels equal st_eval's for every frame. */
+typedef struct st_frames st_frames;
+int st_frames_open(const st_tree* tree, uint64_t records, uint32_t a, uint32_t ring, const st_geom* geom,
+                   uint32_t max_ctas, uint32_t idle_timeout_ms, st_frames** out);
+int st_frames_slot(st_frames* f, uint64_t seq, float** records, uint32_t** labels);
+int st_frames_acquire(st_frames* f, uint64_t seq, void* stream);
+int st_frames_publish(st_frames* f, uint64_t seq, void* stream);
+int st_frames_wait(st_frames* f, uint64_t seq, void* stream);
+int st_frames_push(st_frames* f, const float* host_records, uint64_t* seq);
+int st_frames_pop(st_frames* f, uint64_t seq, uint32_t* host_labels);
+int st_frames_status(st_frames* f, uint64_t* published, uint32_t* stopped);
+int st_frames_close(st_frames* f);
+
 /* One unpipelined host round trip with per-phase timing: the GPU edition of
  * the reference bench windows (bench.hpp:50-56, bench.cpp:228-262) and of the
  * paper's Table 1 (allocation, copy-in, kernel, copy-out, release):

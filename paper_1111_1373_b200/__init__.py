@@ -17,6 +17,7 @@ from .evaluate import (VARIANTS, DataParallelConfig, Forest, GpuGeom, ReductionM
                        eval_sharded, eval_speculative, eval_speculative_basic, last_launch_count,
                        mean_traversal_depth, traversal_depths, tree_info, validate_data_parallel,
                        validate_speculative)
+from .frames import FrameStream
 from .files import (dataset_info, eval_file, load_dataset_bin, load_labels_bin,
                     save_dataset_bin, save_labels_bin)
 from .synthetic import (dataset_checksum, fnv1a64, generate_synthetic_dataset,

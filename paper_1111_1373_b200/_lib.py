@@ -106,6 +106,8 @@ EXPORTS = (
     "st_eval_timed", "st_dataset_save", "st_dataset_info_read", "st_dataset_load",
     "st_labels_save", "st_labels_load", "st_eval_file",
     "st_eval_depths", "st_eval_depths_device",
+    "st_frames_open", "st_frames_slot", "st_frames_acquire", "st_frames_publish", "st_frames_wait",
+    "st_frames_push", "st_frames_pop", "st_frames_status", "st_frames_close",
 )
 
 _lib = None
@@ -177,6 +179,21 @@ def load() -> C.CDLL:
     L.st_labels_load.argtypes = [cp, vp, u64, C.POINTER(u64), C.POINTER(u32)]
     L.st_eval_file.restype = i32
     L.st_eval_file.argtypes = [vp, cp, C.POINTER(st_geom), cp, u32, C.POINTER(u64)]
+    L.st_frames_open.restype = i32
+    L.st_frames_open.argtypes = [vp, u64, u32, u32, C.POINTER(st_geom), u32, u32, C.POINTER(vp)]
+    L.st_frames_slot.restype = i32
+    L.st_frames_slot.argtypes = [vp, u64, C.POINTER(vp), C.POINTER(vp)]
+    for fn in (L.st_frames_acquire, L.st_frames_publish, L.st_frames_wait):
+        fn.restype = i32
+        fn.argtypes = [vp, u64, vp]
+    L.st_frames_push.restype = i32
+    L.st_frames_push.argtypes = [vp, vp, C.POINTER(u64)]
+    L.st_frames_pop.restype = i32
+    L.st_frames_pop.argtypes = [vp, u64, vp]
+    L.st_frames_status.restype = i32
+    L.st_frames_status.argtypes = [vp, C.POINTER(u64), C.POINTER(u32)]
+    L.st_frames_close.restype = i32
+    L.st_frames_close.argtypes = [vp]
     _lib = L
     return L
 

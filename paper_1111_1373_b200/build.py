@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SRCS = [os.path.join(CSRC, f) for f in
-        ("st_capi.cu", "st_data.cu", "st_spec.cu", "st_forest.cu", "st_io.cu", "st_synth.cpp")]
+        ("st_capi.cu", "st_data.cu", "st_spec.cu", "st_forest.cu", "st_frames.cu", "st_io.cu", "st_synth.cpp")]
 HEADERS = [os.path.join(CSRC, "st_kernels.cuh"), os.path.join(CSRC, "st_internal.cuh"),
            os.path.join(ROOT, "include", "spectree_b200.h")]
 OUT = os.path.join(HERE, "libspectree_b200.so")

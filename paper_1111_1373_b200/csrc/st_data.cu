@@ -119,8 +119,8 @@ void launch_data(const Staging& stg, int tloc, const DataArgs& d, const st_tree*
   }
 }
 
-void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
-                      const st_geom& g0, uint32_t* labels, uint32_t* depths, cudaStream_t s, int dev) {
+DataPlan plan_data(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+                   const st_geom& g0, uint32_t* labels, uint32_t* depths, int dev) {
   st_geom g = g0;
   if (depths) {
     // traversal depths come from the record-major walks; the constant-bank
@@ -241,8 +241,20 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     if (g.pdl > 3) fail(ST_ERR_ARGUMENT, "pdl must be 0-3");
     d.pdl = g.pdl == 0 ? (room ? 1u : 2u) : g.pdl == 3 ? 0u : g.pdl;
   }
-  if (depths) return launch_data<true>(stg, tloc, d, t, smem, dev, bps, s, a);
-  return launch_data<false>(stg, tloc, d, t, smem, dev, bps, s, a);
+  DataPlan pl;
+  pl.stg = stg;
+  pl.tloc = tloc;
+  pl.d = d;
+  pl.smem = smem;
+  pl.bps = bps;
+  return pl;
+}
+
+void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+                      const st_geom& g, uint32_t* labels, uint32_t* depths, cudaStream_t s, int dev) {
+  const DataPlan pl = plan_data(t, x, m, a, ld, layout, g, labels, depths, dev);
+  if (depths) return launch_data<true>(pl.stg, pl.tloc, pl.d, t, pl.smem, dev, pl.bps, s, a);
+  return launch_data<false>(pl.stg, pl.tloc, pl.d, t, pl.smem, dev, pl.bps, s, a);
 }
 
 

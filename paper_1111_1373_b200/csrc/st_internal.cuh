@@ -901,6 +901,17 @@ inline PipeArgs pipe_args(const float* x, uint64_t m, uint32_t a, uint64_t ld, i
 inline bool ct_arity(uint32_t a) { return a == 8 || a == 16 || a == 32 || a == 64; }
 
 // ---- cross-translation-unit entry points ------------------------------------
+// Data-kernel launch plan (st_data.cu): staging, tree location, arguments.
+struct DataPlan {
+  Staging stg;
+  int tloc = 0;
+  DataArgs d{};
+  size_t smem = 0;
+  uint32_t bps = 0;
+};
+DataPlan plan_data(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
+                   const st_geom& g, uint32_t* labels, uint32_t* depths, int dev);
+uint32_t choose_S(uint32_t a, uint32_t want, bool small);
 void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
                       const st_geom& g, uint32_t* labels, uint32_t* depths, cudaStream_t s,
                       int dev);                                                         // st_data.cu

@@ -230,6 +230,7 @@ struct Pipe {
   const CUtensorMap* tmap;
   PipeArgs p;
   int lane;
+  uint32_t row0 = 0;  // first 128-byte row of the record range in the tensor map (frame slot)
 
   __device__ __forceinline__ uint32_t arity() const { return A > 0 ? (uint32_t)A : p.a; }
   __device__ __forceinline__ bool full(uint64_t t) const { return (t + 1) * (uint64_t)R <= p.m; }
@@ -239,7 +240,7 @@ struct Pipe {
     const uint32_t bytes = R * arity() * 4u;
     const uint32_t bar = bars + 8u * s;
     mbar_arrive_expect_tx(bar, bytes);
-    tma_load_2d(stage(s), tmap, 0, (int)(t * (uint64_t)R * arity() / 32u), bar);
+    tma_load_2d(stage(s), tmap, 0, (int)(row0 + t * (uint64_t)R * arity() / 32u), bar);
   }
 
   __device__ __forceinline__ void start(uint64_t first, uint64_t step, uint64_t n_tiles) {
@@ -353,7 +354,25 @@ struct DataArgs {
   uint32_t bulk_tree;          // stage the shared tree with one cp.async.bulk (else per-thread loads)
   uint32_t pdl;                // launched as a programmatic dependent (griddepcontrol)
   uint32_t* depths;            // k_data<DEPTH>: per-record traversal depth (edges root -> leaf)
+  // k_data<FRAMES>: resident frame-stream kernel (st_frames_*).  p.m records
+  // per frame, frame seq in slot seq % ring (records at rows slot *
+  // frame_rows of the tensor map, labels at labels + slot * p.m); control
+  // words fctl = {published, closed_at, error, pad} then uint64 done[ring]:
+  // tiles of the frames in that slot walked so far (monotone).
+  uint32_t* fctl;
+  uint32_t ring, frame_rows;
+  uint64_t idle_ns;            // a warp waiting this long for a frame stops the stream (error word)
 };
+
+// Frame-stream control words (k_data<FRAMES>, st_frames.cu); the uint64
+// per-slot completion counters start at word kFDone
+enum : uint32_t { kFPublished = 0, kFClosed = 1, kFError = 2, kFDone = 4 };
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Shared-memory carve-out shared by the kernels:
 //   [tree | windows (1024-aligned)] [warps x ns stages] [warps x ns mbarriers]
@@ -474,11 +493,15 @@ __device__ __forceinline__ float pick_reg(const float (&f)[A], uint32_t meta) {
 // DEPTH: also write each record's traversal depth (edges root -> leaf,
 // eval_serial.cpp:77-105) to args.depths; the host never pairs it with the
 // register / transposed walks (kSharedReg, kSharedT).
-template <int A, int S, int TLOC, int LOADER, int CAP, bool DEPTH = false>
+// FRAMES: the resident frame-stream kernel (st_frames_*): the tree is staged
+// once, then every warp walks its tiles of frame 0, 1, 2, ... as they are
+// published, with no launch and no tree staging per frame (DataArgs.fctl).
+template <int A, int S, int TLOC, int LOADER, int CAP, bool DEPTH = false, bool FRAMES = false>
 __global__ void __launch_bounds__(kMaxThreads)
     k_data(const DataArgs args, const __grid_constant__ CUtensorMap tmap,
            const __grid_constant__ ConstTree<CAP> ctree) {
   static_assert(!DEPTH || (TLOC != kSharedReg && TLOC != kSharedT), "depth output: record-major walks");
+  static_assert(!FRAMES || (LOADER == kTma && !DEPTH), "frame stream: TMA-staged records, labels only");
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int R = 32 * S;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -486,6 +509,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   const uint32_t sbase = align1024(smem_u32(smem));
 
   TreeRef<TLOC, CAP> tree{sbase, reinterpret_cast<const char*>(args.nodes), &ctree};
+  uint32_t* labels = args.labels;  // FRAMES: the current frame's label slot
 
   Pipe<A, S, LOADER> pipe;
   const uint32_t tiles0 = sbase + args.tree_bytes;
@@ -526,8 +550,8 @@ __global__ void __launch_bounds__(kMaxThreads)
     if (args.pdl == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
   // first record tiles in flight before the tree is rebased (the TMA does not
-  // depend on it)
-  pipe.start(first, step, n_tiles);
+  // depend on it); a frame stream only initialises the stage barriers
+  pipe.start(first, step, FRAMES ? 0 : n_tiles);
 
   // ---- stage the node array once per CTA --------------------------------
   constexpr uint32_t kLR = 5u;  // kSharedT: attribute stride 32 records (log2)
@@ -570,7 +594,106 @@ __global__ void __launch_bounds__(kMaxThreads)
   }
 
   uint64_t i = 0;
-  for (uint64_t t = first; t < n_tiles; t += step, ++i) {
+  // FRAMES: the warp walks one continuous tile sequence G = first, first +
+  // step, ... over all frames (G = frame * n_tiles + tile of the frame), so
+  // frame boundaries fall at different times for different warps and the
+  // stage refill runs across them.  A tile is issued once its frame is
+  // published (lane 0 caches the published count; a tile whose frame is not
+  // published yet is issued when the warp reaches it).  Per frame a warp
+  // adds its tile count to the slot's completion counter (one release
+  // reduction per frame visited).
+  uint64_t G = first;
+  uint32_t pub_known = 0, deferred = 0, cur = 0xFFFFFFFFu, cnt = 0;
+  auto frame_row = [&](uint64_t g, uint32_t f) -> uint32_t {
+    return (f % args.ring) * args.frame_rows + (uint32_t)((g - (uint64_t)f * n_tiles) * R * pipe.arity() / 32u);
+  };
+  // lane 0: issue tile g into stage s if its frame is published
+  auto try_issue = [&](uint64_t g, uint32_t s) -> bool {
+    const uint32_t f = (uint32_t)(g / n_tiles);
+    if (f >= pub_known) {
+      uint32_t pub;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(pub) : "l"(args.fctl + kFPublished) : "memory");
+      if (pub > pub_known) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // records arrive through the async proxy
+        pub_known = pub;
+      }
+      if (f >= pub_known) return false;
+    }
+    const uint32_t bar = pipe.bars + 8u * s;
+    mbar_arrive_expect_tx(bar, R * pipe.arity() * 4u);
+    tma_load_2d(pipe.stage(s), pipe.tmap, 0, (int)frame_row(g, f), bar);
+    return true;
+  };
+  auto flush_count = [&]() {
+    if (cnt) {
+      __threadfence();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(reinterpret_cast<uint64_t*>(args.fctl + kFDone) +
+                                                                        cur % args.ring),
+                     "l"((uint64_t)cnt)
+                     : "memory");
+      cnt = 0;
+    }
+  };
+  if constexpr (FRAMES) {
+    if (lane == 0)
+      for (uint32_t s = 0; s < args.ns; ++s)
+        if (!try_issue(first + s * step, s)) deferred |= 1u << s;
+    __syncwarp();
+  }
+  // Done with this warp's i-th tile t: refill its stage with the warp's
+  // tile ns further on.
+  auto release_tile = [&](uint64_t ii, uint64_t tt) {
+    if constexpr (!FRAMES) {
+      pipe.release(ii, tt, step, n_tiles);
+    } else {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      const uint32_t s = (uint32_t)(ii % args.ns);
+      if (lane == 0 && !try_issue(G + args.ns * step, s)) deferred |= 1u << s;
+    }
+  };
+  for (uint64_t t = first;; G += step, t = G, ++i) {
+    if constexpr (!FRAMES) {
+      if (t >= n_tiles) break;
+    } else {
+      const uint32_t f = (uint32_t)(G / n_tiles);
+      t = G - (uint64_t)f * n_tiles;
+      if (f != cur) {  // the previous frame's tiles of this warp are walked: count them now
+        flush_count();
+        cur = f;
+        labels = args.labels + (uint64_t)(f % args.ring) * m;
+      }
+      const uint32_t s = (uint32_t)(i % args.ns);
+      uint32_t ok = 1;
+      if (lane == 0 && (deferred >> s) & 1u) {
+        // wait for the frame (or the close before it / the idle timeout)
+        uint64_t t0 = global_ns();
+        uint32_t seen = pub_known;
+        while (!try_issue(G, s)) {
+          if (pub_known != seen) {  // frames are still arriving: not idle
+            seen = pub_known;
+            t0 = global_ns();
+          }
+          uint32_t closed;
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(closed) : "l"(args.fctl + kFClosed) : "memory");
+          if (closed <= f) {
+            ok = 0;
+            break;
+          }
+          if (global_ns() - t0 > args.idle_ns) {
+            atomicOr(args.fctl + kFError, 1u);
+            ok = 0;
+            break;
+          }
+          __nanosleep(256);
+        }
+        if (ok) deferred &= ~(1u << s);
+      }
+      if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+      ++cnt;
+    }
     const uint64_t r0 = t * (uint64_t)R;
     const uint32_t tile = pipe.acquire(i, t);
     if constexpr (TLOC == kWide) {
@@ -588,7 +711,7 @@ __global__ void __launch_bounds__(kMaxThreads)
           nd = __ldg(args.wide + c);
           ++dep;
         }
-        args.labels[r0 + r] = nd.w;
+        labels[r0 + r] = nd.w;
         if constexpr (DEPTH) args.depths[r0 + r] = dep;
       }
     } else if constexpr (TLOC == kSharedT && LOADER == kTma && (A == 8 || A == 16)) {
@@ -645,7 +768,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         const uint64_t r = r0 + q * 32 + lane;
         if (r < m) {
           const uint32_t c = meta[q] & ~kLeafBit;
-          args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+          labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
         }
       }
     } else if constexpr (TLOC == kSharedReg && LOADER == kTma && (A == 8 || A == 16)) {
@@ -663,7 +786,7 @@ __global__ void __launch_bounds__(kMaxThreads)
           f[q][4 * c + 3] = __uint_as_float(v.w);
         }
       }
-      pipe.release(i, t, step, n_tiles);  // next tile's TMA overlaps this walk
+      release_tile(i, t);  // next tile's TMA overlaps this walk
       uint32_t thr[S], meta[S];
       const uint2 root = tree.get(tree.root());
 #pragma unroll
@@ -692,7 +815,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         const uint64_t r = r0 + q * 32 + lane;
         if (r < m) {
           const uint32_t c = meta[q] & ~kLeafBit;
-          args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+          labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
         }
       }
       continue;  // stage already released
@@ -735,7 +858,7 @@ __global__ void __launch_bounds__(kMaxThreads)
         const uint64_t r = r0 + q * 32 + lane;
         if (r < m) {
           const uint32_t c = meta[q] & ~kLeafBit;
-          args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+          labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
           if constexpr (DEPTH) args.depths[r] = dep[q];
         }
       }
@@ -758,7 +881,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       }
       if (valid) {
         const uint32_t c = meta & ~kLeafBit;
-        args.labels[r0 + r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+        labels[r0 + r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
         if constexpr (DEPTH) args.depths[r0 + r] = dep;
       }
     } else {
@@ -796,13 +919,14 @@ __global__ void __launch_bounds__(kMaxThreads)
         const uint64_t r = r0 + q * 32 + lane;
         if (r < m) {
           const uint32_t c = meta[q] & ~kLeafBit;
-          args.labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
+          labels[r] = args.leaf_class ? __ldg(args.leaf_class + c) : c;
           if constexpr (DEPTH) args.depths[r] = dep[q];
         }
       }
     }
-    pipe.release(i, t, step, n_tiles);
+    release_tile(i, t);
   }
+  if constexpr (FRAMES) flush_count();
 }
 
 // ---------------------------------------------------------------------------
