@@ -199,4 +199,53 @@ inline spectree::ClassAssignment eval_forest(const std::vector<spectree::Encoded
   return out;
 }
 
+/// Resident frame stream (st_frames_*): one data-decomposition grid stays on
+/// the GPU and classifies frame after frame of `records` records (the C3
+/// per-pixel workload) with no launch per frame.  push() copies a host frame
+/// into the next ring slot and publishes it; pop(seq) waits for that frame's
+/// labels (pop frame seq before pushing frame seq + ring).  Device producers
+/// use slot() / acquire() / publish() / wait() on their own CUDA streams
+/// (include/spectree_b200.h).  Labels equal eval_data_parallel's per frame.
+class FrameStream {
+ public:
+  FrameStream(const spectree::EncodedTree& tree, std::uint64_t records, std::uint32_t arity,
+              std::uint32_t ring = 4, const GpuConfig& gpu = {}, std::uint32_t idle_timeout_ms = 0)
+      : tree_(detail::make_handle(tree)), records_(records) {
+    st_geom g = gpu.geom;
+    g.algo = ST_ALGO_DATA;
+    detail::check(st_frames_open(tree_.get(), records, arity, ring, &g, 0, idle_timeout_ms, &f_));
+  }
+  FrameStream(const FrameStream&) = delete;
+  FrameStream& operator=(const FrameStream&) = delete;
+  ~FrameStream() {
+    if (f_) st_frames_close(f_);
+  }
+  std::uint64_t push(const float* frame) {
+    std::uint64_t seq = 0;
+    detail::check(st_frames_push(f_, frame, &seq));
+    return seq;
+  }
+  spectree::ClassAssignment pop(std::uint64_t seq) {
+    spectree::ClassAssignment out(records_);
+    detail::check(st_frames_pop(f_, seq, out.data()));
+    return out;
+  }
+  void slot(std::uint64_t seq, float** records, std::uint32_t** labels) {
+    detail::check(st_frames_slot(f_, seq, records, labels));
+  }
+  void acquire(std::uint64_t seq, void* stream) { detail::check(st_frames_acquire(f_, seq, stream)); }
+  void publish(std::uint64_t seq, void* stream) { detail::check(st_frames_publish(f_, seq, stream)); }
+  void wait(std::uint64_t seq, void* stream) { detail::check(st_frames_wait(f_, seq, stream)); }
+  void close() {
+    st_frames* f = f_;
+    f_ = nullptr;
+    if (f) detail::check(st_frames_close(f));
+  }
+
+ private:
+  detail::TreeHandle tree_;  // outlives the stream (declared first, destroyed last)
+  std::uint64_t records_;
+  st_frames* f_ = nullptr;
+};
+
 }  // namespace spectree_b200

@@ -16,7 +16,9 @@
 //     depth output) vs the reference traversal_depths on the same corpus;
 //   sharded: eval_data_parallel through GpuConfig.devices (every GPU of the
 //     box, or device 0 twice on a one-GPU box) vs the oracle;
-//   error behaviour: ArgumentError before any work, with the reference text.
+//   error behaviour: ArgumentError before any work, with the reference text;
+//   frames: spectree_b200::FrameStream (the resident frame stream) per frame
+//     vs the reference eval_serial.
 //
 // Built by oracle/Makefile into oracle/_ref/gpu_acceptance (needs the GPU
 // library); tests/test_gpu.py runs it.  Prints one PASS/FAIL line per check,
@@ -223,6 +225,35 @@ void errors() {
          "mean traversal depth of an empty dataset -> ArgumentError \"" + gpu_d + "\"");
 }
 
+// The resident frame stream through the C++ wrapper: a C3-shaped tree
+// (depth 12, 2048 leaves, 8 attributes), 7 frames of 16384 records through a
+// 3-slot ring, each frame's labels vs the reference eval_serial.
+void frames() {
+  const EncodedTree tree = generate_synthetic_tree(12, 2048, 8, 8, 301);
+  bool ok = true;
+  std::string detail = "7 frames x 16384 records, ring 3: labels == eval_serial";
+  try {
+    spectree_b200::FrameStream fs(tree, 16384, 8, 3, {}, 20000);
+    std::vector<Dataset> frames_;
+    std::vector<std::uint64_t> seqs;
+    for (int k = 0; k < 7; ++k) frames_.push_back(generate_synthetic_dataset(16384, 8, 4000 + k, k % 2 == 1 ? Distribution::gaussian : Distribution::uniform));
+    std::size_t popped = 0;
+    for (int k = 0; k < 7; ++k) {
+      if (seqs.size() - popped == 3) {
+        ok = ok && fs.pop(seqs[popped]) == eval_serial(tree, frames_[popped]);
+        ++popped;
+      }
+      seqs.push_back(fs.push(frames_[k].values().data()));
+    }
+    for (; popped < seqs.size(); ++popped) ok = ok && fs.pop(seqs[popped]) == eval_serial(tree, frames_[popped]);
+    fs.close();
+  } catch (const std::exception& e) {
+    ok = false;
+    detail = e.what();
+  }
+  report(ok, "frames", detail);
+}
+
 }  // namespace
 
 int main() {
@@ -235,5 +266,6 @@ int main() {
   errors();
   criterion1();
   criterion2();
+  frames();
   return failures;
 }

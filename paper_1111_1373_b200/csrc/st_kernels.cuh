@@ -955,6 +955,7 @@ struct SpecArgs {
   // added to / XOR applied to its swizzled record address)
   uint32_t sl_xmask, sl_leafmin, sl_adv, sl_xor;
   uint32_t sl_wmax;      // SL == 3: window steps every record takes (leaves are sinks)
+  uint32_t sl_wcheck;    // SL == 3: from this step on, stop once every stream of the warp sits in a sink
   uint32_t sl_ws, sl_wmul;  // entries per window (lanes >= sl_ws read lane 0's); bytes per code unit
   // ring label rows hold raw terminal codes: class = ((code & lab_mask) >>
   // lab_shift) - lab_sub (then the leaf-class table, if any)
@@ -1498,7 +1499,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       static_assert(Rec<A, kTma>::kRowLocal, "fixed-trip streams: records inside one 128-byte row");
       // 4 streams per batch (8 per triple measured even on C5, +4 % on C3)
       constexpr int KS = 4;
-      constexpr uint32_t NL = L3 ? 3u : 4u;  // storing lanes per group
+      const uint32_t NL = L3 ? 3u : G;  // lanes per group: lane s % NL stores stream s
       const uint32_t a4 = 4u * (uint32_t)A;
       auto base_of = [&](uint32_t rr) {
         const uint32_t ra4 = rr * a4, rowb = ra4 & ~127u;
@@ -1550,18 +1551,25 @@ __global__ void __launch_bounds__(kMaxThreads)
           }
         };
         step(true);
-        for (uint32_t w = 1; w < args.sl_wmax; ++w) step(false);
-        // lane j of the group stores streams j, j + NL, ... (mirror lanes none)
+        for (uint32_t w = 1; w < args.sl_wmax; ++w) {
+          // skewed trees: the warp's batch ends when all its streams are
+          // absorbed (one vote per step, from step sl_wcheck on) instead of
+          // after the deepest record's window count
+          if (w >= args.sl_wcheck) {
+            bool sunk = true;
+#pragma unroll
+            for (int s = 0; s < KS; ++s) sunk &= c[s] >= args.sl_leafmin;
+            if (__all_sync(0xffffffffu, sunk)) break;
+          }
+          step(false);
+        }
+        // lane s % NL of the group stores stream s (every stream stored even
+        // when the group has fewer lanes than streams: G = 2); mirror lanes none
         const bool st_ok = L3 ? lane < 30 : true;
 #pragma unroll
-        for (int s0 = 0; s0 < KS; s0 += NL) {
-          uint32_t mine = c[s0], mr = rr[s0];
-#pragma unroll
-          for (int s = s0 + 1; s < s0 + (int)NL && s < KS; ++s)
-            if (j == (uint32_t)(s - s0)) mine = c[s], mr = rr[s];
-          if (st_ok && j < (uint32_t)(KS - s0) && mr < rows)
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * mr), "r"(mine) : "memory");
-        }
+        for (int s = 0; s < KS; ++s)
+          if (st_ok && j == (uint32_t)s % NL && rr[s] < rows)
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(lbuf + 4u * rr[s]), "r"(c[s]) : "memory");
       }
     } else if constexpr (SR == 2 && SL == 2) {
       // Two record streams, self-loop codes, the stream advance in a

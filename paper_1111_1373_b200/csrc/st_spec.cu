@@ -137,10 +137,12 @@ void launch_spec_t(bool win_shared, const SpecArgs& sa, const Staging& stg, size
 
 // Lane triples apply to the fixed-trip loop over G = 4 three-node windows
 // with TMA-staged records inside one 128-byte row.
+// (8 / 16 attributes: 80-record slots of 2.5 / 5 KB; 32-attribute ones
+// would take 10 KB and cost resident warps -- C2 +19 %).
 static bool triple_ok(const st_geom& g, uint32_t G, const WinTable& wt, const float* x, uint64_t m, uint32_t a,
                       uint64_t ld, int layout) {
-  return !(g.variant & ST_VAR_SPEC_QUAD) && G == 4 && wt.sl_ws == 3 && m >= kTripleSlot &&
-         (a == 8 || a == 16 || a == 32) && tma_ok(x, m, a, ld, layout, 1);
+  return !(g.variant & ST_VAR_SPEC_QUAD) && G == 4 && wt.sl_ws == 3 && m >= kTripleSlot && (a == 8 || a == 16) &&
+         tma_ok(x, m, a, ld, layout, 1);
 }
 
 void spec_geometry(const st_tree* t, const st_geom& g, uint32_t& G, uint32_t& H) {
@@ -329,28 +331,21 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       if (want_sl && cw && sr >= 2 && wt->sl_units && (a == 8 || a == 16 || a == 32) && adv % 128u == 0 &&
           (rows_step % 8u == 0 || rows_step % 8u == 4) &&
           round1024((size_t)wt->sl_units * sizeof(SEntry)) <= 96 * 1024) {
-        // Loop shape by tree (same-box A/B, profiles/r2_spec_sl_ab.txt):
-        //  * balanced (the deepest record visits <= 1.5x the expected window
-        //    count): fixed trip count, leaves absorbing, no per-step test --
-        //    C5 d8 / d10 / d12 / d14 -5 / -6 / -4 / -17 %, C1 -6 %, C3 -11 %
-        //    vs the select loop;
-        //  * skewed (depth >= log2(leaves) + 3): the stream advance
-        //    predicated -- some stream of the warp resolves in nearly every
-        //    step -- C5 d16 / d18 / d20 -15 / -16 / -17 %, C2 -5 %;
-        //  * otherwise the advance in a divergent branch.
-        // ST_VAR_SPEC_FIXED / _PRED / _BRANCH force one.
-        uint32_t lgl = 0;
-        while ((1u << lgl) < t->info.leaves) ++lgl;
-        // with lane triples (below) the fixed trip pays up to ~2x the mean
-        // window count (C5 d16, ratio 1.96: -9 % vs predicated; d18, 2.18: +4 %)
-        const bool triples = triple_ok(g, G, *wt, x, m, a, ld, layout);
-        const bool balanced = wt->sl_wmax <= (triples ? 2.0 : 1.5) * wt->sl_wmean;
-        sl = (g.variant & ST_VAR_SPEC_PRED) ? 1
-             : (g.variant & ST_VAR_SPEC_BRANCH) ? 2
-             : (g.variant & ST_VAR_SPEC_FIXED) ? 3
-             : balanced ? 3
-             : t->info.depth >= lgl + 3 ? 1 : 2;
+        // Loop shape.  Round 2 chose by tree balance (profiles/r2_spec_sl_ab.txt):
+        // the fixed trip (leaves absorbing, no per-step test) for balanced
+        // trees, a predicated stream advance for skewed ones (C5 d16 - d20,
+        // C2), a divergent advance otherwise.  With lane triples and the
+        // warp's batch ending once every stream is absorbed (one vote per
+        // step, sl_wcheck below), the fixed trip wins everywhere (same-box
+        // A/B): C5 d18 / d20 -5 / -3 % vs predicated, d16 -9 %, C2 -1.5 %
+        // (4-lane groups: its 32-attribute records would make 10 KB triple
+        // slots).  ST_VAR_SPEC_PRED / _BRANCH force the others.
+        sl = (g.variant & ST_VAR_SPEC_PRED) ? 1 : (g.variant & ST_VAR_SPEC_BRANCH) ? 2 : 3;
         rs.sl_wmax = wt->sl_wmax;
+        // early batch exit (one vote per step) only where the deepest record
+        // visits clearly more windows than the mean
+        rs.sl_wcheck = (wt->sl_wmax > 1.25 * wt->sl_wmean) ? std::max<uint32_t>(1u, (uint32_t)wt->sl_wmean)
+                                                           : wt->sl_wmax;
         rs.sl_ws = wt->sl_ws;
         rs.sl_wmul = 8u * wt->sl_ws / G;  // code units (w << log2 G) -> byte offset of window w
         rs.win = wdev + wt->sl_off;

@@ -23,6 +23,7 @@ DATA_GEOMS = [st.GpuGeom(algo="data"),
               st.GpuGeom(algo="data", record_regs=2, stages=3),
               st.GpuGeom(algo="data", record_regs=3, samples_per_thread=4)]   # transposed tiles
 SPEC_GEOMS = [st.GpuGeom(algo="speculative"),
+              st.GpuGeom(algo="speculative", group_lanes=2),                  # fewer lanes than streams
               st.GpuGeom(algo="speculative", group_lanes=4),
               st.GpuGeom(algo="speculative", group_lanes=8),
               st.GpuGeom(algo="speculative", group_lanes=32),
@@ -562,5 +563,6 @@ def test_spec_ring_slot_sizes(cuda, co, tile):
                       st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_branch",)),
                       st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_fixed",)),
                       st.GpuGeom(algo="speculative", variant=("spec_fixed", "spec_quad")),
-                      st.GpuGeom(algo="speculative", group_lanes=8, slot_records=tile)):
+                      st.GpuGeom(algo="speculative", group_lanes=8, slot_records=tile),
+                      st.GpuGeom(algo="speculative", group_lanes=2, slot_records=tile)):
                 assert np.array_equal(_dev_eval(nodes, xd, g, m), want), (depth, a, m, g, tile)
