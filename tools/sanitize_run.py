@@ -1,6 +1,7 @@
 """One small launch of every kernel family (data: shared/global/constant tree,
-S = 1/2/4; speculative: ring, one-window ballot / jump, per-warp, EXACT shfl, EXACT CTA;
-forest), labels
+S = 1/2/4; speculative: ring (lane triples, 4-lane groups, stream loops),
+one-window ballot / jump, per-warp, EXACT shfl, EXACT CTA; forest; with
+--frames the resident frame stream), labels
 checked against the C oracle -- the target for compute-sanitizer
 (memcheck / racecheck / synccheck):
 
@@ -18,8 +19,24 @@ import oracle  # noqa: E402  (checker only)
 import paper_1111_1373_b200 as st  # noqa: E402
 
 co = oracle.COracle()
-m = int(sys.argv[1]) if len(sys.argv) > 1 else 20_000
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+m = int(args[0]) if args else 20_000
 bad = 0
+if "--frames" in sys.argv:
+    # the resident frame stream: 3 frames through a 2-slot ring, labels vs the oracle
+    nodes = co.gen_tree(12, 2048, 8, 8, 301)
+    frames = [co.gen_dataset(8192, 8, 50 + k) for k in range(3)]
+    with st.FrameStream(nodes, 8192, 8, ring=2, idle_timeout_ms=120000) as fs:
+        seqs = []
+        for k, f in enumerate(frames):
+            if len(seqs) == 2:
+                s0 = seqs.pop(0)
+                bad += not np.array_equal(fs.pop(s0), co.eval_serial(nodes, frames[s0]))
+            seqs.append(fs.push(f))
+        for s0 in seqs:
+            bad += not np.array_equal(fs.pop(s0), co.eval_serial(nodes, frames[s0]))
+    print("sanitize_run frames:", "ok" if bad == 0 else f"{bad} mismatches")
+    sys.exit(1 if bad else 0)
 cases = [((24, 256, 32, 8, 201), 32), ((12, 2048, 8, 8, 301), 8), ((10, 1024, 16, 8, 101), 16),
          ((11, 16, 19, 7, 1), 19), ((12, 1024, 64, 8, 401), 64)]
 for targs, a in cases:
@@ -33,6 +50,9 @@ for targs, a in cases:
     geoms += [st.GpuGeom(algo="data", record_regs=3, samples_per_thread=s, stages=n) for s in (1, 4) for n in (1, 2)]
     geoms += [st.GpuGeom(algo="speculative", pipeline=p, group_lanes=g) for p in (1, 2) for g in (0, 2, 8)]
     geoms += [st.GpuGeom(algo="speculative", samples_per_thread=2, group_lanes=g) for g in (2, 4)]
+    # the fixed-trip loop on lane triples (default) and 4-lane groups, the round-2 stream loops
+    geoms += [st.GpuGeom(algo="speculative", variant=v)
+              for v in ((), ("spec_quad",), ("spec_pred",), ("spec_branch",))]
     for g in geoms:
         out = torch.empty(len(x), dtype=torch.int32, device="cuda")
         st.eval_device(nodes, xd, out, g)
