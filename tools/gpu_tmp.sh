@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-for T in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $T --print-limit 20 python tools/sanitize_run.py 8000 > gpurun_out/san_$T.log 2>&1; echo "$T rc=$?"; tail -3 gpurun_out/san_$T.log
-done
-timeout 600 compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize_run.py --frames > gpurun_out/san_frames_memcheck.log 2>&1; echo "frames memcheck rc=$?"; tail -3 gpurun_out/san_frames_memcheck.log
-timeout 900 compute-sanitizer --tool racecheck --print-limit 20 python tools/sanitize_run.py --frames > gpurun_out/san_frames_racecheck.log 2>&1; echo "frames racecheck rc=$?"; tail -3 gpurun_out/san_frames_racecheck.log
+timeout 900 python -m pytest tests/test_gpu.py tests/test_gpu_flow.py -x -q -k "spec or appendix_a or pdl or order" > gpurun_out/t_pdl.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/t_pdl.log
+for W in C1 C3; do timeout 200 python tools/ab_geoms.py $W 'dict(pdl=3)' --algo=speculative --flush 2>&1 | tail -1; done
+for W in C2 C5d12; do timeout 200 python tools/ab_geoms.py $W 'dict(pdl=3)' --algo=speculative 2>&1 | tail -1; done
