@@ -749,6 +749,50 @@ def cpu_baseline(args, nodes, x):
             "cpu": _cpu_model()}
 
 
+def cpu_baseline_forest(args, trees, x, n_classes):
+    """C4 CPU baseline (all 128 trees plus the vote): the
+    reference eval_serial (oracle/_ref) of every tree on ONE host core over a
+    bounded sample, then the vote (numpy, outside the serial walk's time is
+    negligible; included)."""
+    impl, kind = _ref_or_port()
+    sample = min(len(x), max(1000, args.cpu_sample // 40))
+    xs = np.ascontiguousarray(x[:sample])
+    rows = np.arange(sample)
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+        pinned = True
+    except Exception:
+        pinned = False
+    done = 0
+    if kind == "reference":
+        handles = [impl.tree(t) for t in trees]
+        data = impl.data(xs)
+        walk = lambda t: t.eval_serial(data)  # noqa: E731
+    else:
+        handles = trees
+        walk = lambda t: impl.eval_serial(t, xs)  # noqa: E731
+    t0 = time.perf_counter()
+    while True:
+        votes = np.zeros((sample, n_classes), np.uint32)
+        for t in handles:
+            votes[rows, walk(t)] += 1
+        votes.argmax(axis=1)
+        done += sample
+        if time.perf_counter() - t0 >= args.cpu_seconds:
+            break
+    el = time.perf_counter() - t0
+    if pinned:
+        try:
+            os.sched_setaffinity(0, set(range(os.cpu_count())))
+        except Exception:
+            pass
+    return {"value": done / el, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"first {sample} records of the rank-0 C4 workload, {done // sample} passes ({el:.1f} s) "
+                      f"of spectree::eval_serial for each of the {len(trees)} trees + the vote, pinned to 1 core",
+            "note": "the walk is the reference eval_serial; the vote (smallest class on ties) is ours",
+            "cpu": _cpu_model()}
+
+
 def _cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -898,6 +942,8 @@ def run_forest(args):
                 "d2h_bytes_per_step": 4 * m * world, "steps": e_steps, "api": "st_forest_eval (host pinned buffers)"},
         "clocks": clocks, "gpu_launches": launches,
     }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_forest(args, [t.nodes() for t in forest.trees], xnp, F["classes"])
     if rank == 0:
         print(json.dumps(line), flush=True)
     pg.close()
