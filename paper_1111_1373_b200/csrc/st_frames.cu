@@ -182,6 +182,8 @@ int st_frames_open(const st_tree* tree, uint64_t records, uint32_t a, uint32_t r
       // stream of frames), then a tensor map over the whole ring
       DataPlan pl = plan_data(f->tree, f->x, records, a, a, ST_LAYOUT_AOS, g, f->labels, nullptr, dev);
       if (pl.stg.loader != kTma) fail(ST_ERR_ARGUMENT, "frame stream needs TMA-staged records");
+      if (pl.tloc != ST_TREE_SHARED && pl.tloc != ST_TREE_GLOBAL)
+        fail(ST_ERR_ARGUMENT, "frame stream needs the compact node format (tree indices too large)");
       const uint64_t R = 32ull * pl.stg.S;
       if (records % R != 0)
         fail(ST_ERR_ARGUMENT, "records per frame must be a multiple of " + std::to_string(R) +
