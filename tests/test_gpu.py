@@ -189,6 +189,41 @@ def test_edge_semantics(cuda, co):
             assert np.array_equal(st.eval_gpu(t, x, g), want), (thr, g)
 
 
+@pytest.mark.parametrize("a", [8, 16, 32])
+def test_edge_semantics_every_kernel(cuda, co, a):
+    """The same ordered-'>' semantics through the large-input kernels (lane
+    triples, 4-lane groups, stream loops, folded data walks, transposed
+    tiles, the frame stream): a depth-10 tree whose thresholds include ties
+    with the data, +/-0 and subnormals, over records drawn from NaN, +/-inf,
+    +/-0, subnormals and the thresholds themselves."""
+    rng = np.random.default_rng(a)
+    nodes = co.gen_tree(10, 600, a, 8, 900 + a).copy()
+    internal = nodes["class_id"] == 0xFFFFFFFF
+    sub = np.float32(1e-40)
+    special_thr = np.array([0.0, -0.0, sub, -sub, 0.5, 0.25, 0.75], np.float32)
+    pick = rng.random(internal.sum()) < 0.4
+    thr = nodes["threshold"][internal]
+    thr[pick] = rng.choice(special_thr, pick.sum())
+    nodes["threshold"][internal] = thr
+    pool = np.concatenate([special_thr, np.array([np.nan, np.inf, -np.inf, 2 * sub, 0.49999997, 0.50000006,
+                                                  1e30, -1e30], np.float32)])
+    m = 50_000
+    x = rng.choice(pool, (m, a)).astype(np.float32)
+    mix = rng.random((m, a)) < 0.5
+    x[mix] = rng.random(mix.sum()).astype(np.float32)
+    want = co.eval_serial(nodes, x)
+    geoms = [st.GpuGeom(algo="data"), st.GpuGeom(algo="data", record_regs=3),
+             st.GpuGeom(algo="data", variant=("no_fold",)), st.GpuGeom(algo="speculative"),
+             st.GpuGeom(algo="speculative", variant=("spec_quad",)),
+             st.GpuGeom(algo="speculative", variant=("spec_pred",)),
+             st.GpuGeom(algo="speculative", variant=("spec_wide",))]
+    for g in geoms:
+        assert np.array_equal(st.eval_gpu(nodes, x, g), want), (a, g)
+    rec = m // 128 * 128
+    with st.FrameStream(nodes, rec, a, ring=2, idle_timeout_ms=20000) as fs:
+        assert np.array_equal(fs.pop(fs.push(x[:rec])), want[:rec])
+
+
 def test_single_leaf_and_empty(cuda):
     leaf = st.EncodedTree(np.array([(0, np.inf, 0, 6)], dtype=st.NODE_DTYPE))
     x = np.array([[0.1], [0.9]], np.float32)
