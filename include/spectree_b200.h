@@ -91,7 +91,8 @@ typedef struct st_geom {
                                   3 = transpose each tile in place to attribute-major, then walk it */
   uint32_t variant;            /* ST_VAR_* bit flags: A/B variants of the tuned defaults (0 = defaults) */
   uint32_t ring_slots;         /* speculative ring: cap on the tile-slot count (0 = auto; stress tests) */
-  uint32_t slot_records;       /* speculative ring: records per slot / 32, 1 or 2 (0 = auto) */
+  uint32_t slot_records;       /* speculative ring: records per slot / 32, 1 or 2 (0 = auto); with lane
+                                  triples 2 = 80-record and 3 = 120-record slots */
   uint32_t fold_min;           /* data kernel: fold trees of at least this many nodes (0 = auto: 2047) */
   uint32_t pdl;                /* data kernel: programmatic dependent launch, 0 = auto,
                                   1 = trigger dependents early, 2 = at exit, 3 = off */

@@ -39,7 +39,7 @@ constexpr uint32_t kPairBit = 0x40000000u;
 constexpr uint32_t kNoClass = 0xFFFFFFFFu;
 constexpr int kWarpsPerCta = 8;    // default CTA width (warps); launches may use up to 32
 constexpr int kMaxThreads = 1024;
-constexpr int kTripleSlot = 80;   // records per ring slot of the lane-triple speculative loop
+constexpr int kTripleSlot = 80;   // records per ring slot of the lane-triple speculative loop (x 3/2: L3 = 3)
 
 // Compact 8-byte device node.  internal: meta = (8*child) << abits | 4*attr
 // (bit 31 clear; byte offsets so the walk does no scaling); leaf: meta =
@@ -1137,7 +1137,8 @@ struct SpecRingArgs {
   uint32_t n_slots;       // NS
   uint32_t ns_magic;      // floor(2^32 / NS): ticket -> (generation, slot) without a division
   uint32_t bulk_win;      // stage the window table with one cp.async.bulk (else per-thread loads)
-  uint32_t tile_mult;     // host: records per ring slot / 32 (the kernel's RT); 0 = lane triples (kTripleSlot)
+  uint32_t tile_mult;     // host: records per ring slot / 32 (the kernel's RT); 0 = lane triples
+  uint32_t triple;        // host: lane-triple slots of kTripleSlot (1) or 3/2 kTripleSlot (3) records
 };
 
 // RT: records per ring slot / 32.  Two-stream groups over 64-record slots
@@ -1168,7 +1169,7 @@ __global__ void __launch_bounds__(kMaxThreads)
   static_assert(!L3 || (SL == 3 && RT == 1), "lane triples: fixed-trip loop, 80-record slots");
   extern __shared__ __align__(1024) unsigned char smem[];
   const SpecArgs& args = ra.s;
-  constexpr int R = L3 ? kTripleSlot : 32 * RT;
+  constexpr int R = L3 ? (L3 == 3 ? kTripleSlot * 3 / 2 : kTripleSlot) : 32 * RT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t NS = ra.n_slots;
   const uint32_t sbase = align1024(smem_u32(smem));

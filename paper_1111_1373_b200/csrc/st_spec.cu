@@ -35,7 +35,7 @@ template <int A, bool WS, int STEPS, int SR, bool CW = false, int RT = 1, int SL
 void launch_spec_ring_k(const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
                         uint32_t warps, cudaStream_t s) {
   auto fn = k_spec_ring<A, WS, STEPS, SR, CW, RT, SL, L3>;
-  constexpr uint64_t R = L3 ? kTripleSlot : 32 * RT;
+  constexpr uint64_t R = L3 ? (L3 == 3 ? kTripleSlot * 3 / 2 : kTripleSlot) : 32 * RT;
   const uint64_t n_tiles = (ra.s.p.m + R - 1) / R;
   const int blocks = blocks_for((const void*)fn, smem, dev, 0, n_tiles * warps, warps);
   clear_stale_error();
@@ -54,8 +54,10 @@ void launch_spec_ring_sr(uint32_t sr, const SpecRingArgs& ra, const Staging& stg
         return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 1>(ra, stg, smem, dev, warps, s);
       }
       if (sl == 3 && sr >= 2) {  // self-loop codes, fixed trip count
-        if (ra.tile_mult == 0)  // lane triples, 80-record slots
+        if (ra.tile_mult == 0) {  // lane triples, 80- or 120-record slots (ra.triple 1 / 3)
+          if (ra.triple == 3) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 3, 3>(ra, stg, smem, dev, warps, s);
           return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 3, 1>(ra, stg, smem, dev, warps, s);
+        }
         if (ra.tile_mult == 2) return launch_spec_ring_k<A, WS, STEPS, 2, CW, 2, 3>(ra, stg, smem, dev, warps, s);
         return launch_spec_ring_k<A, WS, STEPS, 2, CW, 1, 3>(ra, stg, smem, dev, warps, s);
       }
@@ -377,7 +379,8 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     // = 1 / 2 forces 32 / 64 (profiles/r1_spec_tile_ab.txt).
     uint32_t rt = 1;
     Staging rstg = stg;
-    const uint32_t want_rt = g.slot_records ? g.slot_records : (a == 16 ? 2u : 1u);
+    if (g.slot_records > 3) fail(ST_ERR_ARGUMENT, "slot_records must be 0-3");
+    const uint32_t want_rt = g.slot_records ? std::min<uint32_t>(g.slot_records, 2u) : (a == 16 ? 2u : 1u);
     if (cw && sr >= 2 && (a == 8 || a == 16 || a == 32) && want_rt == 2 && m >= 64) {
       Staging s2 = plan_staging(x, m, a, ld, layout, 2, g.stages, rs.win_bytes, pr);
       if (s2.loader == kTma && s2.S == 2) rt = 2, rstg = s2;
@@ -386,15 +389,22 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     // record groups per warp instead of 8, 80-record slots -- C1 / C3 / C5
     // d8..d14 -8 / -10 / -9 % (same-box A/B); ST_VAR_SPEC_QUAD keeps the
     // 4-lane groups.
+    // Triple slots hold 80 or 120 records (8 or 12 per group): 120 for
+    // 8-attribute records (4 KB slots: C3 -1.3 % per frame, -2.1 % on 32
+    // frames), 80 otherwise (120 would make 16-attribute slots 8 KB: C5 d12
+    // +17 %); st_geom.slot_records = 2 / 3 forces 80 / 120.
+    uint32_t triple = 0;
     if (sl == 3 && triple_ok(g, G, *wt, x, m, a, ld, layout)) {
+      triple = g.slot_records == 3 ? 3u : g.slot_records == 2 ? 1u : a == 8 ? 3u : 1u;
+      const uint32_t recs = triple == 3 ? kTripleSlot * 3 / 2 : kTripleSlot;
       Staging s3 = stg;
       s3.S = 1;
-      s3.stage_bytes = round1024((uint64_t)kTripleSlot * a * 4);
-      make_tmap(s3, x, m, a, kTripleSlot);
+      s3.stage_bytes = round1024((uint64_t)recs * a * 4);
+      make_tmap(s3, x, m, a, recs);
       rstg = s3;
       rt = 0;
     }
-    const size_t slot_recs = rt ? 32u * rt : (size_t)kTripleSlot;
+    const size_t slot_recs = rt ? 32u * rt : (size_t)(triple == 3 ? kTripleSlot * 3 / 2 : kTripleSlot);
     const size_t lb = 32 + 32 * 4 * slot_recs;  // generation padding + ticket + per-warp label rows (<= 32 warps)
     const size_t budget = pr.smem_optin - 1024 - rs.win_bytes - lb;
     const size_t max_slots = budget / (rstg.stage_bytes + 16u);
@@ -408,6 +418,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       ra.ns_magic = (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, (1ull << 32) / ra.n_slots);
       ra.bulk_win = (g.variant & ST_VAR_TREE_LOOP) ? 0u : 1u;
       ra.tile_mult = rt;
+      ra.triple = triple;
       ra.s.stage_bytes = rstg.stage_bytes;
       const size_t rsmem = 1024 + rs.win_bytes + (size_t)ra.n_slots * (rstg.stage_bytes + 8u) +
                            (((size_t)4 * ra.n_slots + 15) & ~size_t(15)) + 16 + (size_t)warps * 4 * slot_recs;

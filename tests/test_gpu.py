@@ -50,7 +50,8 @@ def test_appendix_a_labels(cuda, co, name):
     tree = st.EncodedTree(nodes)
     xd = torch.from_numpy(x).to(cuda)
     geoms = ALL_GEOMS if name in ("paper", "C1", "C2", "C3") else [DATA_GEOMS[0], SPEC_GEOMS[0]]
-    geoms = geoms + [st.GpuGeom(algo="speculative", variant=("spec_fixed", "spec_quad"))]
+    geoms = geoms + [st.GpuGeom(algo="speculative", variant=("spec_fixed", "spec_quad")),
+                     st.GpuGeom(algo="speculative", slot_records=2), st.GpuGeom(algo="speculative", slot_records=3)]
     for g in geoms:
         got = _dev_eval(tree, xd, g, len(x))
         assert co.fnv1a(got) == lab_fnv, f"{name} {g}"
@@ -598,6 +599,8 @@ def test_spec_ring_slot_sizes(cuda, co, tile):
                       st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_branch",)),
                       st.GpuGeom(algo="speculative", slot_records=tile, variant=("spec_fixed",)),
                       st.GpuGeom(algo="speculative", variant=("spec_fixed", "spec_quad")),
+                      st.GpuGeom(algo="speculative", slot_records=2),   # 80-record triple slots
+                      st.GpuGeom(algo="speculative", slot_records=3),   # 120-record triple slots
                       st.GpuGeom(algo="speculative", group_lanes=8, slot_records=tile),
                       st.GpuGeom(algo="speculative", group_lanes=2, slot_records=tile)):
                 assert np.array_equal(_dev_eval(nodes, xd, g, m), want), (depth, a, m, g, tile)
