@@ -73,6 +73,22 @@ def test_no_cpu_fallback(co):
         st.eval_data_parallel(nodes, x)
     with pytest.raises(st.NoDeviceError):
         st.eval_forest(st.Forest([nodes], 7), x)
+    with pytest.raises(st.NoDeviceError):
+        st.FrameStream(co.gen_tree(10, 1024, 16, 8, 101), 4096, 16)
+
+
+def test_frame_stream_argument_errors_before_device(co):
+    """st_frames_open validates before touching a device (same taxonomy as
+    st_eval): arity without TMA row-local tiles, empty frames, ring size,
+    attribute range, the speculative algorithm."""
+    nodes = co.gen_tree(10, 1024, 16, 8, 101)  # reads attributes < 16
+    for args, kw, msg in [((4096, 19), {}, "8, 16 or 32 attributes"),
+                          ((0, 16), {}, "records per frame"),
+                          ((4096, 16), {"ring": 0}, "ring must hold"),
+                          ((4096, 8), {}, "reads attribute"),
+                          ((4096, 16), {"geom": st.GpuGeom(algo="speculative")}, "data-decomposition")]:
+        with pytest.raises(st.ArgumentError, match=msg):
+            st.FrameStream(nodes, *args, **kw)
 
 
 def test_argument_errors_before_device(co):
