@@ -81,7 +81,7 @@ bool forest_smem_path(st_forest* f, int lay, const float* x, uint64_t m, uint32_
     const size_t region = round1024((uint64_t)n * L.max_tree_bytes);
     const size_t base = 1024 + region + 16u * n;
     if (base >= pr.smem_optin) continue;
-    uint32_t w = (uint32_t)std::min<size_t>(32, 1 + (pr.smem_optin - base) / (stg.stage_bytes + 8u));
+    uint32_t w = (uint32_t)std::min<size_t>(kForestMaxThreads / 32, 1 + (pr.smem_optin - base) / (stg.stage_bytes + 8u));
     if (g.warps_per_cta) w = std::min(w, g.warps_per_cta);
     if (w < 2) continue;
     stg.warps = w;

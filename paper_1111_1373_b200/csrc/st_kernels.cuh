@@ -39,6 +39,7 @@ constexpr uint32_t kPairBit = 0x40000000u;
 constexpr uint32_t kNoClass = 0xFFFFFFFFu;
 constexpr int kWarpsPerCta = 8;    // default CTA width (warps); launches may use up to 32
 constexpr int kMaxThreads = 1024;
+constexpr int kForestMaxThreads = 768;  // k_forest_smem: <= 24 warps (the tile ring fits ~21): up to 80 registers
 constexpr int kTripleSlot = 80;   // records per ring slot of the lane-triple speculative loop (x 3/2: L3 = 3)
 
 // Compact 8-byte device node.  internal: meta = (8*child) << abits | 4*attr
@@ -1936,7 +1937,7 @@ __device__ __forceinline__ void forest_step(uint32_t& thr, uint32_t& meta, uint3
 }
 
 template <int A, int S, int U>
-__global__ void __launch_bounds__(kMaxThreads)
+__global__ void __launch_bounds__(kForestMaxThreads)
     k_forest_smem(const Forest2Args args, const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int R = 32 * S;
