@@ -29,7 +29,7 @@ if [[ $PARTS == *launch* ]]; then
 fi
 if [[ $PARTS == *ncu* ]]; then
   # reports are summarised on the box (gpurun_out must stay < 64 MiB)
-  for WA in C5d12:speculative C5d20:speculative C1:speculative C3:speculative C3:data C5d12:data; do
+  for WA in ${NCU_LIST:-C5d12:speculative C5d20:speculative C1:speculative C3:speculative C3:data C5d12:data}; do
     W=${WA%%:*}; A=${WA##*:}; K=k_data; [[ $A == speculative ]] && K=k_spec
     R=$OUT/prof_${W}_${A}_$TAG
     timeout 300 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c 1 -o $R -f \
@@ -38,5 +38,13 @@ if [[ $PARTS == *ncu* ]]; then
     python tools/ncu_sass_hot.py $R.ncu-rep 30 > $OUT/ncu_${W}_${A}_${TAG}_hot.txt 2>&1
     rm -f $R.ncu-rep
   done
+fi
+if [[ $PARTS == *forest* ]]; then
+  R=$OUT/prof_C4_forest_$TAG
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_forest -s 1 -c 1 -o $R -f \
+    python tools/prof_forest.py > $R.log 2>&1; echo "ncu C4 rc=$?"
+  python tools/ncu_summary.py $R.ncu-rep $OUT/ncu_C4_forest_$TAG.json > /dev/null 2>&1
+  python tools/ncu_sass_hot.py $R.ncu-rep 30 > $OUT/ncu_C4_forest_${TAG}_hot.txt 2>&1
+  rm -f $R.ncu-rep
 fi
 ls $OUT | wc -l
