@@ -141,6 +141,52 @@ def test_tree_info_windows(co):
     assert leaf["spec_windows"] == 0 and leaf["nodes"] == 1
 
 
+def _windows_python(nodes, G=4, H=2):
+    """Independent restatement of st_tree::build_windows' partition: windows
+    of <= G internal nodes and <= H levels, breadth-first from each window root,
+    window roots discovered breadth-first."""
+    import collections
+
+    leaf = lambda i: nodes[i]["class_id"] != st.NO_CLASS  # noqa: E731
+    if leaf(0):
+        return 0
+    win_of_root, order, roots = {0: 0}, [0], collections.deque([0])
+    while roots:
+        r = roots.popleft()
+        mem, q, exits = [], collections.deque([(r, 0)]), []
+        while q:
+            u, d = q.popleft()
+            if len(mem) >= G or d >= H:
+                exits.append(u)
+                continue
+            mem.append(u)
+            for c in (int(nodes[u]["child"]), int(nodes[u]["child"]) + 1):
+                if not leaf(c):
+                    q.append((c, d + 1))
+        for u in exits:
+            if u not in win_of_root:
+                win_of_root[u] = len(order)
+                order.append(u)
+                roots.append(u)
+    return len(order)
+
+
+def test_window_partition_matches_restatement(co):
+    """The speculative window count of the default geometry (3-node, 2-level
+    windows for trees with > 32 internal nodes) equals a Python restatement
+    of the partition on random balanced and skewed trees."""
+    rng = np.random.default_rng(7)
+    for k in range(40):
+        depth = int(rng.integers(6, 21))
+        leaves = int(min(2 ** depth, rng.integers(depth + 1, 3000)))
+        nodes = co.gen_tree(depth, leaves, 16, 8, 1000 + k)
+        info = st.tree_info(nodes)
+        if info["internal"] <= 32:
+            continue
+        assert info["spec_group_lanes"] == 4
+        assert info["spec_windows"] == _windows_python(nodes), (depth, leaves)
+
+
 # ------------------------------------------------------------ tree model ---
 def test_encode_matches_reference_layout(co):
     """encode(decode(t)) reproduces the reference BFS bytes (tree.cpp:72-136)."""
