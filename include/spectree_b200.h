@@ -210,7 +210,10 @@ int st_eval_depths_device(const st_tree* tree, const float* x, uint64_t m, uint3
                           uint32_t* depths, void* stream);
 
 /* ---- resident frame stream (C3: video-rate per-pixel classification) ----
- * One data-decomposition grid stays resident and classifies frame 0, 1, 2,
+ * One grid stays resident -- the data decomposition, or with geom->algo =
+ * ST_ALGO_SPECULATIVE the speculative ring's fixed-trip window loop (trees
+ * with > 32 internal nodes, records a multiple of its 32 / 80 / 120-record
+ * slots) -- and classifies frame 0, 1, 2,
  * ... as they are published into a device ring of `ring` frame slots of
  * `records` records x `a` attributes (AoS float32; a = 8, 16 or 32; records a
  * multiple of the walk's tile, 32..128 records): the tree is staged once, no

@@ -147,7 +147,8 @@ int st_frames_open(const st_tree* tree, uint64_t records, uint32_t a, uint32_t r
       fail(ST_ERR_ARGUMENT, "frame ring too large for one tensor map");
     st_geom g{};
     if (geom) g = *geom;
-    if (g.algo == ST_ALGO_SPECULATIVE) fail(ST_ERR_ARGUMENT, "frame streams run the data-decomposition walk");
+    if (g.algo != ST_ALGO_AUTO && g.algo != ST_ALGO_DATA && g.algo != ST_ALGO_SPECULATIVE)
+      fail(ST_ERR_ARGUMENT, "unknown algorithm " + std::to_string(g.algo));
     if (g.tree_loc == ST_TREE_CONSTANT) g.tree_loc = ST_TREE_AUTO;
     const int dev = current_device();
     std::unique_ptr<st_frames> f(new st_frames());
@@ -178,6 +179,19 @@ int st_frames_open(const st_tree* tree, uint64_t records, uint32_t a, uint32_t r
       (void)write_value32();
       (void)wait_value64();
 
+      if (g.algo == ST_ALGO_SPECULATIVE) {
+        // the speculative ring in frame mode (st_spec.cu: k_spec_ring<..., FR>)
+        SpecFrames sf;
+        sf.fctl = f->ctl;
+        sf.ring = ring;
+        sf.max_ctas = max_ctas;
+        sf.ring_records = (uint64_t)ring * records;
+        sf.idle_ns = (uint64_t)f->timeout_ms * 1000000ull;
+        eval_spec_device(f->tree, f->x, records, a, a, ST_LAYOUT_AOS, g, f->labels, nullptr, f->ks, dev, &sf);
+        f->tiles = sf.tiles;
+        *out = f.release();
+        return;
+      }
       // the one-frame data plan (not a small input: the walk geometry of a
       // stream of frames), then a tensor map over the whole ring
       DataPlan pl = plan_data(f->tree, f->x, records, a, a, ST_LAYOUT_AOS, g, f->labels, nullptr, dev);

@@ -916,9 +916,16 @@ void eval_data_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
                       const st_geom& g, uint32_t* labels, uint32_t* depths, cudaStream_t s,
                       int dev);                                                         // st_data.cu
 void spec_geometry(const st_tree* t, const st_geom& g, uint32_t& G, uint32_t& H);     // st_spec.cu
+// frame-stream launch of the speculative ring (st_frames.cu -> st_spec.cu)
+struct SpecFrames {
+  uint32_t* fctl = nullptr;
+  uint32_t ring = 0, max_ctas = 0;
+  uint64_t ring_records = 0, idle_ns = 0;
+  uint64_t tiles = 0;  // out: ring slots (tiles) per frame
+};
 void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
                       const st_geom& g, uint32_t* labels, st_stats* stats, cudaStream_t s,
-                      int dev);                                                         // st_spec.cu
+                      int dev, SpecFrames* fr = nullptr);                             // st_spec.cu
 void forest_device_impl(st_forest* f, const float* x, uint64_t m, uint32_t a, uint64_t ld,
                         int layout, const st_geom& g, uint32_t* labels, cudaStream_t s);  // st_forest.cu
 }  // namespace sti

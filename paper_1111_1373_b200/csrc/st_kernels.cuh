@@ -1138,6 +1138,13 @@ struct SpecRingArgs {
   uint32_t n_slots;       // NS
   uint32_t ns_magic;      // floor(2^32 / NS): ticket -> (generation, slot) without a division
   uint32_t bulk_win;      // stage the window table with one cp.async.bulk (else per-thread loads)
+  // FR (frame stream, st_frames_* with the speculative algorithm): s.p.m
+  // records per frame in tpf tiles, frame f in slot f % ring (tensor-map rows
+  // from slot * frame_rows, labels from s.labels + slot * s.p.m), control
+  // words as DataArgs.fctl
+  uint32_t* fctl;
+  uint32_t ring, frame_rows;
+  uint64_t tpf, idle_ns;
   uint32_t tile_mult;     // host: records per ring slot / 32 (the kernel's RT); 0 = lane triples
   uint32_t triple;        // host: lane-triple slots of kTripleSlot (1) or 3/2 kTripleSlot (3) records
 };
@@ -1160,9 +1167,18 @@ struct SpecRingArgs {
 // source lane is 3g + (code & 3).  Lanes 30 / 31 mirror lanes 27 / 28 (same
 // addresses: broadcasts, no extra wavefronts).  80-record ring slots (8 per
 // group).
-template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false, int RT = 1, int SL = 0, int L3 = 0>
+// FR: the resident frame stream.  The CTA's tickets continue across frames
+// (tile G = blockIdx + ticket * grid of the endless frame sequence); a warp
+// waits for a ticket's frame to be published before touching its slot, and
+// a slot whose next tile lies in a frame not yet published is handed over
+// "deferred" (generation word bit 0): the warp that takes that ticket issues
+// its TMA itself.  Per frame visited a warp adds its walked-tile count to the
+// slot's completion counter (as k_data<FRAMES>).
+template <int A, bool WIN_SHARED, int STEPS, int SR, bool CW = false, int RT = 1, int SL = 0, int L3 = 0,
+          bool FR = false>
 __global__ void __launch_bounds__(kMaxThreads)
     k_spec_ring(const SpecRingArgs ra, const __grid_constant__ CUtensorMap tmap) {
+  static_assert(!FR || (SL == 3 && RT == 1), "frame stream: fixed-trip loop, one-chunk slots");
   static_assert(!CW || (WIN_SHARED && SR >= 1), "8-byte windows: shared table, window-loop paths");
   static_assert(!SL || SR == 0 || (SR == 2 && CW), "self-loop codes: one window, or two 8-byte-window streams");
   static_assert(SL < 2 || SR == 2, "branchy / fixed-trip stream loops: two-stream layout");
@@ -1216,6 +1232,43 @@ __global__ void __launch_bounds__(kMaxThreads)
     }
   };
 
+  // FR: frame of a tile, its tensor-map row, publication (lane 0 caches it)
+  uint32_t pub_known = 0, cur = 0xFFFFFFFFu, cnt = 0;
+  auto fr_published = [&](uint32_t f) -> bool {  // lane 0
+    if (f < pub_known) return true;
+    uint32_t pub;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(pub) : "l"(ra.fctl + kFPublished) : "memory");
+    if (pub > pub_known) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      pub_known = pub;
+    }
+    return f < pub_known;
+  };
+  auto fr_issue = [&](uint64_t jj, uint32_t b) {  // lane 0, frame published
+    const uint64_t G = tile_of(jj);
+    const uint32_t f = (uint32_t)(G / ra.tpf);
+    const uint32_t row = (f % ra.ring) * ra.frame_rows + (uint32_t)((G - (uint64_t)f * ra.tpf) * R * a_rt / 32u);
+    mbar_arrive_expect_tx(full0 + 8u * b, R * a_rt * 4u);
+    tma_load_2d(slots0 + b * args.stage_bytes, &tmap, 0, (int)row, full0 + 8u * b);
+  };
+  auto fr_try_fill = [&](uint64_t jj, uint32_t b) -> bool {  // lane 0
+    if (!fr_published((uint32_t)(tile_of(jj) / ra.tpf))) return false;
+    fr_issue(jj, b);
+    return true;
+  };
+  auto flush_count = [&]() {
+    if (cnt) {
+      __threadfence();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(reinterpret_cast<uint64_t*>(ra.fctl + kFDone) +
+                                                                        cur % ra.ring),
+                     "l"((uint64_t)cnt)
+                     : "memory");
+      cnt = 0;
+    }
+  };
+
   if (threadIdx.x == 0) {
     for (uint32_t b = 0; b < NS; ++b) {
       mbar_init(full0 + 8u * b, 1);
@@ -1230,8 +1283,14 @@ __global__ void __launch_bounds__(kMaxThreads)
     }
   }
   __syncthreads();
-  if (warp == 0)
+  if constexpr (FR) {
+    // generation words: gen << 1 | deferred (the taker of that ticket issues the TMA)
+    if (warp == 0 && lane == 0)
+      for (uint32_t b = 0; b < NS; ++b)
+        if (!fr_try_fill(b, b)) asm volatile("st.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(1u) : "memory");
+  } else if (warp == 0) {
     for (uint64_t jj = 0; jj < NS && jj < my_tiles; ++jj) fill(jj, (uint32_t)jj);
+  }
   // window table staged while the first tiles are in flight
   if constexpr (WIN_SHARED) {
     if (!ra.bulk_win) {
@@ -1308,8 +1367,47 @@ __global__ void __launch_bounds__(kMaxThreads)
     uint32_t tk = 0;
     if (lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(tk) : "r"(ticket) : "memory");
     tk = __shfl_sync(0xffffffffu, tk, 0);
-    if (tk >= my_tiles) break;
-    const uint64_t t = tile_of(tk);
+    uint64_t t;
+    uint32_t* labels = args.labels;
+    if constexpr (FR) {
+      const uint64_t Gt = tile_of(tk);
+      const uint32_t f = (uint32_t)(Gt / ra.tpf);
+      t = Gt - (uint64_t)f * ra.tpf;
+      if (f != cur) {  // this warp's tiles of the previous frame are walked: count them
+        flush_count();
+        cur = f;
+      }
+      labels = args.labels + (uint64_t)(f % ra.ring) * m;
+      // the ticket's frame must be out (or the stream closed before it / idle)
+      uint32_t ok = 1;
+      if (lane == 0 && !fr_published(f)) {
+        uint64_t t0 = global_ns();
+        uint32_t seen = pub_known;
+        while (!fr_published(f)) {
+          if (pub_known != seen) {
+            seen = pub_known;
+            t0 = global_ns();
+          }
+          uint32_t closed;
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(closed) : "l"(ra.fctl + kFClosed) : "memory");
+          if (closed <= f) {
+            ok = 0;
+            break;
+          }
+          if (global_ns() - t0 > ra.idle_ns) {
+            atomicOr(ra.fctl + kFError, 1u);
+            ok = 0;
+            break;
+          }
+          __nanosleep(256);
+        }
+      }
+      if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+      ++cnt;
+    } else {
+      if (tk >= my_tiles) break;
+      t = tile_of(tk);
+    }
     const uint64_t r0 = t * (uint64_t)R;
     uint32_t gen, b;
     divmod_ns(tk, gen, b);
@@ -1325,7 +1423,15 @@ __global__ void __launch_bounds__(kMaxThreads)
     // so plain volatile shared accesses suffice.
     // Every lane polls the same word (one broadcast wavefront, warp-uniform
     // exit): no divergent lane-0 section before the walk's shuffles.
-    {
+    if constexpr (FR) {
+      uint32_t have;
+      do {
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(have) : "r"(gen0 + 4u * b) : "memory");
+      } while (__any_sync(0xffffffffu, (have >> 1) < gen));
+      // handed over deferred: the frame was not out when the slot was freed
+      if (have == ((gen << 1) | 1u) && lane == 0) fr_issue(tk, b);
+      __syncwarp();
+    } else {
       uint32_t have;
       do {
         asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(have) : "r"(gen0 + 4u * b) : "memory");
@@ -1766,7 +1872,12 @@ __global__ void __launch_bounds__(kMaxThreads)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the TMA refill
     __syncwarp();
-    if (tk + NS < my_tiles) {
+    if constexpr (FR) {
+      if (lane == 0) {  // refill now if the next tile's frame is out, else hand over deferred
+        const uint32_t w = ((gen + 1u) << 1) | (fr_try_fill(tk + NS, b) ? 0u : 1u);
+        asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(w) : "memory");
+      }
+    } else if (tk + NS < my_tiles) {
       fill(tk + NS, b);  // this warp freed slot b: refill it ...
       if (lane == 0)  // ... and publish that generation tk / NS + 1 is on its way
         asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(gen0 + 4u * b), "r"(gen + 1u) : "memory");
@@ -1778,11 +1889,12 @@ __global__ void __launch_bounds__(kMaxThreads)
         uint32_t code;
         asm volatile("ld.shared.u32 %0, [%1];" : "=r"(code) : "r"(lbuf + 4u * rr));
         const uint32_t cls = ((code & args.lab_mask) >> args.lab_shift) - args.lab_sub;
-        args.labels[r0 + rr] = args.leaf_class ? __ldg(args.leaf_class + cls) : cls;
+        labels[r0 + rr] = args.leaf_class ? __ldg(args.leaf_class + cls) : cls;
       }
     }
     __syncwarp();
   }
+  if constexpr (FR) flush_count();
 }
 
 // ---------------------------------------------------------------------------

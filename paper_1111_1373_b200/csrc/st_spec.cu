@@ -224,8 +224,36 @@ void eval_spec_exact_cta(st_tree* t, const float* x, uint64_t m, uint32_t a, uin
   if (global_bufs) CK(cudaFreeAsync(ea.gbuf, s));
 }
 
+// The resident frame stream with the speculative kernel (st_frames.cu): the
+// fixed-trip ring loop (G = 4 three-node windows, 8-byte self-loop tables)
+// in k_spec_ring<..., FR = true>.
+template <int A, int L3>
+static void launch_spec_frames_k(const SpecRingArgs& ra, const Staging& stg, size_t smem, int dev,
+                                 uint32_t warps, uint32_t max_ctas, cudaStream_t s) {
+  auto fn = k_spec_ring<A, true, 1, 2, true, 1, 3, L3, true>;
+  int blocks = blocks_for((const void*)fn, smem, dev, 0, ra.tpf * warps, warps);
+  if (max_ctas) blocks = std::min<int>(blocks, (int)max_ctas);
+  clear_stale_error();
+  fn<<<blocks, warps * 32, smem, s>>>(ra, stg.tmap);
+  check_launch();
+}
+
+static void launch_spec_frames(uint32_t a, uint32_t triple, const SpecRingArgs& ra, const Staging& stg, size_t smem,
+                               int dev, uint32_t warps, uint32_t max_ctas, cudaStream_t s) {
+  if (a == 8 && triple == 3) return launch_spec_frames_k<8, 3>(ra, stg, smem, dev, warps, max_ctas, s);
+  if (a == 8 && triple == 1) return launch_spec_frames_k<8, 1>(ra, stg, smem, dev, warps, max_ctas, s);
+  if (a == 8 && triple == 0) return launch_spec_frames_k<8, 0>(ra, stg, smem, dev, warps, max_ctas, s);
+  if (a == 16 && triple == 1) return launch_spec_frames_k<16, 1>(ra, stg, smem, dev, warps, max_ctas, s);
+  if (a == 16 && triple == 0) return launch_spec_frames_k<16, 0>(ra, stg, smem, dev, warps, max_ctas, s);
+  if (a == 32 && triple == 0) return launch_spec_frames_k<32, 0>(ra, stg, smem, dev, warps, max_ctas, s);
+  fail(ST_ERR_ARGUMENT, "speculative frame stream: no kernel for this arity / slot layout");
+}
+
 void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64_t ld, int layout,
-                      const st_geom& g, uint32_t* labels, st_stats* stats, cudaStream_t s, int dev) {
+                      const st_geom& g, uint32_t* labels, st_stats* stats, cudaStream_t s, int dev,
+                      SpecFrames* fr) {
+  if (fr && (stats || t->info.internal <= 32))
+    fail(ST_ERR_ARGUMENT, "speculative frame streams need a multi-window tree (> 32 internal nodes) and no counters");
   if (stats && t->info.internal > 32) {
     // counters are defined by whole-tree speculation (the reference law)
     return eval_spec_exact_cta(t, x, m, a, ld, layout, g.reductions, labels, stats, s, dev);
@@ -425,6 +453,22 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       // one window: ballot + leaf path masks unless pointer jumping is asked
       // for (pm_off then names the self-loop entries, or 0: select per step)
       if (onewin) ra.s.pm_off = (g.variant & ST_VAR_SPEC_JUMP) ? (sl ? wt->sl1_off : 0u) : wt->pm_off;
+      if (fr) {
+        if (!(cw && sl == 3 && sr >= 2 && rt <= 1 && ra.s.smax == 1 && (a == 8 || a == 16 || a == 32)))
+          fail(ST_ERR_ARGUMENT, "speculative frame stream needs the fixed-trip window loop (G = 4 windows, "
+                                "8-byte self-loop tables, 8 / 16 / 32 attributes)");
+        if (m % slot_recs != 0)
+          fail(ST_ERR_ARGUMENT, "records per frame must be a multiple of " + std::to_string(slot_recs) +
+                                    " (whole speculative ring slots per frame)");
+        make_tmap(rstg, x, fr->ring_records, a, (uint32_t)slot_recs);
+        ra.fctl = fr->fctl;
+        ra.ring = fr->ring;
+        ra.frame_rows = (uint32_t)(m * a / 32);
+        ra.tpf = m / slot_recs;
+        ra.idle_ns = fr->idle_ns;
+        fr->tiles = ra.tpf;
+        return launch_spec_frames(a, triple, ra, rstg, rsmem, dev, warps, fr->max_ctas, s);
+      }
       switch (ct_arity(a) ? a : 0) {
         case 8: return launch_spec_ring<8>(ws, sr, cw, sl, ra, rstg, rsmem, dev, warps, s);
         case 16: return launch_spec_ring<16>(ws, sr, cw, sl, ra, rstg, rsmem, dev, warps, s);
@@ -434,6 +478,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
       }
     }
   }
+  if (fr) fail(ST_ERR_ARGUMENT, "speculative frame stream needs the TMA-staged ring kernel");
   if (stg.loader == kTma && ct_arity(a)) {
     switch (a) {
       case 8: return launch_spec_t<8, kTma>(win_shared, sa, stg, smem, dev, bps, s);

@@ -44,6 +44,33 @@ def test_frames_push_pop(cuda, co, depth, leaves, a, records, ring, geom):
         assert fs.status() == (len(frames), False)
 
 
+@pytest.mark.parametrize("depth,leaves,a,records,ring,geom", [
+    (12, 2048, 8, 120 * 500, 3, None),                     # C3-shaped tree: lane triples, 120-record slots
+    (12, 4096, 16, 80 * 400, 2, None),                     # lane triples, 80-record slots
+    (24, 256, 32, 32 * 1000, 2, None),                     # skewed tree, 4-lane groups (early exit)
+    (12, 2048, 8, 80 * 300, 1, st.GpuGeom(algo="speculative", slot_records=2)),
+    (14, 4096, 8, 32 * 900, 4, st.GpuGeom(algo="speculative", variant=("spec_quad",))),
+])
+def test_frames_speculative(cuda, co, depth, leaves, a, records, ring, geom):
+    """The speculative ring as a resident frame stream (deferred slot
+    hand-over across frame boundaries): every frame = the oracle."""
+    g = geom or st.GpuGeom(algo="speculative")
+    nodes = co.gen_tree(depth, leaves, a, 8, 800 + depth)
+    frames = _frames(co, 2 * ring + 3, records, a, 950 + a)
+    want = [co.eval_serial(nodes, f) for f in frames]
+    with st.FrameStream(nodes, records, a, ring=ring, geom=g, idle_timeout_ms=20000) as fs:
+        pending = []
+        for k, f in enumerate(frames):
+            if len(pending) == ring:
+                s0 = pending.pop(0)
+                assert np.array_equal(fs.pop(s0), want[s0]), (s0, depth, a)
+            pending.append(fs.push(f))
+        for s0 in pending:
+            assert np.array_equal(fs.pop(s0), want[s0]), (s0, depth, a)
+    with pytest.raises(st.ArgumentError):  # one-window trees (<= 32 internal nodes) have no window loop
+        st.FrameStream(co.gen_tree(5, 16, a, 8, 1), records, a, geom=g)
+
+
 def test_frames_device_producer(cuda, co):
     """Stream-ordered protocol: a torch stream writes each frame into its
     slot, publishes it; another stream waits for the labels and copies them."""

@@ -85,8 +85,7 @@ def test_frame_stream_argument_errors_before_device(co):
     for args, kw, msg in [((4096, 19), {}, "8, 16 or 32 attributes"),
                           ((0, 16), {}, "records per frame"),
                           ((4096, 16), {"ring": 0}, "ring must hold"),
-                          ((4096, 8), {}, "reads attribute"),
-                          ((4096, 16), {"geom": st.GpuGeom(algo="speculative")}, "data-decomposition")]:
+                          ((4096, 8), {}, "reads attribute")]:
         with pytest.raises(st.ArgumentError, match=msg):
             st.FrameStream(nodes, *args, **kw)
 
