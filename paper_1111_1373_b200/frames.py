@@ -1,7 +1,8 @@
 """Resident frame-stream evaluation (``st_frames_*``, include/spectree_b200.h).
 
-One data-decomposition grid stays resident on the GPU and classifies frame 0,
-1, 2, ... as they are published into a device ring of frame slots -- the C3
+One data-decomposition grid (or, with ``GpuGeom(algo="speculative")``, the
+speculative ring) stays resident on the GPU and classifies frame 0, 1, 2, ...
+as they are published into a device ring of frame slots -- the C3
 per-pixel segmentation workload at video rate without a launch, a tree
 staging or a pipeline ramp-up per frame.  Labels equal ``eval_gpu``'s for
 every frame (the reference's ``eval_serial``, eval_serial.cpp:33-41).
@@ -11,6 +12,10 @@ Host producers::
     with FrameStream(tree, records=1920 * 1080, arity=8, ring=4) as fs:
         seq = fs.push(frame)          # (records, 8) float32
         labels = fs.pop(seq)          # (records,) uint32
+
+While a stream is open its grid stays resident: device-wide synchronisation
+(``torch.cuda.synchronize()``, ``cudaFree`` -- including a tree or forest
+being destroyed) waits until ``close()``.  Synchronise streams instead.
 
 Device producers (stream-ordered, no SM time for the synchronisation)::
 
@@ -98,10 +103,16 @@ class FrameStream:
         return pub.value, bool(stop.value)
 
     def close(self) -> None:
-        """Walk every published frame, stop the resident grid, free the ring."""
+        """Walk every published frame, stop the resident grid, free the ring.
+        The tree reference is dropped here too: a tree destroyed later (its
+        device tables freed by cudaFree, which waits for every resident grid)
+        could otherwise stall behind the next frame stream."""
         if self._h is not None:
             h, self._h = self._h, None
-            _check(_lib.load().st_frames_close(h))
+            try:
+                _check(_lib.load().st_frames_close(h))
+            finally:
+                self.tree = None
 
     def _live(self):
         if self._h is None:

@@ -71,6 +71,23 @@ def test_frames_speculative(cuda, co, depth, leaves, a, records, ring, geom):
         st.FrameStream(co.gen_tree(5, 16, a, 8, 1), records, a, geom=g)
 
 
+def test_frames_back_to_back_streams(cuda, co):
+    """Streams opened one after another over a plain node array, the
+    variable rebound while the next grid is resident: close() drops the
+    tree, so its cudaFree does not stall behind the next stream (which would
+    run into the idle timeout)."""
+    nodes = co.gen_tree(12, 2048, 8, 8, 301)
+    for algo in ("data", "speculative", "data", "speculative"):
+        rec = 128 * 64 if algo == "data" else 120 * 64
+        frames = _frames(co, 3, rec, 8, 77)
+        with st.FrameStream(nodes, rec, 8, ring=2, geom=st.GpuGeom(algo=algo), idle_timeout_ms=5000) as fs:
+            s0, s1 = fs.push(frames[0]), fs.push(frames[1])
+            assert np.array_equal(fs.pop(s0), co.eval_serial(nodes, frames[0])), algo
+            s2 = fs.push(frames[2])
+            assert np.array_equal(fs.pop(s1), co.eval_serial(nodes, frames[1])), algo
+            assert np.array_equal(fs.pop(s2), co.eval_serial(nodes, frames[2])), algo
+
+
 def test_frames_device_producer(cuda, co):
     """Stream-ordered protocol: a torch stream writes each frame into its
     slot, publishes it; another stream waits for the labels and copies them."""

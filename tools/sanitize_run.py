@@ -25,16 +25,18 @@ bad = 0
 if "--frames" in sys.argv:
     # the resident frame stream: 3 frames through a 2-slot ring, labels vs the oracle
     nodes = co.gen_tree(12, 2048, 8, 8, 301)
-    frames = [co.gen_dataset(8192, 8, 50 + k) for k in range(3)]
-    with st.FrameStream(nodes, 8192, 8, ring=2, idle_timeout_ms=120000) as fs:
-        seqs = []
-        for k, f in enumerate(frames):
-            if len(seqs) == 2:
-                s0 = seqs.pop(0)
+    frames = [co.gen_dataset(7680, 8, 50 + k) for k in range(3)]  # whole 128- and 120-record tiles
+    for algo in ("data", "speculative"):
+        print("frames", algo, flush=True)
+        with st.FrameStream(nodes, 7680, 8, ring=2, geom=st.GpuGeom(algo=algo), idle_timeout_ms=1200000) as fs:
+            seqs = []
+            for k, f in enumerate(frames):
+                if len(seqs) == 2:
+                    s0 = seqs.pop(0)
+                    bad += not np.array_equal(fs.pop(s0), co.eval_serial(nodes, frames[s0]))
+                seqs.append(fs.push(f))
+            for s0 in seqs:
                 bad += not np.array_equal(fs.pop(s0), co.eval_serial(nodes, frames[s0]))
-            seqs.append(fs.push(f))
-        for s0 in seqs:
-            bad += not np.array_equal(fs.pop(s0), co.eval_serial(nodes, frames[s0]))
     print("sanitize_run frames:", "ok" if bad == 0 else f"{bad} mismatches")
     sys.exit(1 if bad else 0)
 cases = [((24, 256, 32, 8, 201), 32), ((12, 2048, 8, 8, 301), 8), ((10, 1024, 16, 8, 101), 16),
