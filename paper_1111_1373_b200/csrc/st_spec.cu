@@ -137,7 +137,11 @@ void launch_spec_t(bool win_shared, const SpecArgs& sa, const Staging& stg, size
   return launch_spec_steps<A, LOADER, false>(sa, stg, smem, dev, bps, s);
 }
 
-constexpr uint32_t kRingExtra = 4;  // speculative ring: tile slots beyond one per warp
+// speculative ring: tile slots beyond one per warp -- few where the walk is
+// shared-memory bound (lane triples: a slot fewer buys a resident warp),
+// more where the ring streams at HBM speed (one-window ballot, C2's 4-lane
+// groups: more tiles in flight)
+constexpr uint32_t kRingExtraTriple = 4, kRingExtra = 12;
 
 // Lane triples apply to the fixed-trip loop over G = 4 three-node windows
 // with TMA-staged records inside one 128-byte row.
@@ -314,7 +318,7 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
                       (size_t)stg.warps * 3 * 128;  // + per-warp label/counter rows
   const uint32_t bps = g.blocks_per_sm;  // speculative is latency-bound: keep every resident CTA
   // CTA-shared ring (default for the fast path): up to 32 warps on one SM
-  // share NS = warps + kRingExtra tile slots.
+  // share NS = warps + 4 (lane triples) or + 12 tile slots.
   if (stg.loader == kTma && !stats && g.pipeline != 1) {
     const bool onewin = wt->windows == 1 && win_shared && !(g.variant & ST_VAR_SPEC_GENERAL);
     SpecArgs rs = sa;
@@ -438,15 +442,17 @@ void eval_spec_device(st_tree* t, const float* x, uint64_t m, uint32_t a, uint64
     const size_t lb = 32 + 32 * 4 * slot_recs;  // generation padding + ticket + per-warp label rows (<= 32 warps)
     const size_t budget = pr.smem_optin - 1024 - rs.win_bytes - lb;
     const size_t max_slots = budget / (rstg.stage_bytes + 16u);
-    // warps + 4 slots: the slots beyond one per warp keep refills in flight
-    // while every warp walks a tile; each slot fewer buys a resident warp
-    // where shared memory binds (same-box A/B, profiles/r2_spec_ring_slots_ab.txt:
-    // C3 -4 %, C5 d16 / d20 -1.5 / -2.8 % vs warps + 12; +2 / +4 / +6 even)
-    const uint32_t warps = (uint32_t)std::min<size_t>(32, max_slots > kRingExtra ? max_slots - kRingExtra : 0);
+    // warps + extra slots: the slots beyond one per warp keep refills in
+    // flight while every warp walks a tile; each slot fewer buys a resident
+    // warp where shared memory binds (same-box A/B,
+    // profiles/r2_spec_ring_slots_ab.txt: lane triples with + 4 vs + 12: C3
+    // -4 %, C5 d16 / d20 -1.5 / -2.8 %; but the paper tree +5 %, C2 +1.3 %)
+    const uint32_t extra = triple ? kRingExtraTriple : kRingExtra;
+    const uint32_t warps = (uint32_t)std::min<size_t>(32, max_slots > extra ? max_slots - extra : 0);
     if (warps >= 4) {
       SpecRingArgs ra{};
       ra.s = rs;
-      ra.n_slots = (uint32_t)std::min<size_t>(max_slots, warps + kRingExtra);
+      ra.n_slots = (uint32_t)std::min<size_t>(max_slots, warps + extra);
       // stress knob: any ring depth >= 1 must give exact labels
       if (g.ring_slots) ra.n_slots = std::min<uint32_t>(ra.n_slots, g.ring_slots);
       ra.ns_magic = (uint32_t)std::min<uint64_t>(0xFFFFFFFFull, (1ull << 32) / ra.n_slots);
